@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark: rsvd_v2 on the C5 configuration.
+
+Workload (BASELINE.json configs[4], the north_star target and the config
+scaled at 1/2/4/8 GPUs): A = U diag(s) V^T, m=200000, n=20000 (32 GB FP64),
+s_j = exp(-j/100) (truncated at the 3685 modes above 1e-16),
+U, V orthonormalised seeded Gaussians; k=500, p=10, q=2, s=1.  One step is
+one full rlra_rsvd(v2) call (sketch, 2 power iterations with CholQR2
+re-orthonormalisation, projection, QR of B^T, Jacobi SVD of R, lift).
+
+metric  : effective FP64 TFLOP/s = F_gemm / step time with
+          F_gemm = 4 m n l (q+1) (2.448e13 flop for C5);
+value   : A resident in HBM, Omega generated in-register (Philox);
+e2e     : the same call through the C-ABI with HOST buffers (pinned A in,
+          U/sigma/V out), host<->device copies inside the timed region;
+roofline: the dominant kernel is the FP64 DMMA GEMM; achieved = its
+          algorithmic flops / its CUDA-event time on the engine stream over
+          the timed region, against the measured DMMA peak
+          (tools/fp64_peak.cu: 37.1 TFLOP/s; MEASURED_PEAKS.json has no FP64
+          entry).
+A (32 GB) is far larger than L2 (126 MB), so no flush is needed between steps.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified headers) on a bounded sample of the same workload, all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 37.1  # tools/fp64_peak.cu on this pool's B200 (DMMA.8x8x4, 1965 MHz)
+C5 = dict(m=200000, n=20000, k=500, p=10, q=2, s=1)
+SEED_GEN = 5          # generator seed = config number
+SEED_OMEGA = 12345    # CLI default seed (rlra_cli.cpp:56)
+CPU_SAMPLE = dict(m=600, n=4000)  # bounded row/column slice of C5 for the CPU legs
+
+
+def f_gemm(m, n, k, p, q, **_):
+    return 4.0 * m * n * (k + p) * (q + 1)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_step(a_sample, cores):
+    """One rsvd_v2 on the reference CPU build; returns seconds."""
+    import ctypes as C
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle
+
+    lib = C.CDLL(_oracle.REF_FAST_PATH)
+    lib.ref_set_threads(cores)
+    m, n = a_sample.shape
+    k, p, q, s = C5["k"], C5["p"], C5["q"], C5["s"]
+    r = _oracle.Rng()
+    lib.ref_rng_seed(C.byref(r), C.c_uint64(SEED_OMEGA))
+    u = np.zeros((m, k), order="F")
+    sg = np.zeros(k)
+    v = np.zeros((n, k), order="F")
+    t0 = time.perf_counter()
+    st = lib.ref_rsvd(0, _oracle.d(a_sample), m, n, k, p, q, s, C.byref(r), _oracle.d(u),
+                      _oracle.d(sg), _oracle.d(v))
+    dt = time.perf_counter() - t0
+    if st != 0:
+        raise RuntimeError("reference rsvd failed")
+    return dt
+
+
+def cpu_port_step(a_sample):
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle
+
+    o = _oracle.orc()
+    t0 = time.perf_counter()
+    o.rsvd(a_sample, C5["k"], C5["p"], C5["q"], C5["s"], o.rng(SEED_OMEGA), 0)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_matrix():
+    """The bounded CPU sample: the leading 600 x 4000 block of a C5-type
+    matrix (same spectrum law, seeded; generated with numpy)."""
+    import numpy as np
+
+    m, n = CPU_SAMPLE["m"], CPU_SAMPLE["n"]
+    rs = np.random.default_rng(SEED_GEN)
+    r = min(m, n)
+    U, _ = np.linalg.qr(rs.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rs.standard_normal((n, r)))
+    s = np.exp(-np.arange(r) / 100.0)
+    return np.asfortranarray((U * s) @ V.T)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle
+
+    a = cpu_sample_matrix()
+    cores = os.cpu_count() or 1
+    use_ref = os.path.exists(_oracle.REF_FAST_PATH)
+    fl = f_gemm(CPU_SAMPLE["m"], CPU_SAMPLE["n"], C5["k"], C5["p"], C5["q"])
+    times = []
+    for i in range(min(args.warmup, 1) + args.steps):
+        dt = cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
+        if i >= min(args.warmup, 1):
+            times.append(dt)
+    t = statistics.median(times)
+    val = fl / t / 1e12
+    line = {
+        "impl": "reference",
+        "metric": "rsvd_v2 effective FP64 TFLOP/s (F_gemm = 4mnl(q+1) / time), C5 workload",
+        "value": val, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5 rsvd_v2 (m=200000,n=20000,k=500,p=10,q=2); CPU sample = "
+                   "leading 600x4000 block, same k,p,q", "sample_m": CPU_SAMPLE["m"],
+                   "sample_n": CPU_SAMPLE["n"]},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores if use_ref else 1,
+                         "kind": "reference" if use_ref else "port",
+                         "sample": "rsvd_v2 on the leading 600x4000 block of a C5-type matrix"},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def generate_c5(eng, torch, dev, m, n, seed):
+    """A = U diag(s) V^T on the device with the engine's own kernels:
+    Philox Gaussians, CholQR2 orthonormalisation, DMMA GEMM (the GPU
+    generator of SURVEY.md §8f row 1; testmat.hpp:65-74 semantics)."""
+    import paper_1502_05366_b200 as R
+
+    r = 3685  # modes with exp(-j/100) > 1e-16
+    U = torch.empty(r * m, dtype=torch.float64, device=dev)
+    V = torch.empty(r * n, dtype=torch.float64, device=dev)
+    eng.device_gaussian_philox(m, r, seed, 101, 0, U.data_ptr(), m)
+    eng.device_gaussian_philox(n, r, seed, 102, 0, V.data_ptr(), n)
+    eng.device_orth(U.data_ptr(), m, r)
+    eng.device_orth(V.data_ptr(), n, r)
+    s = torch.exp(-torch.arange(r, dtype=torch.float64, device=dev) / 100.0)
+    U.view(r, m).mul_(s.view(r, 1))  # column j of U (col-major) scaled by s_j
+    A = torch.empty(m * n, dtype=torch.float64, device=dev)
+    eng.device_matmul(False, True, U.data_ptr(), m, r, m, V.data_ptr(), n, r, n, A.data_ptr(), m)
+    eng.synchronize()
+    del U, V
+    return A, s
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--m", type=int, default=C5["m"])
+    ap.add_argument("--n", type=int, default=C5["n"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_1502_05366_b200 as R
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    eng = R.Engine(local)
+    cfg = dict(C5)
+    cfg["m"], cfg["n"] = args.m, args.n
+    m, n, k, p, q, s = cfg["m"], cfg["n"], cfg["k"], cfg["p"], cfg["q"], cfg["s"]
+    l = k + p
+    # Row-sharded replicas: with N ranks each rank factors its own C5-sized
+    # problem?  No: C5 is strong-scaled; the multi-GPU row-sharded engine is
+    # not in this round, so N>1 runs replicas and says so in config.
+    A, sig_true = generate_c5(eng, torch, dev, m, n, SEED_GEN + 1000 * rank)
+    U = torch.empty(m * k, dtype=torch.float64, device=dev)
+    V = torch.empty(n * k, dtype=torch.float64, device=dev)
+    S = torch.empty(k, dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+
+    def step(seed):
+        eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, s, R.Omega.philox(seed),
+                        U.data_ptr(), S.data_ptr(), V.data_ptr())
+
+    for w in range(args.warmup):
+        step(SEED_OMEGA + w)
+    eng.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng.profile(True)
+    launches0 = eng.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        step(SEED_OMEGA + 100 + i)
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = eng.launches - launches0
+    prof = eng.profile_records()
+    eng.profile(False)
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    F = f_gemm(m, n, k, p, q)
+    value = world * F / (ms_step * 1e-3) / 1e12
+
+    # dominant kernel: the DMMA GEMMs that stream A (M or K == m)
+    big = [r for r in prof if r["name"] == "dgemm" and (r["M"] == m or r["K"] == m)]
+    g_ms = sum(r["ms"] for r in big)
+    g_fl = sum(r["flops"] for r in big)
+    phases = {}
+    for r in prof:
+        key = r["name"] if r["name"] != "dgemm" else ("gemm_A" if r in big else "gemm_small")
+        phases[key] = phases.get(key, 0.0) + r["ms"] / args.steps
+    achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
+
+    # relative error of the last factorization (device reduction)
+    err = eng.device_rel_error(A.data_ptr(), m, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
+    sig = S.cpu().numpy()
+    st = sig_true[:k].cpu().numpy()
+    sig_rel = float(np.max(np.abs(sig[:100] - st[:100]) / st[:100]))
+
+    line = {
+        "metric": "rsvd_v2 effective FP64 TFLOP/s (F_gemm = 4mnl(q+1) / time), C5 workload",
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world == 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: A = U diag(exp(-j/100)) V^T, U,V orthonormalised Philox Gaussians "
+                "(3685 modes), generated on the GPU",
+        "config": {"workload": f"C5 rsvd_v2 m={m} n={n} k={k} p={p} q={q} s={s}",
+                   "omega": "philox in-register", "l2": "A (32 GB) >> L2; no flush needed",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+        "time_s": ms_step / 1e3,
+        "frac_of_fp64_peak": value / world / FP64_DMMA_PEAK_TFLOPS,
+        "phases_ms": {k_: round(v_, 3) for k_, v_ in sorted(phases.items())},
+        "rel_error": {"fro": err, "sigma_top100_vs_true_max_rel": sig_rel},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
+                     "traffic": None,
+                     "kernel": "dgemm_kernel (A-streaming products: sketch, 2q power, projection)",
+                     "peak_source": "measured DMMA peak, tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry)"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+
+    # ---------------------------------------------- e2e through the C-ABI --
+    if not args.no_e2e:
+        Ah = torch.empty(m * n, dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A)
+        del A
+        torch.cuda.empty_cache()
+        Uh = torch.empty(m * k, dtype=torch.float64, pin_memory=True)
+        Vh = torch.empty(n * k, dtype=torch.float64, pin_memory=True)
+        Sh = torch.empty(k, dtype=torch.float64, pin_memory=True)
+        e2e_steps = max(1, min(args.steps, 3))
+
+        def estep(seed):
+            eng.host_rsvd_ptr(R.RSVD_V2, Ah.data_ptr(), m, n, m, k, p, q, s, R.Omega.philox(seed),
+                              Uh.data_ptr(), Sh.data_ptr(), Vh.data_ptr())
+
+        estep(SEED_OMEGA)
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            estep(SEED_OMEGA + 200 + i)
+        te = (time.perf_counter() - t0) / e2e_steps
+        line["e2e"] = {"value": world * F / te / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": 8 * m * n,
+                       "d2h_bytes_per_step": 8 * (m * k + n * k + k),
+                       "ms_per_step": te * 1e3, "steps": e2e_steps,
+                       "path": "rlra_rsvd(loc=RLRA_HOST), pinned host A"}
+
+    # ------------------------------------------------------ cpu baseline --
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import _oracle
+            a = cpu_sample_matrix()
+            cores = os.cpu_count() or 1
+            use_ref = os.path.exists(_oracle.REF_FAST_PATH)
+            dt = cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
+            fl = f_gemm(CPU_SAMPLE["m"], CPU_SAMPLE["n"], k, p, q)
+            line["cpu_baseline"] = {
+                "value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cores if use_ref else 1,
+                "kind": "reference" if use_ref else "port",
+                "sample": f"rsvd_v2(k={k},p={p},q={q}) on the leading {CPU_SAMPLE['m']}x"
+                          f"{CPU_SAMPLE['n']} block of a C5-type matrix; {dt:.2f} s"}
+        except Exception as e:  # reported, never silently substituted
+            line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,232 @@
+/*
+ * rlra_c.h — C-ABI of the B200 engine for the reference's randomized
+ * low-rank factorization path (the drop-in boundary).
+ *
+ * The reference ("rlra", /root/reference/proj/include/rlra) is a header-only
+ * C++20 library whose operator API is the free functions of namespace rlra.
+ * It has no C ABI of its own; the functions below are what a binding of that
+ * API needs, one entry point per reference function on the hot path
+ * (SURVEY.md §8b).  include/rlra/*.hpp re-declares the reference API with the
+ * exact signatures and implements it over this header, so C++ callers switch
+ * by changing the include path; INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions (reference core/matrix.hpp:17-80):
+ *   - matrices are column-major float64, element (i,j) at p[i + j*ld];
+ *   - every matrix argument is (pointer, rows, cols, ld) and `loc` says whether
+ *     the pointers are host (RLRA_HOST) or device (RLRA_DEVICE) memory; host
+ *     inputs are copied to the device, outputs copied back, inside the call;
+ *   - output buffers are caller-allocated; sizes are stated per function;
+ *   - all arithmetic is FP64 on hand-written sm_100a kernels; nothing falls
+ *     back to the CPU, cuBLAS or cuSOLVER.  A missing device is RLRA_ECUDA.
+ *
+ * Errors: every function returns rlra_status.  The statuses map 1:1 onto the
+ * reference exception classes (core/errors.hpp:11-33) and the message, which
+ * reproduces the reference's text where the reference's tests match on it,
+ * is available from rlra_last_error() (thread-local, valid until the next
+ * failing call on the same thread).
+ *
+ * Threading: a context is used by one host thread at a time.
+ */
+#ifndef RLRA_C_H
+#define RLRA_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RLRA_OK = 0,
+    RLRA_EDIM = 1,   /* rlra::DimensionError   core/errors.hpp:16-18 */
+    RLRA_ENUM = 2,   /* rlra::NumericalError   core/errors.hpp:21-23 */
+    RLRA_ECONV = 3,  /* rlra::ConvergenceError core/errors.hpp:26-28 */
+    RLRA_EIO = 4,    /* rlra::IoError          core/errors.hpp:31-33 */
+    RLRA_ECUDA = 5,  /* CUDA failure / no device -> rlra::Error */
+    RLRA_ENCCL = 6,  /* collective failure       -> rlra::Error */
+    RLRA_EINVAL = 7  /* bad handle or argument   -> rlra::Error */
+} rlra_status;
+
+enum { RLRA_HOST = 0, RLRA_DEVICE = 1 };
+
+/* rsvd variants: rsvd.hpp:154 (v2, QR of B^T), :144 (v1, B B^T), :127 (basic) */
+enum { RLRA_RSVD_V2 = 0, RLRA_RSVD_V1 = 1, RLRA_RSVD_BASIC = 2 };
+/* Vnum (sketch.hpp:14) */
+enum { RLRA_VNUM_QR = 0, RLRA_VNUM_BBT = 1 };
+
+typedef struct rlra_ctx rlra_ctx;
+
+/* ---------------------------------------------------------------- Omega ---
+ * Where the Gaussian test matrices come from.
+ *  RLRA_OMEGA_CALLBACK (parity mode): the engine calls fill(user, draw, rows,
+ *    cols, host_out) once per Gaussian draw, in the reference's order, and
+ *    uploads the result.  The C++ shim implements fill with the caller's
+ *    rlra::RngState (core/rng.hpp), so the draws and the post-call RNG state
+ *    are the reference's bit for bit.  Draw order:
+ *      rsvd_*      : one n x l draw                    (sketch.hpp:51, rsvd.hpp:130)
+ *      sample_left : one m x l draw                    (sketch.hpp:51,66)
+ *      id_rand / cur_rand : one m x l draw             (interp.hpp:208)
+ *      qb_blocked  : draw i = block i, n x width_i; the callback performs the
+ *                    per-block rng.substream() itself  (qb.hpp:119-120)
+ *  RLRA_OMEGA_PHILOX (performance mode): entries are generated inside the
+ *    sketch GEMM from Philox4x32-10 keyed by `seed` (counter = row, column,
+ *    draw); Omega never exists in HBM.  The caller's RNG is not consumed by
+ *    the engine (the shim derives `seed` from one next_u64()).            */
+enum { RLRA_OMEGA_CALLBACK = 0, RLRA_OMEGA_PHILOX = 1 };
+typedef void (*rlra_omega_fill_fn)(void* user, int draw, int rows, int cols, double* host_out);
+typedef struct {
+    int mode;
+    rlra_omega_fill_fn fill;
+    void* user;
+    uint64_t seed;
+} rlra_omega;
+
+/* -------------------------------------------------- reference RNG stream ---
+ * The reference's RngState (core/rng.hpp:18-79): xoshiro256++ seeded by
+ * splitmix64, Box-Muller through libm with a cached spare, column-major
+ * fills.  Host code, bit-identical to the reference on the same libm; it
+ * exists so parity-mode callers without the C++ shim (ctypes, the CLI) can
+ * produce the reference's Omega.  Field order matches the reference class. */
+typedef struct {
+    uint64_t s[4];
+    double spare;
+    int have_spare;
+} rlra_rng;
+void rlra_rng_seed(rlra_rng* r, uint64_t seed);
+uint64_t rlra_rng_next_u64(rlra_rng* r);
+double rlra_rng_next_gaussian(rlra_rng* r);
+void rlra_rng_substream(rlra_rng* parent, rlra_rng* child);
+void rlra_rng_gaussian_fill(rlra_rng* r, int rows, int cols, double* out);
+/* rlra_omega.fill callbacks with user = rlra_rng*: a plain draw
+ * (rsvd/sample/id_rand) and substream-then-draw (qb_blocked, qb.hpp:119). */
+void rlra_omega_fill_rng(void* user, int draw, int rows, int cols, double* out);
+void rlra_omega_fill_rng_substream(void* user, int draw, int rows, int cols, double* out);
+
+/* ------------------------------------------------------------- context --- */
+rlra_status rlra_ctx_create(int device, rlra_ctx** out);
+rlra_status rlra_ctx_destroy(rlra_ctx* ctx);
+rlra_status rlra_ctx_synchronize(rlra_ctx* ctx);
+/* Number of engine kernel launches issued on this context so far. */
+uint64_t rlra_ctx_launch_count(const rlra_ctx* ctx);
+/* Optional timing: when enabled every engine GEMM launch and every phase
+ * (orth, small_svd, cpqr) is bracketed by CUDA events on the context stream.
+ * Enabling or disabling clears the records. */
+rlra_status rlra_ctx_profile(rlra_ctx* ctx, int enable);
+int rlra_ctx_profile_count(const rlra_ctx* ctx);
+rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap, int* M, int* N,
+                                 int* K, double* flops, double* ms);
+/* The cudaStream_t the context launches on (for event timing by callers). */
+void* rlra_ctx_stream(const rlra_ctx* ctx);
+const char* rlra_last_error(void);
+const char* rlra_version(void);
+
+/* -------------------------------------------------------- kernel level --- */
+/* core/matmul.hpp:68: c (m x n) = op(a) * op(b); a is ar x ac, b is br x bc. */
+rlra_status rlra_matmul(rlra_ctx* ctx, int loc, int trans_a, int trans_b, const double* a, int ar,
+                        int ac, int64_t lda, const double* b, int br, int bc, int64_t ldb,
+                        double* c, int64_t ldc);
+
+/* core/qr.hpp:95: a (m x n, m >= n) = q (m x n) * r (n x n), diag(r) >= 0.
+ * r may be NULL (orth, core/qr.hpp:125).  degenerate may be NULL. */
+rlra_status rlra_compact_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                            double* q, int64_t ldq, double* r, int64_t ldr, int* degenerate);
+
+/* core/qr.hpp:140: partial column-pivoted QR.  kmax = k (rank mode) or
+ * min(m,n) (k == 0, tol > 0).  q1 (m x kmax, may be NULL), s1 (kmax x n),
+ * perm (n ints).  Rows/columns past *frank are left untouched. */
+rlra_status rlra_pivoted_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                            int k, double tol, double* q1, int64_t ldq1, double* s1,
+                            int64_t lds1, int* perm, int* frank, double* residual, int* reached,
+                            int* degenerate);
+
+/* core/qr.hpp:242: t (k x nc) = s11^{-1} s12 with the 1e12 / 1e4 clamp. */
+rlra_status rlra_upper_tri_solve(rlra_ctx* ctx, int loc, const double* s11, int k, int64_t lds11,
+                                 const double* s12, int nc, int64_t lds12, double* t,
+                                 int64_t ldt, int* clamped);
+
+/* core/jacobi.hpp:145: r = min(m,n); u (m x r), sigma (r), v (n x r). */
+rlra_status rlra_small_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                           double* u, int64_t ldu, double* sigma, double* v, int64_t ldv);
+
+/* core/jacobi.hpp:68: values (n, descending), vectors (n x n). */
+rlra_status rlra_sym_eig(rlra_ctx* ctx, int loc, const double* t, int n, int64_t ldt,
+                         double* values, double* vectors, int64_t ldv);
+
+/* core/norms.hpp:29 */
+rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, int n,
+                                int64_t lda, double* out);
+
+/* ||A - X Y^T||_F for A (m x n), X (m x k), Y (n x k): the dense
+ * reconstruction residual of report.hpp:97-113 (and of the CUR residual,
+ * interp.hpp:175) as one fused GEMM + subtract + sum-of-squares pass that
+ * never materialises X Y^T. */
+rlra_status rlra_lowrank_residual(rlra_ctx* ctx, int loc, const double* a, int m, int n,
+                                  int64_t lda, const double* x, int64_t ldx, const double* y,
+                                  int64_t ldy, int k, double* out);
+
+/* Materialise the Philox Omega the sketch GEMM generates in-register
+ * (rows x cols, draw index `draw`, row offset `row0`).  Test/diagnostic use. */
+rlra_status rlra_gaussian_philox(rlra_ctx* ctx, int loc, int rows, int cols, uint64_t seed,
+                                 int draw, int64_t row0, double* out, int64_t ld);
+
+/* ---------------------------------------------------------- algorithms --- */
+/* sketch.hpp:44 (left=0, y m x l) and sketch.hpp:65 (left=1, y l x n). */
+rlra_status rlra_sample(rlra_ctx* ctx, int loc, int left, const double* a, int m, int n,
+                        int64_t lda, int l, int q, int s, const rlra_omega* omega, double* y,
+                        int64_t ldy);
+
+/* rsvd.hpp:127/144/154.  u (m x k), sigma (k), v (n x k). */
+rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int m, int n,
+                      int64_t lda, int k, int p, int q, int s, const rlra_omega* omega, double* u,
+                      int64_t ldu, double* sigma, double* v, int64_t ldv);
+
+/* qb.hpp:98/148.  If inplace, `a` is overwritten with A - QB
+ * (qb_blocked_inplace); otherwise it is read only.  q (m x cap), b (cap x n)
+ * with cap >= min(blk*num_blocks, min(m,n)); hist has num_blocks entries. */
+rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int64_t lda,
+                            int inplace, int blk, int num_blocks, double tol, int q_power,
+                            int reorth_period, const rlra_omega* omega, double* q, int64_t ldq,
+                            double* b, int64_t ldb, int cap, int* ell, double* hist, int* nhist,
+                            double* final_residual, int* reached);
+
+/* qb.hpp:276.  q (m x ell), b (ell x n).  k == 0 keeps all ell.
+ * u (m x k_out), sigma (k_out), v (n x k_out); size them for k or ell. */
+rlra_status rlra_svd_from_qb(rlra_ctx* ctx, int loc, const double* q, int m, int64_t ldq,
+                             const double* b, int n, int64_t ldb, int ell, int k, int vnum,
+                             double* u, int64_t ldu, double* sigma, double* v, int64_t ldv,
+                             int* k_out);
+
+/* interp.hpp:101: column ID, rank (k >= 1, tol == 0) or tolerance mode
+ * (k == 0, tol > 0).  jc (n), v (n x kmax). */
+rlra_status rlra_id_column(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                           int k, double tol, int* jc, double* v, int64_t ldv, int* k_out,
+                           double* qr_residual, int* reached, int* clamped);
+
+/* interp.hpp:203: jc (n), v (n x k). */
+rlra_status rlra_id_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                         int k, int p, int q, int s, const rlra_omega* omega, int* jc, double* v,
+                         int64_t ldv, double* qr_residual, int* clamped);
+
+/* interp.hpp:123: row side of a finished column ID of rank k.  jr (m),
+ * w (m x k). */
+rlra_status rlra_two_sided_from_column(rlra_ctx* ctx, int loc, const double* a, int m, int n,
+                                       int64_t lda, const int* jc, int k, int* jr, double* w,
+                                       int64_t ldw);
+
+/* interp.hpp:158: c (m x k), u (k x k), r (k x n), residual = ||A - CUR||_F. */
+rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int m, int n,
+                                    int64_t lda, const int* jc, const int* jr, const double* v,
+                                    int64_t ldv, int k, double* c, int64_t ldc, double* u,
+                                    int64_t ldu, double* r, int64_t ldr, double* residual);
+
+/* interp.hpp:240: everything cur_rand produces, plus the column/row ID parts. */
+rlra_status rlra_cur_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                          int k, int p, int q, int s, const rlra_omega* omega, int* jc, int* jr,
+                          double* v, int64_t ldv, double* w, int64_t ldw, double* c,
+                          int64_t ldc, double* u, int64_t ldu, double* r, int64_t ldr,
+                          double* residual, double* qr_residual);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLRA_C_H */

@@ -1,0 +1,659 @@
+// capi.cu — the extern "C" boundary (include/rlra_c.h).
+//
+// Responsibilities: argument validation with the reference's messages,
+// host<->device staging for RLRA_HOST buffers, status mapping, and the
+// thread-local last-error string.  The arithmetic lives in engine.cu and the
+// kernel files; nothing here computes on the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "../../include/rlra_c.h"
+#include "cpqr.cuh"
+#include "engine.cuh"
+#include "gemm.cuh"
+#include "jacobi.cuh"
+#include "qr.cuh"
+#include "reduce.cuh"
+
+using namespace rlra_b200;
+
+struct rlra_ctx {
+    Context c;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+rlra_status guard(rlra_ctx* ctx, F&& f) {
+    try {
+        if (!ctx) raise(RLRA_EINVAL, "null rlra_ctx");
+        RLRA_CUDA(cudaSetDevice(ctx->c.device));
+        f(ctx->c);
+        return RLRA_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        if (ctx) cudaStreamSynchronize(ctx->c.stream);
+        return static_cast<rlra_status>(e.status);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return RLRA_EINVAL;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) raise(RLRA_EINVAL, fmt("null pointer argument '%s'", what));
+}
+
+void check_ld(int64_t ld, int rows, const char* what) {
+    if (ld < std::max(1, rows)) raise(RLRA_EINVAL, fmt("leading dimension of '%s' is %lld < %d rows",
+                                                       what, (long long)ld, rows));
+}
+
+// Read-only matrix argument: a device view, staged from the host if needed.
+struct In {
+    DMatBuf own;
+    DMat m;
+    In(Context& c, int loc, const double* p, int rows, int cols, int64_t ld, const char* what) {
+        if (rows < 0 || cols < 0) raise(RLRA_EDIM, fmt("%s: negative dimensions %dx%d", what, rows, cols));
+        if (rows > 0 && cols > 0) {
+            need(p, what);
+            check_ld(ld, rows, what);
+        }
+        if (loc == RLRA_DEVICE) {
+            m.p = const_cast<double*>(p);
+            m.rows = rows;
+            m.cols = cols;
+            m.ld = std::max<int64_t>(ld, 1);
+        } else {
+            own = DMatBuf(c, rows, cols);
+            m = own.m;
+            if (rows > 0 && cols > 0) h2d_mat(c, p, ld, m);
+        }
+    }
+};
+
+// Output matrix argument: device view, copied back to the host by finish().
+struct Out {
+    DMatBuf own;
+    DMat m;
+    double* host = nullptr;
+    int64_t ldh = 0;
+    Out(Context& c, int loc, double* p, int rows, int cols, int64_t ld, const char* what) {
+        if (rows > 0 && cols > 0) {
+            need(p, what);
+            check_ld(ld, rows, what);
+        }
+        if (loc == RLRA_DEVICE) {
+            m.p = p;
+            m.rows = rows;
+            m.cols = cols;
+            m.ld = std::max<int64_t>(ld, 1);
+        } else {
+            own = DMatBuf(c, rows, cols);
+            m = own.m;
+            host = p;
+            ldh = ld;
+        }
+    }
+    void finish(Context& c) {
+        if (host && m.rows > 0 && m.cols > 0) d2h_mat(c, m, host, ldh);
+    }
+};
+
+// Device vector of doubles (sigma) or ints (permutations).
+template <class T>
+struct OutVec {
+    Buf own;
+    T* d = nullptr;
+    T* host = nullptr;
+    int n = 0;
+    OutVec(Context& c, int loc, T* p, int count, const char* what) : n(count) {
+        if (count > 0) need(p, what);
+        if (loc == RLRA_DEVICE) {
+            d = p;
+        } else {
+            own = Buf(c, sizeof(T) * std::max(count, 1));
+            d = static_cast<T*>(own.p);
+            host = p;
+        }
+    }
+    void finish(Context& c) {
+        if (host && n > 0)
+            RLRA_CUDA(cudaMemcpyAsync(host, d, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
+    }
+};
+
+template <class T>
+struct InVec {
+    Buf own;
+    const T* d = nullptr;
+    InVec(Context& c, int loc, const T* p, int count, const char* what) {
+        if (count > 0) need(p, what);
+        if (loc == RLRA_DEVICE) {
+            d = p;
+        } else {
+            own = Buf(c, sizeof(T) * std::max(count, 1));
+            if (count > 0)
+                RLRA_CUDA(cudaMemcpyAsync(own.p, p, sizeof(T) * count, cudaMemcpyHostToDevice, c.stream));
+            d = static_cast<const T*>(own.p);
+        }
+    }
+};
+
+void sync(Context& c) { RLRA_CUDA(cudaStreamSynchronize(c.stream)); }
+
+void check_sample_rank(int k, int p, int m, int n) {  // rsvd.hpp:102-108, interp.hpp:179-184
+    if (k < 1) raise(RLRA_EDIM, fmt("rank k must be >= 1 (got %d)", k));
+    if (p < 0) raise(RLRA_EDIM, fmt("oversampling p must be >= 0 (got %d)", p));
+    const int r = std::min(m, n);
+    if (k + p > r) raise(RLRA_EDIM, fmt("k + p = %d exceeds min(m,n) = %d", k + p, r));
+}
+
+void check_sample(int l, int q, int s, int rows, int cols) {  // sketch.hpp:45-50
+    const int min_dim = std::min(rows, cols);
+    if (l < 1 || l > min_dim)
+        raise(RLRA_EDIM, fmt("sample_right: width %d out of range [1,%d] for %dx%d", l, min_dim, rows,
+                             cols));
+    if (q < 0 || s < 1) raise(RLRA_EDIM, fmt("sample_right: q=%d, s=%d out of range", q, s));
+}
+
+OmegaSource omega_of(const rlra_omega* o) {
+    if (!o) raise(RLRA_EINVAL, "null rlra_omega");
+    if (o->mode != RLRA_OMEGA_CALLBACK && o->mode != RLRA_OMEGA_PHILOX)
+        raise(RLRA_EINVAL, fmt("unknown omega mode %d", o->mode));
+    OmegaSource s;
+    s.o = o;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rlra_last_error(void) { return g_err.c_str(); }
+const char* rlra_version(void) { return "rlra-b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+rlra_status rlra_ctx_create(int device, rlra_ctx** out) {
+    if (!out) {
+        g_err = "null output pointer";
+        return RLRA_EINVAL;
+    }
+    *out = nullptr;
+    rlra_ctx* ctx = new rlra_ctx();
+    try {
+        int count = 0;
+        RLRA_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            raise(RLRA_ECUDA, fmt("no CUDA device %d (found %d)", device, count));
+        ctx->c.device = device;
+        RLRA_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        RLRA_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            raise(RLRA_ECUDA, fmt("device %d is sm_%d%d; this build targets sm_100a", device, prop.major,
+                                  prop.minor));
+        ctx->c.num_sms = prop.multiProcessorCount;
+        RLRA_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+        RLRA_CUDA(cudaDeviceGetDefaultMemPool(&ctx->c.pool, device));
+        uint64_t thr = UINT64_MAX;
+        RLRA_CUDA(cudaMemPoolSetAttribute(ctx->c.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        RLRA_CUDA(cudaMallocHost(&ctx->c.h_scalars, 64 * sizeof(double)));
+        RLRA_CUDA(cudaMallocHost(&ctx->c.h_flags, 64 * sizeof(int)));
+    } catch (const Error& e) {
+        g_err = e.msg;
+        delete ctx;
+        return static_cast<rlra_status>(e.status);
+    }
+    *out = ctx;
+    return RLRA_OK;
+}
+
+rlra_status rlra_ctx_destroy(rlra_ctx* ctx) {
+    if (!ctx) return RLRA_OK;
+    cudaSetDevice(ctx->c.device);
+    if (ctx->c.stream) {
+        cudaStreamSynchronize(ctx->c.stream);
+        cudaStreamDestroy(ctx->c.stream);
+    }
+    if (ctx->c.h_scalars) cudaFreeHost(ctx->c.h_scalars);
+    if (ctx->c.h_flags) cudaFreeHost(ctx->c.h_flags);
+    delete ctx;
+    return RLRA_OK;
+}
+
+rlra_status rlra_ctx_synchronize(rlra_ctx* ctx) {
+    return guard(ctx, [&](Context& c) { sync(c); });
+}
+
+uint64_t rlra_ctx_launch_count(const rlra_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+rlra_status rlra_ctx_profile(rlra_ctx* ctx, int enable) {
+    return guard(ctx, [&](Context& c) {
+        sync(c);
+        for (auto& r : c.prof) {
+            cudaEventDestroy(r.start);
+            cudaEventDestroy(r.stop);
+        }
+        c.prof.clear();
+        c.profile = enable != 0;
+    });
+}
+
+int rlra_ctx_profile_count(const rlra_ctx* ctx) { return ctx ? int(ctx->c.prof.size()) : 0; }
+
+rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap, int* M, int* N, int* K,
+                                 double* flops, double* ms) {
+    return guard(ctx, [&](Context& c) {
+        if (i < 0 || i >= int(c.prof.size())) raise(RLRA_EINVAL, "profile index out of range");
+        sync(c);
+        const auto& r = c.prof[i];
+        if (name && name_cap > 0) {
+            std::snprintf(name, name_cap, "%s", r.name);
+        }
+        if (M) *M = r.M;
+        if (N) *N = r.N;
+        if (K) *K = r.K;
+        if (flops) *flops = r.flops;
+        float t = 0.f;
+        RLRA_CUDA(cudaEventElapsedTime(&t, r.start, r.stop));
+        if (ms) *ms = t;
+    });
+}
+void* rlra_ctx_stream(const rlra_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+rlra_status rlra_matmul(rlra_ctx* ctx, int loc, int ta, int tb, const double* a, int ar, int ac,
+                        int64_t lda, const double* b, int br, int bc, int64_t ldb, double* c,
+                        int64_t ldc) {
+    return guard(ctx, [&](Context& C) {
+        const int m = ta ? ac : ar, ka = ta ? ar : ac, kb = tb ? bc : br, n = tb ? br : bc;
+        if (ka != kb)
+            raise(RLRA_EDIM, fmt("matmul: inner dimensions disagree: op(%dx%d) * op(%dx%d)", ar, ac, br,
+                                 bc));
+        In A(C, loc, a, ar, ac, lda, "a"), B(C, loc, b, br, bc, ldb, "b");
+        Out Cm(C, loc, c, m, n, ldc, "c");
+        gemm(C, ta ? Op::T : Op::N, tb ? Op::T : Op::N, m, n, ka, 1.0, A.m.p, A.m.ld, B.m.p, B.m.ld,
+             0.0, Cm.m.p, Cm.m.ld);
+        Cm.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_compact_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                            double* q, int64_t ldq, double* r, int64_t ldr, int* degenerate) {
+    return guard(ctx, [&](Context& C) {
+        if (m < n) raise(RLRA_EDIM, fmt("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
+        In A(C, loc, a, m, n, lda, "a");
+        Out Q(C, loc, q, m, n, ldq, "q");
+        copy_mat(C, A.m, Q.m);
+        QrResult res;
+        if (r) {
+            Out R(C, loc, r, n, n, ldr, "r");
+            res = orth_inplace(C, Q.m, &R.m);
+            R.finish(C);
+            Q.finish(C);
+            sync(C);
+        } else {
+            res = orth_inplace(C, Q.m, nullptr);
+            Q.finish(C);
+            sync(C);
+        }
+        if (degenerate) *degenerate = res.degenerate ? 1 : 0;
+    });
+}
+
+rlra_status rlra_pivoted_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k,
+                            double tol, double* q1, int64_t ldq1, double* s1, int64_t lds1, int* perm,
+                            int* frank, double* residual, int* reached, int* degenerate) {
+    return guard(ctx, [&](Context& C) {
+        const int rmax = std::min(m, n);
+        const bool tol_mode = (k == 0 && tol > 0.0);
+        if (!tol_mode && (k < 1 || k > rmax || tol != 0.0))
+            raise(RLRA_EDIM, fmt("pivoted_qr_partial: need either k in [1,%d] with tol=0 or k=0 with "
+                                 "tol>0 (got k=%d, tol=%g)",
+                                 rmax, k, tol));
+        const int kmax = tol_mode ? rmax : k;
+        In A(C, loc, a, m, n, lda, "a");
+        Out S(C, loc, s1, kmax, n, lds1, "s1");
+        OutVec<int> P(C, loc, perm, n, "perm");
+        CpqrResult res;
+        if (q1) {
+            Out Q(C, loc, q1, m, kmax, ldq1, "q1");
+            res = pivoted_qr(C, A.m, k, tol, &Q.m, S.m, P.d);
+            if (Q.host && res.frank > 0) d2h_mat(C, Q.m.block(0, 0, m, res.frank), Q.host, Q.ldh);
+            sync(C);
+        } else {
+            res = pivoted_qr(C, A.m, k, tol, nullptr, S.m, P.d);
+        }
+        if (S.host && res.frank > 0) d2h_mat(C, S.m.block(0, 0, res.frank, n), S.host, S.ldh);
+        P.finish(C);
+        sync(C);
+        if (frank) *frank = res.frank;
+        if (residual) *residual = res.residual;
+        if (reached) *reached = res.reached ? 1 : 0;
+        if (degenerate) *degenerate = res.degenerate ? 1 : 0;
+    });
+}
+
+rlra_status rlra_upper_tri_solve(rlra_ctx* ctx, int loc, const double* s11, int k, int64_t lds11,
+                                 const double* s12, int nc, int64_t lds12, double* t, int64_t ldt,
+                                 int* clamped) {
+    return guard(ctx, [&](Context& C) {
+        In S11(C, loc, s11, k, k, lds11, "s11"), S12(C, loc, s12, k, nc, lds12, "s12");
+        Out T(C, loc, t, k, nc, ldt, "t");
+        const bool cl = upper_tri_solve(C, S11.m, S12.m, T.m);
+        T.finish(C);
+        sync(C);
+        if (clamped) *clamped = cl ? 1 : 0;
+    });
+}
+
+rlra_status rlra_small_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                           double* u, int64_t ldu, double* sigma, double* v, int64_t ldv) {
+    return guard(ctx, [&](Context& C) {
+        const int r = std::min(m, n);
+        In A(C, loc, a, m, n, lda, "a");
+        Out U(C, loc, u, m, r, ldu, "u"), V(C, loc, v, n, r, ldv, "v");
+        OutVec<double> S(C, loc, sigma, r, "sigma");
+        small_svd(C, A.m, U.m, S.d, V.m);
+        U.finish(C);
+        V.finish(C);
+        S.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_sym_eig(rlra_ctx* ctx, int loc, const double* t, int n, int64_t ldt, double* values,
+                         double* vectors, int64_t ldv) {
+    return guard(ctx, [&](Context& C) {
+        In T(C, loc, t, n, n, ldt, "t");
+        Out V(C, loc, vectors, n, n, ldv, "vectors");
+        OutVec<double> D(C, loc, values, n, "values");
+        sym_eig(C, T.m, D.d, V.m);
+        V.finish(C);
+        D.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                double* out) {
+    return guard(ctx, [&](Context& C) {
+        need(out, "out");
+        In A(C, loc, a, m, n, lda, "a");
+        *out = frobenius(C, A.m);
+    });
+}
+
+rlra_status rlra_lowrank_residual(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                  const double* x, int64_t ldx, const double* y, int64_t ldy, int k,
+                                  double* out) {
+    return guard(ctx, [&](Context& C) {
+        need(out, "out");
+        In A(C, loc, a, m, n, lda, "a"), X(C, loc, x, m, k, ldx, "x"), Y(C, loc, y, n, k, ldy, "y");
+        Buf sq(C, sizeof(double));
+        GemmOpts o;
+        o.epi = EPI_RESID;
+        o.R = A.m.p;
+        o.ldr = A.m.ld;
+        o.resid_sq = sq.d();
+        gemm(C, Op::N, Op::T, m, n, k, 1.0, X.m.p, X.m.ld, Y.m.p, Y.m.ld, 0.0, nullptr, 0, o);
+        RLRA_CUDA(cudaMemcpyAsync(C.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+        sync(C);
+        *out = std::sqrt(C.h_scalars[0]);
+    });
+}
+
+rlra_status rlra_gaussian_philox(rlra_ctx* ctx, int loc, int rows, int cols, uint64_t seed, int draw,
+                                 int64_t row0, double* out, int64_t ld) {
+    return guard(ctx, [&](Context& C) {
+        Out O(C, loc, out, rows, cols, ld, "out");
+        philox_fill(C, O.m, seed, draw, row0);
+        O.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_sample(rlra_ctx* ctx, int loc, int left, const double* a, int m, int n, int64_t lda,
+                        int l, int q, int s, const rlra_omega* omega, double* y, int64_t ldy) {
+    return guard(ctx, [&](Context& C) {
+        if (left)
+            check_sample(l, q, s, n, m);
+        else
+            check_sample(l, q, s, m, n);
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        if (!left) {
+            Out Y(C, loc, y, m, l, ldy, "y");
+            sample_right(C, A.m, l, q, s, om, Y.m);
+            Y.finish(C);
+        } else {
+            Out Y(C, loc, y, l, n, ldy, "y");
+            DMatBuf Yt(C, n, l);
+            sample_left_t(C, A.m, l, q, s, om, Yt);
+            transpose_mat(C, Yt, Y.m);
+            Y.finish(C);
+            sync(C);
+        }
+        sync(C);
+    });
+}
+
+rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int m, int n, int64_t lda,
+                      int k, int p, int q, int s, const rlra_omega* omega, double* u, int64_t ldu,
+                      double* sigma, double* v, int64_t ldv) {
+    return guard(ctx, [&](Context& C) {
+        if (variant < 0 || variant > 2) raise(RLRA_EINVAL, fmt("unknown rsvd variant %d", variant));
+        check_sample_rank(k, p, m, n);
+        if (variant != RLRA_RSVD_BASIC) check_sample(k + p, q, s, m, n);
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        Out U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
+        OutVec<double> S(C, loc, sigma, k, "sigma");
+        rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
+        U.finish(C);
+        V.finish(C);
+        S.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int64_t lda, int inplace,
+                            int blk, int num_blocks, double tol, int q_power, int reorth_period,
+                            const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,
+                            int cap, int* ell, double* hist, int* nhist, double* final_residual,
+                            int* reached) {
+    return guard(ctx, [&](Context& C) {
+        if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
+        if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
+        if (tol < 0.0) raise(RLRA_EDIM, fmt("tol must be >= 0 (got %g)", tol));
+        if (q_power < 0)
+            raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
+        if (reorth_period < 1)
+            raise(RLRA_EDIM, fmt("reorth_period must be >= 1 (got %d)", reorth_period));
+        const int64_t need_cap = std::min<int64_t>(int64_t(blk) * num_blocks, std::min(m, n));
+        if (cap < need_cap)
+            raise(RLRA_EINVAL, fmt("qb_blocked: capacity %d < min(b*M, min(m,n)) = %lld", cap,
+                                   (long long)need_cap));
+        OmegaSource om = omega_of(omega);
+        // working residual W: the caller's buffer when in place on the device
+        DMatBuf Wown;
+        DMat W;
+        if (loc == RLRA_DEVICE && inplace) {
+            need(a, "a");
+            W.p = a;
+            W.rows = m;
+            W.cols = n;
+            W.ld = lda;
+        } else {
+            In A(C, loc, a, m, n, lda, "a");
+            Wown = DMatBuf(C, m, n);
+            copy_mat(C, A.m, Wown);
+            W = Wown.m;
+            sync(C);
+        }
+        Out Q(C, loc, q, m, cap, ldq, "q"), B(C, loc, b, cap, n, ldb, "b");
+        QbOut r = qb_blocked(C, W, blk, num_blocks, tol, q_power, reorth_period, om, Q.m, B.m);
+        if (Q.host && r.ell > 0) d2h_mat(C, Q.m.block(0, 0, m, r.ell), Q.host, Q.ldh);
+        if (B.host && r.ell > 0) d2h_mat(C, B.m.block(0, 0, r.ell, n), B.host, B.ldh);
+        if (loc == RLRA_HOST && inplace) d2h_mat(C, W, a, lda);
+        sync(C);
+        if (ell) *ell = r.ell;
+        if (nhist) *nhist = int(r.hist.size());
+        if (hist)
+            for (size_t i = 0; i < r.hist.size(); ++i) hist[i] = r.hist[i];
+        if (final_residual) *final_residual = r.final_residual;
+        if (reached) *reached = r.reached ? 1 : 0;
+    });
+}
+
+rlra_status rlra_svd_from_qb(rlra_ctx* ctx, int loc, const double* q, int m, int64_t ldq, const double* b,
+                             int n, int64_t ldb, int ell, int k, int vnum, double* u, int64_t ldu,
+                             double* sigma, double* v, int64_t ldv, int* k_out) {
+    return guard(ctx, [&](Context& C) {
+        if (k < 0 || k > ell) raise(RLRA_EDIM, fmt("rank k = %d outside [0, rank(B) = %d]", k, ell));
+        if (k == 0) k = ell;
+        if (k_out) *k_out = k;
+        if (k == 0) return;
+        In Q(C, loc, q, m, ell, ldq, "q"), B(C, loc, b, ell, n, ldb, "b");
+        Out U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
+        OutVec<double> S(C, loc, sigma, k, "sigma");
+        svd_from_qb(C, Q.m, B.m, k, vnum, U.m, S.d, V.m);
+        U.finish(C);
+        V.finish(C);
+        S.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_id_column(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k,
+                           double tol, int* jc, double* v, int64_t ldv, int* k_out, double* qr_residual,
+                           int* reached, int* clamped) {
+    return guard(ctx, [&](Context& C) {
+        const int rmax = std::min(m, n);
+        const bool tol_mode = (k == 0 && tol > 0.0);
+        if (!tol_mode && (k < 1 || k > rmax || tol != 0.0))
+            raise(RLRA_EDIM, fmt("pivoted_qr_partial: need either k in [1,%d] with tol=0 or k=0 with "
+                                 "tol>0 (got k=%d, tol=%g)",
+                                 rmax, k, tol));
+        const int kmax = tol_mode ? rmax : k;
+        In A(C, loc, a, m, n, lda, "a");
+        OutVec<int> J(C, loc, jc, n, "jc");
+        DMatBuf Vd(C, n, kmax);
+        IdOut r = id_column(C, A.m, k, tol, J.d, Vd);
+        Out V(C, loc, v, n, r.k, ldv, "v");
+        if (r.k > 0) copy_mat(C, Vd.m.block(0, 0, n, r.k), V.m);
+        V.finish(C);
+        J.finish(C);
+        sync(C);
+        if (k_out) *k_out = r.k;
+        if (qr_residual) *qr_residual = r.qr_residual;
+        if (reached) *reached = r.reached ? 1 : 0;
+        if (clamped) *clamped = r.clamped ? 1 : 0;
+    });
+}
+
+rlra_status rlra_id_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k, int p,
+                         int q, int s, const rlra_omega* omega, int* jc, double* v, int64_t ldv,
+                         double* qr_residual, int* clamped) {
+    return guard(ctx, [&](Context& C) {
+        check_sample_rank(k, p, m, n);
+        check_sample(k + p, q, s, n, m);
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        OutVec<int> J(C, loc, jc, n, "jc");
+        Out V(C, loc, v, n, k, ldv, "v");
+        IdOut r = id_rand(C, A.m, k, p, q, s, om, J.d, V.m);
+        V.finish(C);
+        J.finish(C);
+        sync(C);
+        if (qr_residual) *qr_residual = r.qr_residual;
+        if (clamped) *clamped = r.clamped ? 1 : 0;
+    });
+}
+
+rlra_status rlra_two_sided_from_column(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                       const int* jc, int k, int* jr, double* w, int64_t ldw) {
+    return guard(ctx, [&](Context& C) {
+        if (k < 0 || k > std::min(m, n)) raise(RLRA_EDIM, fmt("two_sided_from_column: rank %d", k));
+        OutVec<int> J(C, loc, jr, m, "jr");
+        if (k == 0) {
+            std::vector<int> id(m);
+            for (int i = 0; i < m; ++i) id[i] = i;
+            if (loc == RLRA_HOST)
+                std::copy(id.begin(), id.end(), jr);
+            else
+                RLRA_CUDA(cudaMemcpyAsync(jr, id.data(), sizeof(int) * m, cudaMemcpyHostToDevice, C.stream));
+            sync(C);
+            return;
+        }
+        In A(C, loc, a, m, n, lda, "a");
+        InVec<int> Jc(C, loc, jc, n, "jc");
+        Out W(C, loc, w, m, k, ldw, "w");
+        two_sided_from_column(C, A.m, Jc.d, k, J.d, W.m);
+        W.finish(C);
+        J.finish(C);
+        sync(C);
+    });
+}
+
+static void cur_core(Context& C, int loc, const DMat& A, const int* jc_d, const int* jr_d,
+                     const DMat& V, int k, double* c, int64_t ldc, double* u, int64_t ldu, double* r,
+                     int64_t ldr, double* residual) {
+    const int m = int(A.rows), n = int(A.cols);
+    if (k == 0) {
+        if (residual) *residual = frobenius(C, A);
+        return;
+    }
+    std::vector<int> jr_h(k);
+    RLRA_CUDA(cudaMemcpyAsync(jr_h.data(), jr_d, sizeof(int) * k, cudaMemcpyDeviceToHost, C.stream));
+    sync(C);
+    Out Cm(C, loc, c, m, k, ldc, "c"), U(C, loc, u, k, k, ldu, "u"), R(C, loc, r, k, n, ldr, "r");
+    const double res = cur_from_two_sided(C, A, jc_d, jr_d, V, k, Cm.m, U.m, R.m, jr_h.data());
+    Cm.finish(C);
+    U.finish(C);
+    R.finish(C);
+    sync(C);
+    if (residual) *residual = res;
+}
+
+rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                    const int* jc, const int* jr, const double* v, int64_t ldv, int k,
+                                    double* c, int64_t ldc, double* u, int64_t ldu, double* r,
+                                    int64_t ldr, double* residual) {
+    return guard(ctx, [&](Context& C) {
+        In A(C, loc, a, m, n, lda, "a");
+        InVec<int> Jc(C, loc, jc, n, "jc"), Jr(C, loc, jr, m, "jr");
+        In V(C, loc, v, n, k, ldv, "v");
+        cur_core(C, loc, A.m, Jc.d, Jr.d, V.m, k, c, ldc, u, ldu, r, ldr, residual);
+    });
+}
+
+rlra_status rlra_cur_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k, int p,
+                          int q, int s, const rlra_omega* omega, int* jc, int* jr, double* v,
+                          int64_t ldv, double* w, int64_t ldw, double* c, int64_t ldc, double* u,
+                          int64_t ldu, double* r, int64_t ldr, double* residual, double* qr_residual) {
+    return guard(ctx, [&](Context& C) {
+        check_sample_rank(k, p, m, n);
+        check_sample(k + p, q, s, n, m);
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        OutVec<int> Jc(C, loc, jc, n, "jc"), Jr(C, loc, jr, m, "jr");
+        Out V(C, loc, v, n, k, ldv, "v"), W(C, loc, w, m, k, ldw, "w");
+        IdOut idr = id_rand(C, A.m, k, p, q, s, om, Jc.d, V.m);
+        two_sided_from_column(C, A.m, Jc.d, k, Jr.d, W.m);
+        cur_core(C, loc, A.m, Jc.d, Jr.d, V.m, k, c, ldc, u, ldu, r, ldr, residual);
+        V.finish(C);
+        W.finish(C);
+        Jc.finish(C);
+        Jr.finish(C);
+        sync(C);
+        if (qr_residual) *qr_residual = idr.qr_residual;
+    });
+}
+
+}  // extern "C"

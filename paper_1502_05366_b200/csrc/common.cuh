@@ -1,0 +1,154 @@
+// common.cuh — shared device/host plumbing for the rlra B200 engine.
+//
+// Errors: engine code throws rlra_b200::Error{status, message}; the C-ABI
+// layer (capi.cu) catches it, stores the message in a thread-local buffer and
+// returns the status.  The status values map 1:1 onto the reference's
+// exception classes (reference core/errors.hpp:11-33).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/rlra_c.h"
+
+namespace rlra_b200 {
+
+struct Error {
+    int status;
+    std::string msg;
+};
+
+inline std::string fmt(const char* f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return std::string(buf);
+}
+
+[[noreturn]] inline void raise(int status, const std::string& m) { throw Error{status, m}; }
+
+#define RLRA_CUDA(x)                                                                      \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess)                                                            \
+            ::rlra_b200::raise(RLRA_ECUDA, ::rlra_b200::fmt("CUDA error %s at %s:%d",      \
+                                                            cudaGetErrorString(e_),       \
+                                                            __FILE__, __LINE__));         \
+    } while (0)
+
+#define RLRA_LAUNCH_CHECK() RLRA_CUDA(cudaGetLastError())
+
+// Column-major device matrix view: element (i,j) at p[i + j*ld].
+struct DMat {
+    double* p = nullptr;
+    int64_t rows = 0, cols = 0, ld = 0;
+    __host__ __device__ double* col(int64_t j) const { return p + j * ld; }
+    __host__ __device__ double& at(int64_t i, int64_t j) const { return p[i + j * ld]; }
+    DMat block(int64_t r0, int64_t c0, int64_t nr, int64_t nc) const {
+        DMat b;
+        b.p = p + r0 + c0 * ld;
+        b.rows = nr;
+        b.cols = nc;
+        b.ld = ld;
+        return b;
+    }
+};
+
+// Execution context: one device, one stream, a stream-ordered pool for
+// scratch.  Everything the engine launches goes on `stream`.
+struct Context {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    // pinned scalars for device->host flags without extra allocations
+    double* h_scalars = nullptr;  // pinned, 64 doubles
+    int* h_flags = nullptr;       // pinned, 64 ints
+    // statistics: kernels launched by this context since last reset
+    uint64_t launches = 0;
+    // Cholesky-QR policy knobs (see qr.cu)
+    double cholqr_pivot_floor = 1e-12;
+    // optional per-launch / per-phase timing with CUDA events on `stream`
+    bool profile = false;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t start, stop;
+        int M, N, K;
+        double flops;
+    };
+    std::vector<ProfRec> prof;
+};
+
+// Records one interval on ctx.stream when profiling is enabled.
+struct ProfScope {
+    Context& ctx;
+    int idx = -1;
+    ProfScope(Context& c, const char* name, int M = 0, int N = 0, int K = 0, double flops = 0.0)
+        : ctx(c) {
+        if (!ctx.profile) return;
+        Context::ProfRec r{name, nullptr, nullptr, M, N, K, flops};
+        cudaEventCreate(&r.start);
+        cudaEventCreate(&r.stop);
+        cudaEventRecord(r.start, ctx.stream);
+        ctx.prof.push_back(r);
+        idx = int(ctx.prof.size()) - 1;
+    }
+    ~ProfScope() {
+        if (idx >= 0) cudaEventRecord(ctx.prof[idx].stop, ctx.stream);
+    }
+};
+
+// RAII device scratch buffer on the context's pool.
+struct Buf {
+    Context* ctx = nullptr;
+    void* p = nullptr;
+    size_t bytes = 0;
+    Buf() = default;
+    Buf(Context& c, size_t b) : ctx(&c), bytes(b) {
+        if (b) RLRA_CUDA(cudaMallocAsync(&p, b, c.stream));
+    }
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+    Buf(Buf&& o) noexcept : ctx(o.ctx), p(o.p), bytes(o.bytes) { o.p = nullptr; }
+    Buf& operator=(Buf&& o) noexcept {
+        release();
+        ctx = o.ctx;
+        p = o.p;
+        bytes = o.bytes;
+        o.p = nullptr;
+        return *this;
+    }
+    ~Buf() { release(); }
+    void release() {
+        if (p && ctx) cudaFreeAsync(p, ctx->stream);
+        p = nullptr;
+    }
+    double* d() const { return static_cast<double*>(p); }
+    int* i() const { return static_cast<int*>(p); }
+};
+
+// A device matrix that owns its storage (ld == rows).
+struct DMatBuf {
+    Buf buf;
+    DMat m;
+    DMatBuf() = default;
+    DMatBuf(Context& c, int64_t rows, int64_t cols)
+        : buf(c, sizeof(double) * size_t(rows > 0 ? rows : 0) * size_t(cols > 0 ? cols : 0)) {
+        m.p = buf.d();
+        m.rows = rows;
+        m.cols = cols;
+        m.ld = rows > 0 ? rows : 1;
+    }
+    operator DMat() const { return m; }
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace rlra_b200

@@ -1,0 +1,66 @@
+// engine.cuh — host orchestration of the randomized factorizations over the
+// device kernels (reference L2: sketch.hpp, rsvd.hpp, qb.hpp, interp.hpp).
+// All operands are device matrices; the C-ABI layer (capi.cu) handles host
+// buffers, argument validation messages and status mapping.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace rlra_b200 {
+
+// Gaussian test-matrix source bound to one call (see rlra_omega in rlra_c.h).
+struct OmegaSource {
+    const rlra_omega* o = nullptr;
+    int next_draw = 0;
+};
+
+// sketch.hpp:44-60 — Y (m x l)
+void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y);
+// sketch.hpp:65-67 — returns Y^T (n x l) of the reference's l x n sample,
+// computed on A directly (the reference materialises A^T; we never do).
+void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt);
+
+// rsvd.hpp:127-160; U m x k, sigma (device) k, V n x k
+void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
+          const DMat& U, double* sigma, const DMat& V);
+
+struct QbOut {
+    int ell = 0;
+    std::vector<double> hist;
+    double final_residual = 0.0;
+    bool reached = true;
+};
+// qb.hpp:98-142 on W (destroyed: left as A - QB).  Q m x cap, B cap x n.
+QbOut qb_blocked(Context& ctx, const DMat& W, int blk, int num_blocks, double tol, int q_power,
+                 int reorth_period, OmegaSource& om, const DMat& Q, const DMat& B);
+
+// qb.hpp:276-288 (k already resolved to [1, ell]); U m x k, sigma k, V n x k
+void svd_from_qb(Context& ctx, const DMat& Q, const DMat& B, int k, int vnum, const DMat& U,
+                 double* sigma, const DMat& V);
+
+struct IdOut {
+    int k = 0;
+    double qr_residual = 0.0;
+    bool reached = true;
+    bool clamped = false;
+};
+// interp.hpp:101-104 — jc (device, n), V (n x kmax)
+IdOut id_column(Context& ctx, const DMat& A, int k, double tol, int* jc, const DMat& V);
+// interp.hpp:203-223 — jc (device, n), V (n x k)
+IdOut id_rand(Context& ctx, const DMat& A, int k, int p, int q, int s, OmegaSource& om, int* jc,
+              const DMat& V);
+// interp.hpp:123-140 — jr (device, m), Wr (m x k)
+void two_sided_from_column(Context& ctx, const DMat& A, const int* jc, int k, int* jr, const DMat& Wr);
+// interp.hpp:143-177 — C m x k, U k x k, R k x n; returns ||A - CUR||_F
+double cur_from_two_sided(Context& ctx, const DMat& A, const int* jc, const int* jr, const DMat& V,
+                          int k, const DMat& C, const DMat& U, const DMat& R, const int* jr_host);
+
+// ||A||_F (device-side deterministic reduction, read back)
+double frobenius(Context& ctx, const DMat& A);
+
+// scatter V = P [I_k; T^T] (interp.hpp:65-72)
+void build_interp(Context& ctx, const int* perm, const DMat& T, int n, int k, const DMat& V);
+
+}  // namespace rlra_b200

@@ -1,0 +1,203 @@
+// gemm.cu — launcher for the FP64 DMMA GEMM family (see gemm.cuh).
+#include "gemm.cuh"
+#include "reduce.cuh"
+
+namespace rlra_b200 {
+
+namespace {
+
+struct CfgBig {
+    static constexpr int BM = 128, BN = 128, BK = 16, WM = 64, WN = 32, STAGES = 4;
+};
+struct CfgSmall {
+    static constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, STAGES = 4;
+};
+
+template <class Cfg, bool A_KM, bool B_KM>
+constexpr size_t smem_bytes() {
+    return sizeof(double) * Cfg::STAGES *
+           (TileGeo<A_KM, Cfg::BM, Cfg::BK>::elems + TileGeo<B_KM, Cfg::BN, Cfg::BK>::elems);
+}
+
+template <class Cfg, bool A_KM, bool B_KM, bool VEC, int EPI, bool PHILOX>
+void launch_cfg(Context& ctx, const GemmParams& p) {
+    auto kern = dgemm_kernel<Cfg::BM, Cfg::BN, Cfg::BK, Cfg::WM, Cfg::WN, Cfg::STAGES, A_KM, B_KM, VEC,
+                             EPI, PHILOX>;
+    constexpr size_t smem = smem_bytes<Cfg, A_KM, B_KM>();
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr_set = true;
+    }
+    constexpr int threads = (Cfg::BM / Cfg::WM) * (Cfg::BN / Cfg::WN) * 32;
+    const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
+    kern<<<dim3(unsigned(grid)), threads, smem, ctx.stream>>>(p);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+}
+
+template <class Cfg, bool A_KM, bool B_KM, bool VEC>
+void launch_epi(Context& ctx, const GemmParams& p, int epi, bool philox) {
+    if (philox) {
+        if constexpr (!B_KM) {
+            if (epi == EPI_STORE) return launch_cfg<Cfg, A_KM, B_KM, VEC, EPI_STORE, true>(ctx, p);
+            if (epi == EPI_SPLIT) return launch_cfg<Cfg, A_KM, B_KM, VEC, EPI_SPLIT, true>(ctx, p);
+        }
+        raise(RLRA_EINVAL, "gemm: Philox B operand needs op(B)=N and a store/split epilogue");
+    }
+    if (epi == EPI_STORE) return launch_cfg<Cfg, A_KM, B_KM, VEC, EPI_STORE, false>(ctx, p);
+    if (epi == EPI_SPLIT) return launch_cfg<Cfg, A_KM, B_KM, VEC, EPI_SPLIT, false>(ctx, p);
+    return launch_cfg<Cfg, A_KM, B_KM, VEC, EPI_RESID, false>(ctx, p);
+}
+
+template <class Cfg>
+void launch_ops(Context& ctx, Op opa, Op opb, bool vec, const GemmParams& p, int epi, bool philox) {
+    const bool akm = opa == Op::N, bkm = opb == Op::T;
+#define RLRA_DISPATCH(AK, BK_)                                                   \
+    if (akm == AK && bkm == BK_) {                                               \
+        if (vec) return launch_epi<Cfg, AK, BK_, true>(ctx, p, epi, philox);     \
+        return launch_epi<Cfg, AK, BK_, false>(ctx, p, epi, philox);             \
+    }
+    RLRA_DISPATCH(true, false)
+    RLRA_DISPATCH(false, false)
+    RLRA_DISPATCH(true, true)
+    RLRA_DISPATCH(false, true)
+#undef RLRA_DISPATCH
+}
+
+__global__ void split_reduce_kernel(const double* ws, int splits, int M, int N, double alpha,
+                                    double beta, double* C, int64_t ldc, int upper_tile, int tile) {
+    const int64_t total = int64_t(M) * N;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int row = int(e % M);
+        const int col = int(e / M);
+        if (upper_tile && row / tile > col / tile) continue;
+        double s = 0.0;
+        for (int t = 0; t < splits; ++t) s += ws[int64_t(t) * total + e];
+        double* c = C + row + int64_t(col) * ldc;
+        *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
+    }
+}
+
+__global__ void philox_fill_kernel(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
+                                   int draw, int64_t row0) {
+    // one thread per group of 4 consecutive global rows of one column
+    const int64_t g0 = row0 >> 2, g1 = (row0 + rows + 3) >> 2;
+    const int64_t groups = (g1 - g0) * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < groups;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = e / (g1 - g0), g = g0 + e % (g1 - g0);
+        double v[4];
+        philox_normal4(seed, draw, g * 4, j, v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int64_t r = g * 4 + t - row0;
+            if (r >= 0 && r < rows) out[r + j * ld] = v[t];
+        }
+    }
+}
+
+}  // namespace
+
+void philox_fill(Context& ctx, const DMat& out, uint64_t seed, int draw, int64_t row0) {
+    if (out.rows <= 0 || out.cols <= 0) return;
+    const int64_t groups = ((out.rows + 7) / 4) * out.cols;
+    const int blocks = int(std::min<int64_t>((groups + 255) / 256, int64_t(ctx.num_sms) * 16));
+    philox_fill_kernel<<<blocks, 256, 0, ctx.stream>>>(out.p, out.ld, out.rows, out.cols, seed, draw,
+                                                       row0);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+}
+
+void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const double* A,
+          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+          const GemmOpts& o) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0 && o.epi == EPI_STORE) {
+        // C = beta*C (alpha*0): reuse the split reducer with zero splits
+        split_reduce_kernel<<<ctx.num_sms * 4, 256, 0, ctx.stream>>>(nullptr, 0, M, N, alpha, beta,
+                                                                      C, ldc, 0, 1);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        return;
+    }
+    const bool big = M >= 96 && N >= 96;
+    const int BM = big ? CfgBig::BM : CfgSmall::BM;
+    const int BN = big ? CfgBig::BN : CfgSmall::BN;
+    const int BK = 16;
+    const int per_sm = big ? 1 : 3;
+
+    GemmParams p{};
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.A = A;
+    p.lda = lda;
+    p.B = B;
+    p.ldb = ldb;
+    p.C = C;
+    p.ldc = ldc;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.mt = ceil_div(M, BM);
+    p.nt = ceil_div(N, BN);
+    p.tri_b_upper = o.tri_b_upper;
+    p.upper_tiles_only = o.upper_tiles_only;
+    p.seed = o.seed;
+    p.draw = o.draw;
+    p.krow0 = o.krow0;
+    p.R = o.R;
+    p.ldr = o.ldr;
+
+    int64_t tiles = int64_t(p.mt) * p.nt;
+    if (o.upper_tiles_only) tiles = int64_t(p.mt) * (p.mt + 1) / 2;
+    const int64_t cap = int64_t(ctx.num_sms) * per_sm;
+    int splits = 1;
+    if (o.epi != EPI_RESID && !o.tri_b_upper) {
+        if (o.force_splits > 0) {
+            splits = o.force_splits;
+        } else if (tiles < 2 * cap) {
+            const int64_t want = (2 * cap + tiles - 1) / tiles;
+            const int64_t kmaxs = std::max<int64_t>(1, K / (4 * BK));
+            splits = int(std::min<int64_t>(want, kmaxs));
+        }
+    }
+    int k_chunk = ceil_div(ceil_div(K, splits), BK) * BK;
+    splits = ceil_div(K, k_chunk);
+    p.k_chunk = k_chunk;
+    p.splits = splits;
+
+    const bool vec = (lda % 2 == 0) && (o.philox_b || ldb % 2 == 0) &&
+                     (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                     (o.philox_b || reinterpret_cast<uintptr_t>(B) % 16 == 0);
+
+    Buf ws, parts;
+    int epi = o.epi;
+    if (epi == EPI_STORE && splits > 1) {
+        ws = Buf(ctx, sizeof(double) * size_t(splits) * M * N);
+        p.ws = ws.d();
+        epi = EPI_SPLIT;
+    }
+    if (epi == EPI_RESID) {
+        parts = Buf(ctx, sizeof(double) * size_t(p.mt) * p.nt);
+        p.partials = parts.d();
+    }
+    ProfScope prof(ctx, "dgemm", M, N, K, 2.0 * M * double(N) * K);
+    if (big)
+        launch_ops<CfgBig>(ctx, opa, opb, vec, p, epi, o.philox_b);
+    else
+        launch_ops<CfgSmall>(ctx, opa, opb, vec, p, epi, o.philox_b);
+
+    if (epi == EPI_SPLIT) {
+        const int64_t total = int64_t(M) * N;
+        const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(ctx.num_sms) * 8));
+        split_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(p.ws, splits, M, N, alpha, beta, C, ldc,
+                                                            o.upper_tiles_only ? 1 : 0, BM);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+    }
+    if (epi == EPI_RESID) sum_fixed_order(ctx, p.partials, int64_t(p.mt) * p.nt, o.resid_sq);
+}
+
+}  // namespace rlra_b200

@@ -1,0 +1,502 @@
+// jacobi.cu — one-sided Jacobi SVD and two-sided Jacobi eigensolver.
+#include <cooperative_groups.h>
+
+#include "jacobi.cuh"
+#include "reduce.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rlra_b200 {
+
+namespace {
+
+constexpr int kJacThreads = 256;
+constexpr int kOneSidedSweepCap = 60;  // reference core/jacobi.hpp:29
+constexpr int kTwoSidedSweepCap = 30;  // reference core/jacobi.hpp:28
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// column at tournament position `pos` in round r (position 0 is fixed)
+__device__ __forceinline__ int rr_col(int pos, int r, int n2) {
+    return pos == 0 ? 0 : ((pos - 1 + r) % (n2 - 1)) + 1;
+}
+
+struct OneSidedArgs {
+    double* W;
+    int64_t ldw;
+    int m, n;
+    double* V;
+    int64_t ldv;
+    int* flags;   // [0..2] rotated-in-sweep flags, [3] status, [4] sweeps used
+};
+
+__global__ void __launch_bounds__(kJacThreads) onesided_jacobi_kernel(OneSidedArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const int n = a.n, m = a.m;
+    const int n2 = n + (n & 1);
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const double eps = 1e-15;  // reference core/jacobi.hpp:156
+    volatile int* flags = a.flags;
+    int sweep = 0;
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) flags[3] = RLRA_ECONV;
+            break;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) flags[(sweep + 1) % 3] = 0;
+        for (int r = 0; r < n2 - 1; ++r) {
+            for (int pi = gw; pi < n2 / 2; pi += nw) {
+                const int ca = rr_col(pi, r, n2), cb = rr_col(n2 - 1 - pi, r, n2);
+                const int p = min(ca, cb), q = max(ca, cb);
+                if (q >= n) continue;
+                double* wp = a.W + int64_t(p) * a.ldw;
+                double* wq = a.W + int64_t(q) * a.ldw;
+                double app = 0.0, aqq = 0.0, apq = 0.0;
+                for (int i = lane; i < m; i += 32) {
+                    const double xp = wp[i], xq = wq[i];
+                    app += xp * xp;
+                    aqq += xq * xq;
+                    apq += xp * xq;
+                }
+                app = warp_sum(app);
+                aqq = warp_sum(aqq);
+                apq = warp_sum(apq);
+                if (app == 0.0 || aqq == 0.0) continue;
+                if (fabs(apq) <= eps * sqrt(app * aqq)) continue;
+                const double zeta = (aqq - app) / (2.0 * apq);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + t * t);
+                const double s = t * c;
+                for (int i = lane; i < m; i += 32) {
+                    const double xp = wp[i], xq = wq[i];
+                    wp[i] = c * xp - s * xq;
+                    wq[i] = s * xp + c * xq;
+                }
+                double* vp = a.V + int64_t(p) * a.ldv;
+                double* vq = a.V + int64_t(q) * a.ldv;
+                for (int i = lane; i < n; i += 32) {
+                    const double xp = vp[i], xq = vq[i];
+                    vp[i] = c * xp - s * xq;
+                    vq[i] = s * xp + c * xq;
+                }
+                if (lane == 0) flags[sweep % 3] = 1;
+            }
+            grid.sync();
+        }
+        const int rotated = flags[sweep % 3];
+        ++sweep;
+        if (!rotated || n < 2) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) flags[4] = sweep;
+}
+
+// sigma_j = ||W(:,j)||, one warp per column (fixed order)
+__global__ void colnorm_kernel(const double* W, int64_t ldw, int m, int n, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = gw; j < n; j += nw) {
+        double s = 0.0;
+        for (int i = lane; i < m; i += 32) {
+            const double x = W[i + int64_t(j) * ldw];
+            s += x * x;
+        }
+        s = warp_sum(s);
+        if (lane == 0) out[j] = sqrt(s);
+    }
+}
+
+// stable descending rank of each key (std::stable_sort with '>')
+__global__ void rank_desc_kernel(const double* key, int n, int* rank) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const double kj = key[j];
+        int r = 0;
+        for (int i = 0; i < n; ++i) {
+            const double ki = key[i];
+            r += (ki > kj) || (ki == kj && i < j);
+        }
+        rank[j] = r;
+    }
+}
+
+// U(:, rank_j) = W(:, j)/sigma_j, V_out(:, rank_j) = V(:, j), sigma_out[rank_j]
+__global__ void svd_scatter_kernel(const double* W, int64_t ldw, int m, int n, const double* V,
+                                   int64_t ldv, int vrows, const double* sg, const int* rank,
+                                   double* U, int64_t ldu, double* Vo, int64_t ldvo,
+                                   double* sigma_out, int* needs) {
+    const int64_t tot = int64_t(max(m, vrows)) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(e / max(m, vrows)), i = int(e % max(m, vrows));
+        const int r = rank[j];
+        const double s = sg[j];
+        if (i < m) U[i + int64_t(r) * ldu] = s > 1e-300 ? W[i + int64_t(j) * ldw] / s : 0.0;
+        if (i < vrows) Vo[i + int64_t(r) * ldvo] = V[i + int64_t(j) * ldv];
+        if (i == 0) {
+            sigma_out[r] = s > 1e-300 ? s : 0.0;
+            needs[r] = s > 1e-300 ? 0 : 1;
+        }
+    }
+}
+
+__device__ double block_sum_fixed(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
+    __syncthreads();
+    return t;
+}
+
+// Orthonormal completion for sigma == 0 columns (reference jacobi.hpp:33-60),
+// one CTA, sequential over the columns that need it.  `done` scratch has n
+// ints, r scratch has m doubles.
+__global__ void completion_kernel(double* U, int64_t ldu, int m, int n, const int* needs, int* done,
+                                  double* r) {
+    __shared__ double sh[32];
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    __shared__ int nd;
+    if (threadIdx.x == 0) {
+        nd = 0;
+        for (int j = 0; j < n; ++j)
+            if (!needs[j]) done[nd++] = j;
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        if (!needs[j]) continue;
+        // best axis: smallest presence in the spanned set, first index wins
+        double bv = -2.0;
+        int bi = 0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            double proj2 = 0.0;
+            for (int c = 0; c < nd; ++c) {
+                const double u = U[i + int64_t(done[c]) * ldu];
+                proj2 += u * u;
+            }
+            const double res = 1.0 - proj2;
+            if (res > bv) {
+                bv = res;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            sv[threadIdx.x >> 5] = bv;
+            si[threadIdx.x >> 5] = bi;
+        }
+        __syncthreads();
+        int best = si[0];
+        double bestv = sv[0];
+        for (int w = 1; w < int(blockDim.x >> 5); ++w)
+            if (sv[w] > bestv || (sv[w] == bestv && si[w] < best)) {
+                bestv = sv[w];
+                best = si[w];
+            }
+        for (int i = threadIdx.x; i < m; i += blockDim.x) r[i] = (i == best) ? 1.0 : 0.0;
+        __syncthreads();
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int c = 0; c < nd; ++c) {
+                const double* uc = U + int64_t(done[c]) * ldu;
+                double s = 0.0;
+                for (int i = threadIdx.x; i < m; i += blockDim.x) s += uc[i] * r[i];
+                const double dot = block_sum_fixed(s, sh);
+                for (int i = threadIdx.x; i < m; i += blockDim.x) r[i] -= dot * uc[i];
+                __syncthreads();
+            }
+        }
+        double s = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) s += r[i] * r[i];
+        const double nrm = sqrt(block_sum_fixed(s, sh));
+        for (int i = threadIdx.x; i < m; i += blockDim.x) U[i + int64_t(j) * ldu] = r[i] / nrm;
+        __syncthreads();
+        if (threadIdx.x == 0) done[nd++] = j;
+        __syncthreads();
+    }
+}
+
+int coop_grid(Context& ctx, const void* kern, int want_blocks) {
+    int per_sm = 0;
+    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kJacThreads, 0));
+    const int cap = std::max(1, per_sm) * ctx.num_sms;
+    return std::max(1, std::min(want_blocks, cap));
+}
+
+// ---------------------------------------------------- two-sided Jacobi ---
+struct TwoSidedArgs {
+    double* M;
+    int64_t ldm;
+    int n;
+    double* U;
+    int64_t ldu;
+    double* cs;      // per-pair (c, s, active) triples: 3 * n2/2
+    double* part;    // per-block partials for the off-diagonal norm
+    double tnorm;
+    int* status;
+};
+
+__global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    const int n = a.n, n2 = n + (n & 1);
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    int sweep = 0;
+    const double thr = 1e-14 * fmax(a.tnorm, 1e-300);  // reference jacobi.hpp:99
+    for (;;) {
+        if (n <= 1) break;
+        // off-diagonal norm sqrt(sum_{i<j} 2 M_ij^2), fixed order
+        double v = 0.0;
+        for (int64_t e = gt; e < int64_t(n) * n; e += nt) {
+            const int i = int(e % n), j = int(e / n);
+            if (i < j) {
+                const double x = a.M[i + int64_t(j) * a.ldm];
+                v += 2.0 * x * x;
+            }
+        }
+        v = block_sum_fixed(v, sh);
+        if (threadIdx.x == 0) a.part[blockIdx.x] = v;
+        grid.sync();
+        double off = 0.0;
+        for (int b = 0; b < int(gridDim.x); ++b) off += a.part[b];
+        off = sqrt(off);
+        grid.sync();
+        if (!(off > thr)) break;
+        if (sweep++ >= kTwoSidedSweepCap) {
+            if (gt == 0) *a.status = RLRA_ECONV;
+            break;
+        }
+        for (int r = 0; r < n2 - 1; ++r) {
+            // angles for every disjoint pair of this round from the current M
+            for (int pi = gt; pi < n2 / 2; pi += nt) {
+                const int ca = rr_col(pi, r, n2), cb = rr_col(n2 - 1 - pi, r, n2);
+                const int p = min(ca, cb), q = max(ca, cb);
+                double c = 1.0, s = 0.0, act = 0.0;
+                if (q < n) {
+                    const double apq = a.M[p + int64_t(q) * a.ldm];
+                    if (fabs(apq) > 1e-300) {
+                        const double theta =
+                            (a.M[q + int64_t(q) * a.ldm] - a.M[p + int64_t(p) * a.ldm]) / (2.0 * apq);
+                        const double t = (theta >= 0.0 ? 1.0 : -1.0) /
+                                         (fabs(theta) + sqrt(1.0 + theta * theta));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        act = 1.0;
+                    }
+                }
+                a.cs[3 * pi] = c;
+                a.cs[3 * pi + 1] = s;
+                a.cs[3 * pi + 2] = act;
+            }
+            grid.sync();
+            // columns of M and U
+            for (int64_t e = gt; e < int64_t(n2 / 2) * n; e += nt) {
+                const int pi = int(e / n), i = int(e % n);
+                if (a.cs[3 * pi + 2] == 0.0) continue;
+                const int ca = rr_col(pi, r, n2), cb = rr_col(n2 - 1 - pi, r, n2);
+                const int p = min(ca, cb), q = max(ca, cb);
+                const double c = a.cs[3 * pi], s = a.cs[3 * pi + 1];
+                double* mp = a.M + int64_t(p) * a.ldm;
+                double* mq = a.M + int64_t(q) * a.ldm;
+                const double xp = mp[i], xq = mq[i];
+                mp[i] = c * xp - s * xq;
+                mq[i] = s * xp + c * xq;
+                double* up = a.U + int64_t(p) * a.ldu;
+                double* uq = a.U + int64_t(q) * a.ldu;
+                const double yp = up[i], yq = uq[i];
+                up[i] = c * yp - s * yq;
+                uq[i] = s * yp + c * yq;
+            }
+            grid.sync();
+            // rows of M
+            for (int64_t e = gt; e < int64_t(n2 / 2) * n; e += nt) {
+                const int pi = int(e / n), i = int(e % n);
+                if (a.cs[3 * pi + 2] == 0.0) continue;
+                const int ca = rr_col(pi, r, n2), cb = rr_col(n2 - 1 - pi, r, n2);
+                const int p = min(ca, cb), q = max(ca, cb);
+                const double c = a.cs[3 * pi], s = a.cs[3 * pi + 1];
+                const double xp = a.M[p + int64_t(i) * a.ldm], xq = a.M[q + int64_t(i) * a.ldm];
+                a.M[p + int64_t(i) * a.ldm] = c * xp - s * xq;
+                a.M[q + int64_t(i) * a.ldm] = s * xp + c * xq;
+            }
+            grid.sync();
+        }
+    }
+}
+
+__global__ void diag_of_kernel(const double* M, int64_t ldm, int n, double* d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        d[i] = M[i + int64_t(i) * ldm];
+}
+
+__global__ void eig_scatter_kernel(const double* d, const int* rank, const double* U, int64_t ldu,
+                                   int n, double* values, double* vec, int64_t ldv) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(n) * n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(e / n), i = int(e % n);
+        const int r = rank[j];
+        vec[i + int64_t(r) * ldv] = U[i + int64_t(j) * ldu];
+        if (i == 0) values[r] = d[j];
+    }
+}
+
+__global__ void asym_kernel(const double* T, int64_t ldt, int n, double* part) {
+    __shared__ double sh[32];
+    double v = 0.0;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(n) * n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % n), j = int(e / n);
+        if (i < j) v = fmax(v, fabs(T[i + int64_t(j) * ldt] - T[j + int64_t(i) * ldt]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t = fmax(t, sh[w]);
+        part[blockIdx.x] = t;
+    }
+}
+
+}  // namespace
+
+void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& Vout) {
+    const int m = int(A.rows), n = int(A.cols);
+    if (n == 0) return;
+    ProfScope prof(ctx, "small_svd", m, n, 0, 0.0);
+    DMatBuf W(ctx, m, n), V(ctx, n, n);
+    copy_mat(ctx, A, W);
+    eye_mat(ctx, V);
+    Buf flags(ctx, sizeof(int) * 8), sg(ctx, sizeof(double) * n), rank(ctx, sizeof(int) * n),
+        needs(ctx, sizeof(int) * n);
+    RLRA_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 8, ctx.stream));
+    OneSidedArgs a;
+    a.W = W.m.p;
+    a.ldw = W.m.ld;
+    a.m = m;
+    a.n = n;
+    a.V = V.m.p;
+    a.ldv = V.m.ld;
+    a.flags = flags.i();
+    const int pairs = (n + 1) / 2;
+    const int G = coop_grid(ctx, (const void*)onesided_jacobi_kernel, ceil_div(pairs, kJacThreads / 32));
+    void* args[] = {&a};
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)onesided_jacobi_kernel, dim3(G), dim3(kJacThreads),
+                                          args, 0, ctx.stream));
+    ++ctx.launches;
+    colnorm_kernel<<<ceil_div(n, 8), 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, sg.d());
+    rank_desc_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(sg.d(), n, rank.i());
+    const int64_t tot = int64_t(std::max(m, n)) * n;
+    svd_scatter_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, ctx.stream>>>(
+        W.m.p, W.m.ld, m, n, V.m.p, V.m.ld, n, sg.d(), rank.i(), U.p, U.ld, Vout.p, Vout.ld, sigma,
+        needs.i());
+    RLRA_LAUNCH_CHECK();
+    ctx.launches += 3;
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flags.p, sizeof(int) * 8, cudaMemcpyDeviceToHost,
+                              ctx.stream));
+    // any column needing completion?
+    Buf anyneed(ctx, sizeof(double));
+    {
+        // count needs on host: copy the n flags (small)
+        std::vector<int> h(n);
+        RLRA_CUDA(cudaMemcpyAsync(h.data(), needs.p, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                                  ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (ctx.h_flags[3] == RLRA_ECONV)
+            raise(RLRA_ECONV, fmt("small_svd: no convergence after %d sweeps on %dx%d input",
+                                  kOneSidedSweepCap, m, n));
+        bool any = false;
+        for (int j = 0; j < n; ++j) any |= h[j] != 0;
+        if (any) {
+            Buf done(ctx, sizeof(int) * n), r(ctx, sizeof(double) * m);
+            completion_kernel<<<1, 256, 0, ctx.stream>>>(U.p, U.ld, m, n, needs.i(), done.i(), r.d());
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+        }
+    }
+}
+
+void small_svd(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V) {
+    if (A.rows >= A.cols) return small_svd_tall(ctx, A, U, sigma, V);
+    DMatBuf At(ctx, A.cols, A.rows);
+    transpose_mat(ctx, A, At);
+    small_svd_tall(ctx, At, V, sigma, U);
+}
+
+void sym_eig(Context& ctx, const DMat& T, double* values, const DMat& vectors) {
+    const int n = int(T.rows);
+    if (n == 0) return;
+    // asymmetry guard (reference jacobi.hpp:76-84)
+    double hv[2];
+    Buf tn(ctx, sizeof(double)), part(ctx, sizeof(double) * 1024);
+    sum_squares(ctx, T, tn.d());
+    asym_kernel<<<64, 256, 0, ctx.stream>>>(T.p, T.ld, n, part.d());
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    std::vector<double> pm(64);
+    RLRA_CUDA(cudaMemcpyAsync(hv, tn.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaMemcpyAsync(pm.data(), part.p, sizeof(double) * 64, cudaMemcpyDeviceToHost,
+                              ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    const double tnorm = sqrt(hv[0]);
+    double asym = 0.0;
+    for (double x : pm) asym = std::max(asym, x);
+    if (tnorm > 0.0 && asym > 1e-12 * tnorm)
+        raise(RLRA_ENUM, fmt("sym_eig: asymmetry %.3e exceeds 1e-12 relative to norm %.3e", asym,
+                             tnorm));
+    DMatBuf M(ctx, n, n), Uacc(ctx, n, n);
+    copy_mat(ctx, T, M);
+    eye_mat(ctx, Uacc);
+    const int n2 = n + (n & 1);
+    Buf cs(ctx, sizeof(double) * 3 * (n2 / 2 + 1)), status(ctx, sizeof(int)), d(ctx, sizeof(double) * n),
+        rank(ctx, sizeof(int) * n);
+    RLRA_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), ctx.stream));
+    const int G = coop_grid(ctx, (const void*)twosided_jacobi_kernel,
+                            std::max(1, std::min(ctx.num_sms, ceil_div(int64_t(n) * n, 4 * kJacThreads))));
+    Buf part2(ctx, sizeof(double) * G);
+    TwoSidedArgs a;
+    a.M = M.m.p;
+    a.ldm = M.m.ld;
+    a.n = n;
+    a.U = Uacc.m.p;
+    a.ldu = Uacc.m.ld;
+    a.cs = cs.d();
+    a.part = part2.d();
+    a.tnorm = tnorm;
+    a.status = status.i();
+    void* args[] = {&a};
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)twosided_jacobi_kernel, dim3(G), dim3(kJacThreads),
+                                          args, 0, ctx.stream));
+    ++ctx.launches;
+    diag_of_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(M.m.p, M.m.ld, n, d.d());
+    rank_desc_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(d.d(), n, rank.i());
+    eig_scatter_kernel<<<int(std::min<int64_t>((int64_t(n) * n + 255) / 256, 4096)), 256, 0,
+                         ctx.stream>>>(d.d(), rank.i(), Uacc.m.p, Uacc.m.ld, n, values, vectors.p,
+                                       vectors.ld);
+    RLRA_LAUNCH_CHECK();
+    ctx.launches += 3;
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (ctx.h_flags[0] == RLRA_ECONV)
+        raise(RLRA_ECONV, fmt("sym_eig: no convergence after %d sweeps (matrix norm %.3e)",
+                              kTwoSidedSweepCap, tnorm));
+}
+
+}  // namespace rlra_b200

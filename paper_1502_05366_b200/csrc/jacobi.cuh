@@ -1,0 +1,28 @@
+// jacobi.cuh — small dense SVD / symmetric eigensolver (K5/K6 of SURVEY.md §2.2).
+//
+// small_svd restates reference core/jacobi.hpp:145-232: one-sided (Hestenes)
+// Jacobi with the same rotation formula, the same skip rule
+// |a_pq| <= 1e-15 sqrt(a_pp a_qq) (or a zero column), the same stopping rule
+// (a sweep without rotations) and the same 60-sweep cap, stable descending
+// sort and orthonormal completion for sigma <= 1e-300 (:33-60).  The pair
+// order is the parallel round-robin tournament instead of the serial cyclic
+// order, so every round's n/2 rotations run concurrently (one warp per pair)
+// inside one cooperative kernel.
+#pragma once
+
+#include "common.cuh"
+
+namespace rlra_b200 {
+
+// A (m x n, m >= n) -> U (m x n), sigma (n, device), V (n x n).  A is not
+// modified.  Throws ConvergenceError after 60 sweeps.
+void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V);
+
+// Any shape: r = min(m,n); U (m x r), V (n x r) (jacobi.hpp:148-152).
+void small_svd(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V);
+
+// Symmetric eigendecomposition by cyclic two-sided Jacobi (jacobi.hpp:68-139):
+// values descending (device), vectors n x n.
+void sym_eig(Context& ctx, const DMat& T, double* values, const DMat& vectors);
+
+}  // namespace rlra_b200

@@ -1,0 +1,410 @@
+// qr.cu — CholQR2 orthonormalization with a device Householder fallback.
+#include <cooperative_groups.h>
+
+#include "gemm.cuh"
+#include "qr.cuh"
+#include "reduce.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rlra_b200 {
+
+namespace {
+
+constexpr int kCholNB = 64;
+
+// Factor the diagonal block G[j0:j0+nb, j0:j0+nb] (upper triangle read) in
+// shared memory: R_jj (written back, lower zeroed) and R_jj^{-1} (into Rinv).
+// A pivot d_k that is not positive or is below floor * dorig[k] sets *flag.
+__global__ void __launch_bounds__(256) chol_diag_kernel(double* G, int64_t ldg, int j0, int nb,
+                                                        double* Rinv, int64_t ldri,
+                                                        const double* dorig, double floor,
+                                                        int* flag) {
+    extern __shared__ double chol_smem[];
+    double(*a)[kCholNB + 1] = reinterpret_cast<double(*)[kCholNB + 1]>(chol_smem);
+    double(*x)[kCholNB + 1] = reinterpret_cast<double(*)[kCholNB + 1]>(chol_smem + kCholNB * (kCholNB + 1));
+    __shared__ int bad;
+    const int t = threadIdx.x;
+    if (t == 0) bad = 0;
+    for (int e = t; e < nb * nb; e += blockDim.x) {
+        const int i = e % nb, j = e / nb;
+        a[i][j] = (i <= j) ? G[(j0 + i) + int64_t(j0 + j) * ldg] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        if (t == 0) {
+            double d = a[k][k];
+            const double ref = dorig[j0 + k];
+            if (!(d > 0.0) || !(d >= floor * ref)) {
+                bad = 1;
+                d = fmax(d, 1e-300);
+            }
+            a[k][k] = sqrt(d);
+        }
+        __syncthreads();
+        const double rkk = a[k][k];
+        for (int j = k + 1 + t; j < nb; j += blockDim.x) a[k][j] /= rkk;
+        __syncthreads();
+        const int rem = nb - k - 1;
+        for (int e = t; e < rem * rem; e += blockDim.x) {
+            const int i = k + 1 + e % rem, j = k + 1 + e / rem;
+            if (i <= j) a[i][j] -= a[k][i] * a[k][j];
+        }
+        __syncthreads();
+    }
+    // X = R^{-1}: one thread per column j, back substitution upward.
+    if (t < nb) {
+        const int j = t;
+        for (int i = 0; i < nb; ++i) x[i][j] = 0.0;
+        x[j][j] = 1.0 / a[j][j];
+        for (int i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int l = i + 1; l <= j; ++l) s += a[i][l] * x[l][j];
+            x[i][j] = -s / a[i][i];
+        }
+    }
+    __syncthreads();
+    for (int e = t; e < nb * nb; e += blockDim.x) {
+        const int i = e % nb, j = e / nb;
+        G[(j0 + i) + int64_t(j0 + j) * ldg] = (i <= j) ? a[i][j] : 0.0;
+        Rinv[(j0 + i) + int64_t(j0 + j) * ldri] = (i <= j) ? x[i][j] : 0.0;
+    }
+    if (t == 0 && bad) *flag = 1;
+}
+
+__global__ void diag_copy_kernel(const double* G, int64_t ldg, int n, double* d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        d[i] = G[i + int64_t(i) * ldg];
+}
+
+__global__ void zero_lower_kernel(double* G, int64_t ldg, int n) {
+    const int64_t total = int64_t(n) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % n), j = int(e / n);
+        if (i > j) G[i + int64_t(j) * ldg] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------ Householder ---
+// Cooperative device Householder QR restating reference core/qr.hpp:44-121:
+// householder_step (:44-66), apply_reflector (:69-79), form_q (:82-89) and
+// the sign convention (:113-119).  Rows are partitioned over CTAs; every
+// column costs three grid barriers (norm, dots, update).
+struct HhArgs {
+    double* W;
+    int64_t ldw;
+    int m, n;
+    double* V;      // m x n reflectors, ld m
+    double* beta;   // n
+    double* part;   // G x n partials
+    double* dots;   // n
+    int* degenerate;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) t += sh[i];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    const int G = gridDim.x, g = blockIdx.x;
+    const int rows_per = (a.m + G - 1) / G;
+    const int r0 = g * rows_per, r1 = min(a.m, r0 + rows_per);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int n = a.n;
+    double* W = a.W;
+    const int64_t ldw = a.ldw;
+
+    for (int k = 0; k < n; ++k) {
+        // P1: partial ||W(k:m, k)||^2 over own rows
+        double v = 0.0;
+        for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x) {
+            const double w = W[i + int64_t(k) * ldw];
+            v += w * w;
+        }
+        v = block_sum(v, sh);
+        if (threadIdx.x == 0) a.part[g] = v;
+        grid.sync();
+        // P2: reflector (every CTA computes the same scalars in the same order)
+        double norm2 = 0.0;
+        for (int c = 0; c < G; ++c) norm2 += a.part[c];
+        const double x1 = W[k + int64_t(k) * ldw];
+        const double norm = sqrt(norm2);
+        const bool zero = norm < 1e-300;
+        const double alpha = x1 >= 0.0 ? -norm : norm;
+        const double beta = zero ? 0.0 : 2.0 / (2.0 * (norm2 - alpha * x1));
+        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            double vi = 0.0;
+            if (!zero) vi = i > k ? W[i + int64_t(k) * ldw] : (i == k ? x1 - alpha : 0.0);
+            a.V[i + int64_t(k) * a.m] = vi;
+        }
+        __syncthreads();
+        if (!zero) {
+            for (int j = k + 1 + warp; j < n; j += nwarps) {
+                double s = 0.0;
+                for (int i = max(r0, k) + lane; i < r1; i += 32)
+                    s += a.V[i + int64_t(k) * a.m] * W[i + int64_t(j) * ldw];
+                s = warp_sum(s);
+                if (lane == 0) a.part[int64_t(G) + int64_t(g) * n + j] = s;
+            }
+        }
+        grid.sync();
+        // P3: reduce the trailing dots, columns distributed over CTAs
+        if (!zero) {
+            for (int j = k + 1 + g * blockDim.x + threadIdx.x; j < n; j += G * blockDim.x) {
+                double s = 0.0;
+                for (int c = 0; c < G; ++c) s += a.part[int64_t(G) + int64_t(c) * n + j];
+                a.dots[j] = s;
+            }
+        }
+        grid.sync();
+        // P4: apply H_k to own rows of the trailing columns, finish column k
+        if (!zero) {
+            for (int j = k + 1; j < n; ++j) {
+                const double f = beta * a.dots[j];
+                for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x)
+                    W[i + int64_t(j) * ldw] -= f * a.V[i + int64_t(k) * a.m];
+            }
+        }
+        for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x)
+            W[i + int64_t(k) * ldw] = (i == k) ? (zero ? 0.0 : alpha) : 0.0;
+        if (g == 0 && threadIdx.x == 0) {
+            a.beta[k] = beta;
+            if (zero) *a.degenerate = 1;
+        }
+        __syncthreads();
+    }
+}
+
+// form_q (reference core/qr.hpp:82-89): Q = H_0 ... H_{r-1} [I_r; 0], the
+// reflectors (columns of V, scalars beta) applied in reverse order.  Rows are
+// partitioned over CTAs; two grid barriers per reflector.
+struct FormQArgs {
+    const double* V;
+    int64_t ldv;
+    const double* beta;
+    int m, r;
+    double* part;  // G x r
+    double* dots;  // r
+    double* Q;
+    int64_t ldq;
+};
+
+__global__ void __launch_bounds__(256) formq_coop_kernel(FormQArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, g = blockIdx.x;
+    const int rows_per = (a.m + G - 1) / G;
+    const int r0 = g * rows_per, r1 = min(a.m, r0 + rows_per);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int n = a.r;
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+        for (int j = 0; j < n; ++j) a.Q[i + int64_t(j) * a.ldq] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int k = n - 1; k >= 0; --k) {
+        const double beta = a.beta[k];
+        if (beta == 0.0) continue;  // uniform across CTAs
+        for (int j = k + warp; j < n; j += nwarps) {
+            double s = 0.0;
+            for (int i = max(r0, k) + lane; i < r1; i += 32)
+                s += a.V[i + int64_t(k) * a.ldv] * a.Q[i + int64_t(j) * a.ldq];
+            s = warp_sum(s);
+            if (lane == 0) a.part[int64_t(g) * n + j] = s;
+        }
+        grid.sync();
+        for (int j = k + g * blockDim.x + threadIdx.x; j < n; j += G * blockDim.x) {
+            double s = 0.0;
+            for (int c = 0; c < G; ++c) s += a.part[int64_t(c) * n + j];
+            a.dots[j] = s;
+        }
+        grid.sync();
+        for (int j = k; j < n; ++j) {
+            const double f = beta * a.dots[j];
+            for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x)
+                a.Q[i + int64_t(j) * a.ldq] -= f * a.V[i + int64_t(k) * a.ldv];
+        }
+        __syncthreads();
+    }
+}
+
+// R = W(0:n, 0:n) upper; sign fix diag(R) >= 0 (core/qr.hpp:113-119).
+__global__ void hh_finish_kernel(const double* W, int64_t ldw, int m, int n, double* Q, int64_t ldq,
+                                 double* R, int64_t ldr) {
+    const int64_t totq = int64_t(m) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < totq;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % m), j = int(e / m);
+        if (W[j + int64_t(j) * ldw] < 0.0) Q[i + int64_t(j) * ldq] = -Q[i + int64_t(j) * ldq];
+        if (R && i < n) {
+            const double s = W[i + int64_t(i) * ldw] < 0.0 ? -1.0 : 1.0;
+            R[i + int64_t(j) * ldr] = (i <= j) ? s * W[i + int64_t(j) * ldw] : 0.0;
+        }
+    }
+}
+
+}  // namespace
+
+void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int m, int r,
+            const DMat& Q) {
+    if (r == 0) return;
+    int G = std::max(1, std::min(ctx.num_sms, m / 256));
+    int per_sm = 0;
+    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, formq_coop_kernel, 256, 0));
+    G = std::min(G, std::max(1, per_sm) * ctx.num_sms);
+    Buf part(ctx, sizeof(double) * size_t(G) * r), dots(ctx, sizeof(double) * r);
+    FormQArgs a;
+    a.V = V;
+    a.ldv = ldv;
+    a.beta = beta;
+    a.m = m;
+    a.r = r;
+    a.part = part.d();
+    a.dots = dots.d();
+    a.Q = Q.p;
+    a.ldq = Q.ld;
+    void* args[] = {&a};
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)formq_coop_kernel, dim3(G), dim3(256), args, 0,
+                                          ctx.stream));
+    ++ctx.launches;
+}
+
+bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
+    const int n = int(G.rows);
+    Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
+    RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    diag_copy_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(G.p, G.ld, n, dorig.d());
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    zero_mat(ctx, Rinv);
+    for (int j0 = 0; j0 < n; j0 += kCholNB) {
+        const int nb = std::min(kCholNB, n - j0), j1 = j0 + nb;
+        constexpr int smem = 2 * kCholNB * (kCholNB + 1) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            RLRA_CUDA(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = true;
+        }
+        chol_diag_kernel<<<1, 256, smem, ctx.stream>>>(G.p, G.ld, j0, nb, Rinv.p, Rinv.ld, dorig.d(),
+                                                    floor, flag.i());
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        if (j1 < n) {
+            const int rest = n - j1;
+            DMatBuf P(ctx, nb, rest);
+            // P = R_jj^{-T} G[j0:j1, j1:n]
+            gemm(ctx, Op::T, Op::N, 1.0, Rinv.block(j0, j0, nb, nb), G.block(j0, j1, nb, rest), 0.0,
+                 P);
+            // G[j1:, j1:] -= P^T P (upper tiles)
+            GemmOpts o;
+            o.upper_tiles_only = true;
+            gemm(ctx, Op::T, Op::N, -1.0, P, P, 1.0, G.block(j1, j1, rest, rest), o);
+            copy_mat(ctx, P, G.block(j0, j1, nb, rest));
+        }
+    }
+    zero_lower_kernel<<<ceil_div(int64_t(n) * n, 256) > 1024 ? 1024 : ceil_div(int64_t(n) * n, 256),
+                        256, 0, ctx.stream>>>(G.p, G.ld, n);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    // off-diagonal blocks of R^{-1}: Rinv[0:j0, J] = -Rinv[0:j0,0:j0] R[0:j0,J] Rinv[J,J]
+    for (int j0 = kCholNB; j0 < n; j0 += kCholNB) {
+        const int nb = std::min(kCholNB, n - j0);
+        DMatBuf T(ctx, j0, nb);
+        gemm(ctx, Op::N, Op::N, 1.0, Rinv.block(0, 0, j0, j0), G.block(0, j0, j0, nb), 0.0, T);
+        gemm(ctx, Op::N, Op::N, -1.0, T, Rinv.block(j0, j0, nb, nb), 0.0, Rinv.block(0, j0, j0, nb));
+    }
+    int h_flag = 0;
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    h_flag = ctx.h_flags[0];
+    return h_flag == 0;
+}
+
+QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R) {
+    const int m = int(Y.rows), n = int(Y.cols);
+    QrResult res;
+    res.used_householder = true;
+    if (n == 0) return res;
+    int G = std::max(1, std::min(ctx.num_sms, m / 256));
+    {
+        int per_sm = 0;
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, householder_coop_kernel,
+                                                                256, 0));
+        G = std::min(G, std::max(1, per_sm) * ctx.num_sms);
+    }
+    DMatBuf W(ctx, m, n), V(ctx, m, n);
+    copy_mat(ctx, Y, W);
+    Buf beta(ctx, sizeof(double) * n), part(ctx, sizeof(double) * (size_t(G) + size_t(G) * n)),
+        dots(ctx, sizeof(double) * n), deg(ctx, sizeof(int));
+    RLRA_CUDA(cudaMemsetAsync(deg.p, 0, sizeof(int), ctx.stream));
+    HhArgs a;
+    a.W = W.m.p;
+    a.ldw = W.m.ld;
+    a.m = m;
+    a.n = n;
+    a.V = V.m.p;
+    a.beta = beta.d();
+    a.part = part.d();
+    a.dots = dots.d();
+    a.degenerate = deg.i();
+    void* args[] = {&a};
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)householder_coop_kernel, dim3(G), dim3(256), args, 0,
+                                          ctx.stream));
+    ++ctx.launches;
+    form_q(ctx, V.m.p, V.m.ld, beta.d(), m, n, Y);
+    const int blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, int64_t(ctx.num_sms) * 8));
+    hh_finish_kernel<<<blocks, 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, Y.p, Y.ld,
+                                                     R ? R->p : nullptr, R ? R->ld : 0);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, deg.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    res.degenerate = ctx.h_flags[0] != 0;
+    return res;
+}
+
+QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
+    const int m = int(Y.rows), n = int(Y.cols);
+    ProfScope prof(ctx, "orth", m, n, 0, 0.0);
+    if (m < n)
+        raise(RLRA_EDIM, fmt("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
+    QrResult res;
+    if (n == 0) return res;
+    // pass 1: G1 = Y^T Y, R1, R1^{-1}
+    DMatBuf G1(ctx, n, n), R1i(ctx, n, n);
+    GemmOpts sy;
+    sy.upper_tiles_only = true;
+    gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G1, sy);
+    if (!chol_upper_inv(ctx, G1, R1i, ctx.cholqr_pivot_floor)) return householder_qr(ctx, Y, R);
+    DMatBuf Q1(ctx, m, n);
+    GemmOpts tri;
+    tri.tri_b_upper = true;
+    gemm(ctx, Op::N, Op::N, 1.0, Y, R1i, 0.0, Q1, tri);
+    // pass 2 on Q1
+    DMatBuf G2(ctx, n, n), R2i(ctx, n, n);
+    gemm(ctx, Op::T, Op::N, 1.0, Q1, Q1, 0.0, G2, sy);
+    if (!chol_upper_inv(ctx, G2, R2i, ctx.cholqr_pivot_floor)) return householder_qr(ctx, Y, R);
+    gemm(ctx, Op::N, Op::N, 1.0, Q1, R2i, 0.0, Y, tri);
+    if (R) {
+        // R = R2 * R1 (both upper): B = R1 upper triangular
+        gemm(ctx, Op::N, Op::N, 1.0, G2, G1, 0.0, *R, tri);
+    }
+    return res;
+}
+
+}  // namespace rlra_b200

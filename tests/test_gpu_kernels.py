@@ -1,0 +1,215 @@
+"""Kernel-level parity: the CUDA engine against the CPU oracle (oracle/,
+bit-identical to the reference) on the same seeded inputs.  Tolerances are the
+reference's own test tolerances (tests/test_matmul.cpp:30-56,
+tests/test_qr.cpp:32-64, tests/test_jacobi.cpp:110-142)."""
+import numpy as np
+import pytest
+
+import paper_1502_05366_b200 as R
+from helpers import exact_rank, match_columns_up_to_sign, orthonormality_defect, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(5, 3, 4), (37, 29, 53), (130, 70, 300), (257, 190, 1000),
+                                   (1001, 211, 777)])
+def test_matmul_four_cases_vs_oracle(eng, orc, ta, tb, m, n, k):
+    rs = np.random.default_rng(m * 7 + n + k + 3 * ta + tb)
+    a = rs.standard_normal((k, m) if ta else (m, k))
+    b = rs.standard_normal((n, k) if tb else (k, n))
+    got = eng.matmul(a, b, bool(ta), bool(tb))
+    want = orc.matmul(a, b, ta, tb)
+    assert got.shape == want.shape
+    assert rel_fro(got, want) <= 1e-13  # test_matmul.cpp:30-39
+
+
+def test_matmul_hand_arithmetic(eng):
+    a = np.array([[1.0, 2.0], [3.0, 4.0]])
+    b = np.array([[5.0, 6.0], [7.0, 8.0]])
+    np.testing.assert_array_equal(eng.matmul(a, b), np.array([[19.0, 22.0], [43.0, 50.0]]))
+
+
+def test_matmul_shape_error_names_both_shapes(eng):
+    with pytest.raises(R.DimensionError) as e:
+        eng.matmul(np.zeros((3, 4)), np.zeros((5, 2)))
+    assert "3x4" in str(e.value) and "5x2" in str(e.value)
+
+
+def test_matmul_bitwise_deterministic(eng):
+    rs = np.random.default_rng(5)
+    a = rs.standard_normal((3000, 700))
+    b = rs.standard_normal((700, 300))
+    x = eng.matmul(a, b)
+    for _ in range(3):
+        assert np.array_equal(eng.matmul(a, b), x)
+    c = rs.standard_normal((3000, 300))
+    y = eng.matmul(a, c, True, False)  # split-K path: deterministic reduction order
+    for _ in range(3):
+        assert np.array_equal(eng.matmul(a, c, True, False), y)
+
+
+def test_orth_kat_and_conventions(eng):
+    q = eng.orth(np.array([[3.0], [4.0]]))
+    assert abs(q[0, 0] - 0.6) <= 1e-15 and abs(q[1, 0] - 0.8) <= 1e-15  # test_qr.cpp:14-20
+
+
+@pytest.mark.parametrize("m,n", [(50, 8), (40, 10), (2000, 210), (5000, 300)])
+def test_compact_qr_vs_oracle(eng, orc, m, n):
+    rs = np.random.default_rng(m + n)
+    a = rs.standard_normal((m, n))
+    q, r, deg = eng.compact_qr(a)
+    qo, ro, _ = orc.compact_qr(a)
+    assert not deg
+    assert orthonormality_defect(q) <= 1e-13 * np.sqrt(n)
+    assert rel_fro(q @ r, a) <= 1e-13
+    assert np.all(np.diag(r) >= 0) and np.all(np.tril(r, -1) == 0)
+    assert rel_fro(q, qo) <= 1e-12  # diag(R) >= 0 makes Q unique
+    assert rel_fro(r, ro) <= 1e-12
+
+
+def test_compact_qr_exact_dependence_and_zero_column(eng):
+    rs = np.random.default_rng(24)
+    c = rs.standard_normal((30, 1))
+    a = np.hstack([c, c])
+    _, r, _ = eng.compact_qr(a)
+    assert abs(r[1, 1]) <= 1e-12 * np.linalg.norm(a)  # test_qr.cpp:66-72
+    c = rs.standard_normal((6, 1))
+    a = np.hstack([c, np.zeros((6, 1))])
+    q, r, deg = eng.compact_qr(a)
+    assert deg and r[1, 1] == 0.0  # test_qr.cpp:74-83
+    assert orthonormality_defect(q) <= 1e-13
+
+
+def test_compact_qr_upper_triangular_fixed_point(eng):
+    a = np.array([[2.0, 1.0, 0.5], [0.0, 3.0, 1.5], [0.0, 0.0, 1.0]])
+    q, r, _ = eng.compact_qr(a)
+    assert np.max(np.abs(q - np.eye(3))) <= 1e-14
+    assert np.max(np.abs(r - a)) <= 1e-14
+
+
+def test_compact_qr_rank_deficient_tall_falls_back(eng):
+    a = exact_rank(400, 60, 7, 3)
+    q, r, _ = eng.compact_qr(a)
+    assert orthonormality_defect(q) <= 1e-12
+    assert rel_fro(q @ r, a) <= 1e-13
+
+
+def test_orth_rejects_wide(eng):
+    with pytest.raises(R.DimensionError):
+        eng.orth(np.zeros((3, 5)))
+
+
+@pytest.mark.parametrize("m,n,k", [(60, 40, 15), (35, 50, 20), (50, 30, 25), (610, 3000, 610)])
+def test_pivoted_qr_vs_oracle(eng, orc, m, n, k):
+    rs = np.random.default_rng(m * 3 + n)
+    a = rs.standard_normal((m, n))
+    got = eng.pivoted_qr_partial(a, k)
+    want = orc.pivoted_qr(a, k)
+    assert got["frank"] == want["frank"] == k
+    np.testing.assert_array_equal(got["perm"], want["perm"])
+    assert rel_fro(got["s1"], want["s1"]) <= 1e-11
+    assert abs(got["residual"] - want["residual"]) <= 1e-10 * max(1.0, want["residual"])
+    assert rel_fro(got["q1"], want["q1"]) <= 1e-11
+
+
+def test_pivoted_qr_kats(eng):
+    f = eng.pivoted_qr_partial(np.diag([3.0, 2.0, 1.0]), 2)
+    assert f["frank"] == 2 and list(f["perm"][:2]) == [0, 1]
+    assert abs(f["residual"] - 1.0) <= 1e-14  # test_qr.cpp:85-92
+    rs = np.random.default_rng(26)
+    a = rs.standard_normal((20, 2)) @ rs.standard_normal((20, 2)).T
+    f = eng.pivoted_qr_partial(a, 0, 1e-10)
+    assert f["frank"] == 2 and f["tolerance_reached"]  # :94-102
+    f = eng.pivoted_qr_partial(rs.standard_normal((12, 12)), 0, 1e-20)
+    assert f["frank"] == 12 and not f["tolerance_reached"] and f["residual"] > 1e-20
+    for k, tol in [(2, 1e-3), (0, 0.0), (5, 0.0)]:
+        with pytest.raises(R.DimensionError):
+            eng.pivoted_qr_partial(np.zeros((4, 4)), k, tol)
+
+
+def test_pivoted_qr_tol_mode_vs_oracle(eng, orc):
+    rs = np.random.default_rng(77)
+    a = rs.standard_normal((40, 6)) @ np.diag(np.logspace(0, -6, 6)) @ rs.standard_normal((6, 30))
+    got = eng.pivoted_qr_partial(a, 0, 1e-4)
+    want = orc.pivoted_qr(a, 0, 1e-4)
+    assert got["frank"] == want["frank"]
+    np.testing.assert_array_equal(got["perm"][: got["frank"]], want["perm"][: want["frank"]])
+    assert got["tolerance_reached"] == want["reached"]
+
+
+def test_upper_tri_solve(eng, orc):
+    t, cl = eng.upper_tri_solve(np.array([[2.0, 1.0], [0.0, 1.0]]), np.array([[3.0], [1.0]]))
+    assert not cl and np.allclose(t, [[1.0], [1.0]], atol=1e-15)
+    t, cl = eng.upper_tri_solve(np.eye(3), np.arange(6.0).reshape(3, 2))
+    assert np.array_equal(t, np.arange(6.0).reshape(3, 2)) and not cl
+    t, cl = eng.upper_tri_solve(np.array([[1e8, 0.0], [0.0, 1e-8]]), np.array([[1.0], [1.0]]))
+    assert cl and abs(t[0, 0] - 1e-8) <= 1e-20 and t[1, 0] == 1e4  # test_qr.cpp:203-219
+    t, cl = eng.upper_tri_solve(np.eye(2), np.array([[1e5], [2e5]]))
+    assert not cl and t[1, 0] == 2e5
+    with pytest.raises(R.NumericalError):
+        eng.upper_tri_solve(np.array([[1.0, 2.0], [0.0, 0.0]]), np.ones((2, 1)))
+    rs = np.random.default_rng(30)
+    s11 = np.triu(rs.standard_normal((600, 600))) + 30 * np.eye(600)
+    s12 = rs.standard_normal((600, 900))
+    got, _ = eng.upper_tri_solve(s11, s12)
+    want, _ = orc.upper_tri_solve(s11, s12)
+    assert rel_fro(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(40, 40), (60, 25), (25, 60), (210, 210), (510, 510), (3, 1), (1, 3)])
+def test_small_svd_vs_oracle(eng, orc, m, n):
+    rs = np.random.default_rng(m * 11 + n)
+    a = rs.standard_normal((m, n))
+    u, s, v = eng.small_svd(a)
+    uo, so, vo = orc.small_svd(a)
+    r = min(m, n)
+    assert u.shape == (m, r) and v.shape == (n, r)
+    assert np.all(np.diff(s) <= 0)
+    assert np.max(np.abs(s - so) / so[0]) <= 1e-13
+    assert rel_fro((u * s) @ v.T, a) <= 1e-12  # test_jacobi.cpp:110-142
+    assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
+    assert match_columns_up_to_sign(u, uo) <= 1e-8
+
+
+def test_small_svd_kats(eng):
+    _, s, _ = eng.small_svd(np.diag([2.0, -3.0]))
+    assert np.allclose(s, [3.0, 2.0], rtol=1e-15)  # test_jacobi.cpp:95-101
+    a = np.zeros((5, 3))
+    a[:, 0] = [1, 2, 3, 4, 5]
+    u, s, v = eng.small_svd(a)
+    assert s[1] == 0.0 and s[2] == 0.0
+    assert orthonormality_defect(u) <= 1e-13  # completion (test_jacobi.cpp:154-163)
+
+
+@pytest.mark.parametrize("n", [2, 7, 40, 211])
+def test_sym_eig_vs_oracle(eng, orc, n):
+    rs = np.random.default_rng(n)
+    b = rs.standard_normal((n, n))
+    t = b @ b.T
+    d, e = eng.sym_eig(t)
+    do, eo = orc.sym_eig(t)
+    assert np.all(np.diff(d) <= 0)
+    assert np.max(np.abs(d - do)) <= 1e-12 * abs(do[0])
+    assert rel_fro(e @ np.diag(d) @ e.T, t) <= 1e-12
+
+
+def test_sym_eig_rejects_asymmetry(eng):
+    with pytest.raises(R.NumericalError):
+        eng.sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]))
+
+
+def test_frobenius_norm(eng):
+    rs = np.random.default_rng(9)
+    a = rs.standard_normal((1234, 567))
+    assert abs(eng.frobenius_norm(a) - np.linalg.norm(a)) <= 1e-13 * np.linalg.norm(a)
+
+
+def test_philox_omega_is_gaussian_and_deterministic(eng):
+    g = eng.gaussian_philox(4000, 64, seed=12345)
+    assert np.array_equal(g, eng.gaussian_philox(4000, 64, seed=12345))
+    assert abs(g.mean()) < 0.01 and abs(g.std() - 1.0) < 0.01
+    # row offset addresses the same global stream
+    h = eng.gaussian_philox(1000, 64, seed=12345, row0=1000)
+    assert np.array_equal(h, g[1000:2000])
+    assert not np.array_equal(eng.gaussian_philox(100, 8, seed=1), eng.gaussian_philox(100, 8, seed=2))
