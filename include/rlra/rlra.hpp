@@ -1,0 +1,728 @@
+// rlra/rlra.hpp — drop-in C++ API for the B200 engine.
+//
+// Re-declares the reference's public API (namespace rlra, reference
+// proj/include/rlra/*.hpp) with the same names, signatures, value types and
+// exception classes, and implements every numerical entry point by calling
+// the C-ABI in rlra_c.h, i.e. on the GPU.  A program written against the
+// reference switches by putting this include directory first and linking
+// librlra_b200.so.  Per-file forwarding headers (rlra/rsvd.hpp,
+// rlra/core/qr.hpp, ...) exist so the reference's include lines keep working.
+//
+// Host-side pieces kept on the host exactly as the reference has them: the
+// DenseMatrix/Permutation value types and their copy helpers, and RngState
+// (the Omega stream is the reference's, drawn on the host and uploaded:
+// parity mode, rlra_c.h RLRA_OMEGA_CALLBACK).
+//
+// Context: each host thread lazily opens one engine context on device
+// $RLRA_DEVICE (default 0).  config::set_threads is accepted and ignored
+// for the GPU path (it only sized the reference's CPU matmul fan-out).
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstddef>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <initializer_list>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../rlra_c.h"
+
+namespace rlra {
+
+// ------------------------------------------------------------- errors ---
+// reference core/errors.hpp:11-33
+struct Error : std::runtime_error {
+    explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+struct DimensionError : Error {
+    using Error::Error;
+};
+struct NumericalError : Error {
+    using Error::Error;
+};
+struct ConvergenceError : Error {
+    using Error::Error;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+
+namespace detail {
+inline std::string msg(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    return buf;
+}
+
+[[noreturn]] inline void throw_status(rlra_status st) {
+    const std::string m = rlra_last_error();
+    switch (st) {
+        case RLRA_EDIM: throw DimensionError(m);
+        case RLRA_ENUM: throw NumericalError(m);
+        case RLRA_ECONV: throw ConvergenceError(m);
+        case RLRA_EIO: throw IoError(m);
+        default: throw Error(m);
+    }
+}
+inline void check(rlra_status st) {
+    if (st != RLRA_OK) throw_status(st);
+}
+
+struct CtxHolder {
+    rlra_ctx* ctx = nullptr;
+    ~CtxHolder() {
+        if (ctx) rlra_ctx_destroy(ctx);
+    }
+};
+inline rlra_ctx* ctx() {
+    thread_local CtxHolder h;
+    if (!h.ctx) {
+        const char* d = std::getenv("RLRA_DEVICE");
+        check(rlra_ctx_create(d ? std::atoi(d) : 0, &h.ctx));
+    }
+    return h.ctx;
+}
+}  // namespace detail
+
+// ------------------------------------------------------------- config ---
+namespace config {
+inline std::atomic<int>& thread_count_ref() {
+    static std::atomic<int> n{1};
+    return n;
+}
+inline void set_threads(int n) { thread_count_ref().store(std::max(1, n)); }
+inline int threads() { return thread_count_ref().load(); }
+}  // namespace config
+
+// ------------------------------------------------------- value types ---
+// Column-major doubles, element (i,j) at data()[i + j*rows()]
+// (reference core/matrix.hpp:17-80).
+class DenseMatrix {
+public:
+    DenseMatrix() = default;
+    DenseMatrix(int rows, int cols) : r_(rows), c_(cols) {
+        if (rows < 0 || cols < 0)
+            throw DimensionError(detail::msg("DenseMatrix: negative dimensions %dx%d", rows, cols));
+        v_.assign(std::size_t(rows) * std::size_t(cols), 0.0);
+    }
+    DenseMatrix(std::initializer_list<std::initializer_list<double>> rows_list) {
+        r_ = int(rows_list.size());
+        c_ = r_ ? int(rows_list.begin()->size()) : 0;
+        v_.assign(std::size_t(r_) * c_, 0.0);
+        int i = 0;
+        for (const auto& row : rows_list) {
+            if (int(row.size()) != c_) throw DimensionError("DenseMatrix: ragged initializer list");
+            int j = 0;
+            for (double x : row) (*this)(i, j++) = x;
+            ++i;
+        }
+    }
+    static DenseMatrix identity(int n) {
+        DenseMatrix e(n, n);
+        for (int i = 0; i < n; ++i) e(i, i) = 1.0;
+        return e;
+    }
+    static DenseMatrix diag(const std::vector<double>& d) {
+        DenseMatrix e(int(d.size()), int(d.size()));
+        for (int i = 0; i < int(d.size()); ++i) e(i, i) = d[i];
+        return e;
+    }
+    int rows() const { return r_; }
+    int cols() const { return c_; }
+    std::size_t size() const { return v_.size(); }
+    double& operator()(int i, int j) { return v_[std::size_t(i) + std::size_t(j) * r_]; }
+    double operator()(int i, int j) const { return v_[std::size_t(i) + std::size_t(j) * r_]; }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    double* col(int j) { return v_.data() + std::size_t(j) * r_; }
+    const double* col(int j) const { return v_.data() + std::size_t(j) * r_; }
+    bool all_finite() const {
+        return std::all_of(v_.begin(), v_.end(), [](double x) { return std::isfinite(x); });
+    }
+
+private:
+    int r_ = 0, c_ = 0;
+    std::vector<double> v_;
+};
+
+// 0-based bijection (core/matrix.hpp:83-110)
+class Permutation {
+public:
+    Permutation() = default;
+    explicit Permutation(std::vector<int> idx) : p_(std::move(idx)) {
+        std::vector<char> seen(p_.size(), 0);
+        for (int x : p_) {
+            if (x < 0 || x >= int(p_.size()))
+                throw DimensionError(detail::msg("Permutation: index %d out of range [0,%zu)", x, p_.size()));
+            if (seen[x]) throw DimensionError(detail::msg("Permutation: duplicate index %d", x));
+            seen[x] = 1;
+        }
+    }
+    static Permutation identity(int n) {
+        std::vector<int> v(n);
+        std::iota(v.begin(), v.end(), 0);
+        return Permutation(std::move(v));
+    }
+    int operator[](int i) const { return p_[std::size_t(i)]; }
+    int size() const { return int(p_.size()); }
+    const std::vector<int>& indices() const { return p_; }
+
+private:
+    std::vector<int> p_;
+};
+
+inline DenseMatrix transpose(const DenseMatrix& a) {
+    DenseMatrix t(a.cols(), a.rows());
+    for (int j = 0; j < a.cols(); ++j)
+        for (int i = 0; i < a.rows(); ++i) t(j, i) = a(i, j);
+    return t;
+}
+inline DenseMatrix submatrix(const DenseMatrix& a, int r0, int nr, int c0, int nc) {
+    if (r0 < 0 || c0 < 0 || nr < 0 || nc < 0 || r0 + nr > a.rows() || c0 + nc > a.cols())
+        throw DimensionError(detail::msg("submatrix: block %d+%d x %d+%d exceeds %dx%d", r0, nr, c0, nc,
+                                         a.rows(), a.cols()));
+    DenseMatrix b(nr, nc);
+    for (int j = 0; j < nc; ++j) std::copy(a.col(c0 + j) + r0, a.col(c0 + j) + r0 + nr, b.col(j));
+    return b;
+}
+inline DenseMatrix select_columns(const DenseMatrix& a, const Permutation& idx, int count) {
+    if (count < 0 || count > idx.size() || count > a.cols())
+        throw DimensionError(detail::msg("select_columns: count %d out of range", count));
+    DenseMatrix c(a.rows(), count);
+    for (int j = 0; j < count; ++j) std::copy(a.col(idx[j]), a.col(idx[j]) + a.rows(), c.col(j));
+    return c;
+}
+inline DenseMatrix select_rows(const DenseMatrix& a, const Permutation& idx, int count) {
+    if (count < 0 || count > idx.size() || count > a.rows())
+        throw DimensionError(detail::msg("select_rows: count %d out of range", count));
+    DenseMatrix r(count, a.cols());
+    for (int j = 0; j < a.cols(); ++j)
+        for (int i = 0; i < count; ++i) r(i, j) = a(idx[i], j);
+    return r;
+}
+inline DenseMatrix hconcat(const DenseMatrix& a, const DenseMatrix& b) {
+    if (a.rows() != b.rows())
+        throw DimensionError(detail::msg("hconcat: row counts disagree (%d vs %d)", a.rows(), b.rows()));
+    DenseMatrix c(a.rows(), a.cols() + b.cols());
+    std::copy(a.data(), a.data() + a.size(), c.data());
+    std::copy(b.data(), b.data() + b.size(), c.data() + a.size());
+    return c;
+}
+inline DenseMatrix vconcat(const DenseMatrix& a, const DenseMatrix& b) {
+    if (a.cols() != b.cols())
+        throw DimensionError(detail::msg("vconcat: column counts disagree (%d vs %d)", a.cols(), b.cols()));
+    DenseMatrix c(a.rows() + b.rows(), a.cols());
+    for (int j = 0; j < a.cols(); ++j) {
+        std::copy(a.col(j), a.col(j) + a.rows(), c.col(j));
+        std::copy(b.col(j), b.col(j) + b.rows(), c.col(j) + a.rows());
+    }
+    return c;
+}
+namespace detail {
+template <class Op>
+DenseMatrix zip(const DenseMatrix& a, const DenseMatrix& b, const char* name, Op op) {
+    if (a.rows() != b.rows() || a.cols() != b.cols())
+        throw DimensionError(msg("%s: shapes disagree (%dx%d vs %dx%d)", name, a.rows(), a.cols(), b.rows(),
+                                 b.cols()));
+    DenseMatrix c(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.size(); ++i) c.data()[i] = op(a.data()[i], b.data()[i]);
+    return c;
+}
+}  // namespace detail
+inline DenseMatrix subtract(const DenseMatrix& a, const DenseMatrix& b) {
+    return detail::zip(a, b, "subtract", [](double x, double y) { return x - y; });
+}
+inline DenseMatrix add(const DenseMatrix& a, const DenseMatrix& b) {
+    return detail::zip(a, b, "add", [](double x, double y) { return x + y; });
+}
+inline DenseMatrix scale(const DenseMatrix& a, double s) {
+    DenseMatrix c(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.size(); ++i) c.data()[i] = s * a.data()[i];
+    return c;
+}
+inline void scale_columns_inplace(DenseMatrix& a, const std::vector<double>& s) {
+    if (int(s.size()) != a.cols())
+        throw DimensionError(detail::msg("scale_columns_inplace: %zu factors for %d columns", s.size(), a.cols()));
+    for (int j = 0; j < a.cols(); ++j)
+        for (int i = 0; i < a.rows(); ++i) a(i, j) *= s[j];
+}
+inline double max_abs_diff(const DenseMatrix& a, const DenseMatrix& b) {
+    if (a.rows() != b.rows() || a.cols() != b.cols()) throw DimensionError("max_abs_diff: shapes disagree");
+    double m = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.data()[i] - b.data()[i]));
+    return m;
+}
+
+// ---------------------------------------------------------------- rng ---
+// The reference stream (core/rng.hpp:18-87) through the library's host RNG.
+class RngState {
+public:
+    explicit RngState(std::uint64_t seed = 0) { rlra_rng_seed(&s_, seed); }
+    std::uint64_t next_u64() { return rlra_rng_next_u64(&s_); }
+    double next_unit() { return double(next_u64() >> 11) * 0x1.0p-53; }
+    double next_gaussian() { return rlra_rng_next_gaussian(&s_); }
+    RngState substream() {
+        RngState c;
+        rlra_rng_substream(&s_, &c.s_);
+        return c;
+    }
+    rlra_rng* raw() { return &s_; }
+
+private:
+    rlra_rng s_{};
+};
+
+inline DenseMatrix gaussian_matrix(int rows, int cols, RngState& rng) {
+    DenseMatrix g(rows, cols);
+    rlra_rng_gaussian_fill(rng.raw(), rows, cols, g.data());
+    return g;
+}
+
+namespace detail {
+inline rlra_omega omega_from(RngState& rng, bool substreams) {
+    rlra_omega o{};
+    o.mode = RLRA_OMEGA_CALLBACK;
+    o.fill = substreams ? rlra_omega_fill_rng_substream : rlra_omega_fill_rng;
+    o.user = rng.raw();
+    return o;
+}
+inline int ld(const DenseMatrix& a) { return std::max(1, a.rows()); }
+}  // namespace detail
+
+// ------------------------------------------------------------ kernels ---
+inline DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b, bool trans_a = false,
+                          bool trans_b = false) {
+    const int m = trans_a ? a.cols() : a.rows(), n = trans_b ? b.rows() : b.cols();
+    const int ka = trans_a ? a.rows() : a.cols(), kb = trans_b ? b.cols() : b.rows();
+    if (ka != kb)
+        throw DimensionError(detail::msg("matmul: inner dimensions disagree: op(%dx%d) * op(%dx%d)", a.rows(),
+                                         a.cols(), b.rows(), b.cols()));
+    DenseMatrix c(m, n);
+    if (m == 0 || n == 0) return c;
+    detail::check(rlra_matmul(detail::ctx(), RLRA_HOST, trans_a, trans_b, a.data(), a.rows(), a.cols(),
+                              detail::ld(a), b.data(), b.rows(), b.cols(), detail::ld(b), c.data(),
+                              std::max(1, m)));
+    return c;
+}
+
+inline double frobenius_norm(const DenseMatrix& a) {
+    if (a.size() == 0) return 0.0;
+    double out = 0.0;
+    detail::check(rlra_frobenius_norm(detail::ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), detail::ld(a), &out));
+    return out;
+}
+inline double column_norm(const DenseMatrix& a, int j) {
+    double out = 0.0;
+    if (a.rows() == 0) return 0.0;
+    detail::check(rlra_frobenius_norm(detail::ctx(), RLRA_HOST, a.col(j), a.rows(), 1, a.rows(), &out));
+    return out;
+}
+inline double spectral_norm_est(const DenseMatrix& a, int iters, RngState& rng) {  // norms.hpp:41-56
+    if (iters < 20) throw DimensionError(detail::msg("spectral_norm_est: iters=%d, need >= 20", iters));
+    if (a.rows() == 0 || a.cols() == 0) return 0.0;
+    DenseMatrix v = gaussian_matrix(a.cols(), 1, rng);
+    double sigma = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        const double vn = frobenius_norm(v);
+        if (vn == 0.0) return 0.0;
+        for (int i = 0; i < v.rows(); ++i) v(i, 0) /= vn;
+        DenseMatrix w = matmul(a, v);
+        sigma = frobenius_norm(w);
+        v = matmul(a, w, true);
+    }
+    return sigma;
+}
+
+struct QrFactors {
+    DenseMatrix q;
+    DenseMatrix r;
+    bool degenerate_rank = false;
+};
+struct PivotedQr {
+    DenseMatrix q1;
+    DenseMatrix s1;
+    Permutation perm;
+    int frank = 0;
+    double residual = 0.0;
+    bool tolerance_reached = false;
+    bool degenerate_rank = false;
+};
+struct TriSolve {
+    DenseMatrix t;
+    bool clamped = false;
+};
+
+inline QrFactors compact_qr(const DenseMatrix& a) {
+    const int m = a.rows(), n = a.cols();
+    if (m < n) throw DimensionError(detail::msg("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
+    QrFactors f{DenseMatrix(m, n), DenseMatrix(n, n), false};
+    if (n == 0) return f;
+    int deg = 0;
+    detail::check(rlra_compact_qr(detail::ctx(), RLRA_HOST, a.data(), m, n, detail::ld(a), f.q.data(), m,
+                                  f.r.data(), n, &deg));
+    f.degenerate_rank = deg != 0;
+    return f;
+}
+inline DenseMatrix orth(const DenseMatrix& a, bool* degenerate = nullptr) {
+    QrFactors f = compact_qr(a);
+    if (degenerate) *degenerate = f.degenerate_rank;
+    return f.q;
+}
+inline PivotedQr pivoted_qr_partial(const DenseMatrix& a, int k, double tol = 0.0) {
+    const int m = a.rows(), n = a.cols(), rmax = std::min(m, n);
+    const bool tol_mode = k == 0 && tol > 0.0;
+    const int kmax = tol_mode ? rmax : std::max(k, 1);
+    DenseMatrix q1(m, kmax), s1(kmax, n);
+    std::vector<int> perm(n);
+    int frank = 0, reached = 0, deg = 0;
+    double res = 0.0;
+    detail::check(rlra_pivoted_qr(detail::ctx(), RLRA_HOST, a.data(), m, n, detail::ld(a), k, tol, q1.data(),
+                                  std::max(1, m), s1.data(), kmax, perm.data(), &frank, &res, &reached, &deg));
+    PivotedQr out;
+    out.q1 = submatrix(q1, 0, m, 0, frank);
+    out.s1 = submatrix(s1, 0, frank, 0, n);
+    out.perm = Permutation(std::move(perm));
+    out.frank = frank;
+    out.residual = res;
+    out.tolerance_reached = reached != 0;
+    out.degenerate_rank = deg != 0;
+    return out;
+}
+inline TriSolve upper_tri_solve(const DenseMatrix& s11, const DenseMatrix& s12) {
+    const int k = s11.rows();
+    if (s11.cols() != k) throw DimensionError(detail::msg("upper_tri_solve: S11 is %dx%d, need square", k, s11.cols()));
+    if (s12.rows() != k) throw DimensionError(detail::msg("upper_tri_solve: S12 has %d rows, need %d", s12.rows(), k));
+    TriSolve out{DenseMatrix(k, s12.cols()), false};
+    if (k == 0) return out;
+    int cl = 0;
+    detail::check(rlra_upper_tri_solve(detail::ctx(), RLRA_HOST, s11.data(), k, k, s12.data(), s12.cols(), k,
+                                       out.t.data(), k, &cl));
+    out.clamped = cl != 0;
+    return out;
+}
+
+struct SymEig {
+    std::vector<double> values;
+    DenseMatrix vectors;
+};
+struct SvdFactors {
+    DenseMatrix u;
+    std::vector<double> sigma;
+    DenseMatrix v;
+    int k = 0;
+};
+
+inline SymEig sym_eig(const DenseMatrix& t) {
+    const int n = t.rows();
+    if (t.cols() != n) throw DimensionError(detail::msg("sym_eig: matrix is %dx%d, need square", n, t.cols()));
+    SymEig e{std::vector<double>(n), DenseMatrix(n, n)};
+    if (n == 0) return e;
+    detail::check(rlra_sym_eig(detail::ctx(), RLRA_HOST, t.data(), n, n, e.values.data(), e.vectors.data(), n));
+    return e;
+}
+inline SvdFactors small_svd(const DenseMatrix& a) {
+    const int m = a.rows(), n = a.cols(), r = std::min(m, n);
+    SvdFactors f{DenseMatrix(m, r), std::vector<double>(r), DenseMatrix(n, r), r};
+    if (r == 0) return f;
+    detail::check(rlra_small_svd(detail::ctx(), RLRA_HOST, a.data(), m, n, detail::ld(a), f.u.data(),
+                                 std::max(1, m), f.sigma.data(), f.v.data(), std::max(1, n)));
+    return f;
+}
+
+// ------------------------------------------------------------- sketch ---
+enum class Vnum { kQr, kBbt };
+
+struct SketchParams {  // sketch.hpp:18-39
+    int k = 0;
+    int p = 5;
+    int q = 1;
+    int s = 1;
+    double tol = 0.0;
+    int block = 20;
+    int max_blocks = 12;
+    Vnum vnum = Vnum::kQr;
+    std::uint64_t seed = 0;
+    void validate(int m, int n) const {
+        if ((k >= 1) == (tol > 0.0))
+            throw DimensionError(detail::msg(
+                "SketchParams: exactly one of rank (k=%d) and tolerance (tol=%g) must be set", k, tol));
+        if (k >= 1 && k + p > std::min(m, n))
+            throw DimensionError(detail::msg("SketchParams: k+p = %d exceeds min(m,n) = %d for %dx%d", k + p,
+                                             std::min(m, n), m, n));
+        if (p < 0 || q < 0 || s < 1 || block < 1 || max_blocks < 1 || tol < 0.0 || k < 0)
+            throw DimensionError("SketchParams: negative or zero-valued parameter out of range");
+    }
+};
+
+inline DenseMatrix sample_right(const DenseMatrix& a, int l, int q, int s, RngState& rng) {
+    DenseMatrix y(a.rows(), std::max(l, 0));
+    rlra_omega om = detail::omega_from(rng, false);
+    detail::check(rlra_sample(detail::ctx(), RLRA_HOST, 0, a.data(), a.rows(), a.cols(), detail::ld(a), l, q, s,
+                              &om, y.data(), std::max(1, a.rows())));
+    return y;
+}
+inline DenseMatrix sample_left(const DenseMatrix& a, int l, int q, int s, RngState& rng) {
+    DenseMatrix y(std::max(l, 0), a.cols());
+    rlra_omega om = detail::omega_from(rng, false);
+    detail::check(rlra_sample(detail::ctx(), RLRA_HOST, 1, a.data(), a.rows(), a.cols(), detail::ld(a), l, q, s,
+                              &om, y.data(), std::max(1, l)));
+    return y;
+}
+
+// --------------------------------------------------------------- rsvd ---
+namespace detail {
+inline SvdFactors rsvd_call(int variant, const DenseMatrix& a, int k, int p, int q, int s, RngState& rng) {
+    const int kk = std::max(k, 0);
+    SvdFactors f{DenseMatrix(a.rows(), kk), std::vector<double>(kk), DenseMatrix(a.cols(), kk), kk};
+    rlra_omega om = omega_from(rng, false);
+    check(rlra_rsvd(ctx(), RLRA_HOST, variant, a.data(), a.rows(), a.cols(), ld(a), k, p, q, s, &om, f.u.data(),
+                    std::max(1, a.rows()), f.sigma.data(), f.v.data(), std::max(1, a.cols())));
+    return f;
+}
+inline SvdFactors truncate_svd(const SvdFactors& f, int k) {
+    if (k < 0 || k > f.k) throw DimensionError(msg("truncation rank %d outside [0, %d]", k, f.k));
+    SvdFactors out;
+    out.k = k;
+    out.u = submatrix(f.u, 0, f.u.rows(), 0, k);
+    out.v = submatrix(f.v, 0, f.v.rows(), 0, k);
+    out.sigma.assign(f.sigma.begin(), f.sigma.begin() + k);
+    return out;
+}
+}  // namespace detail
+
+inline SvdFactors svd_truncated(const DenseMatrix& a, int k, double tol = 0.0) {  // rsvd.hpp:98-123
+    const int r = std::min(a.rows(), a.cols());
+    const bool rank_mode = k >= 1 && tol == 0.0, tol_mode = k == 0 && tol > 0.0;
+    if (!rank_mode && !tol_mode)
+        throw DimensionError(detail::msg("exactly one of rank k >= 1 or tol > 0 must be set (got k=%d, tol=%g)", k, tol));
+    if (rank_mode && k > r) throw DimensionError(detail::msg("rank %d exceeds min(m,n) = %d", k, r));
+    if (r > 2000)
+        throw DimensionError(detail::msg(
+            "min(m,n) = %d exceeds the dense SVD limit of 2000; use the randomized routines for matrices this large", r));
+    SvdFactors full = small_svd(a);
+    int keep = k;
+    if (tol_mode) {
+        keep = r;
+        for (int i = 0; i < r; ++i)
+            if (full.sigma[i] < tol) {
+                keep = i;
+                break;
+            }
+    }
+    return detail::truncate_svd(full, keep);
+}
+inline SvdFactors rsvd_basic(const DenseMatrix& a, int k, int p, RngState& rng) {
+    return detail::rsvd_call(RLRA_RSVD_BASIC, a, k, p, 0, 1, rng);
+}
+inline SvdFactors rsvd_v1(const DenseMatrix& a, int k, int p, int q_power, int s, RngState& rng) {
+    return detail::rsvd_call(RLRA_RSVD_V1, a, k, p, q_power, s, rng);
+}
+inline SvdFactors rsvd_v2(const DenseMatrix& a, int k, int p, int q_power, int s, RngState& rng) {
+    return detail::rsvd_call(RLRA_RSVD_V2, a, k, p, q_power, s, rng);
+}
+
+// ----------------------------------------------------------------- qb ---
+struct ResidualReport {
+    double final_residual = 0.0;
+    std::vector<double> history;
+    bool tolerance_reached = true;
+};
+struct QbFactors {
+    DenseMatrix q;
+    DenseMatrix b;
+    int ell = 0;
+    ResidualReport residual_report;
+};
+
+namespace detail {
+inline QbFactors qb_call(DenseMatrix& w, bool inplace, int b, int num_blocks, double tol, int q_power,
+                         int reorth_period, RngState& rng) {
+    const int m = w.rows(), n = w.cols();
+    const int cap = (b >= 1 && num_blocks >= 1) ? std::max(1, int(std::min<long long>(
+                                                              (long long)b * num_blocks, std::min(m, n))))
+                                                : 1;
+    DenseMatrix Q(m, cap), B(cap, n);
+    std::vector<double> hist(std::max(num_blocks, 1));
+    int ell = 0, nh = 0, reached = 0;
+    double fin = 0.0;
+    rlra_omega om = omega_from(rng, true);
+    check(rlra_qb_blocked(ctx(), RLRA_HOST, w.data(), m, n, ld(w), inplace ? 1 : 0, b, num_blocks, tol, q_power,
+                          reorth_period, &om, Q.data(), std::max(1, m), B.data(), cap, cap, &ell, hist.data(), &nh,
+                          &fin, &reached));
+    QbFactors f;
+    f.q = submatrix(Q, 0, m, 0, ell);
+    f.b = submatrix(B, 0, ell, 0, n);
+    f.ell = ell;
+    f.residual_report.history.assign(hist.begin(), hist.begin() + nh);
+    f.residual_report.final_residual = fin;
+    f.residual_report.tolerance_reached = reached != 0;
+    return f;
+}
+}  // namespace detail
+
+inline QbFactors qb_blocked_inplace(DenseMatrix& w, int b, int num_blocks, double tol, int q_power,
+                                    int reorth_period, RngState& rng) {
+    return detail::qb_call(w, true, b, num_blocks, tol, q_power, reorth_period, rng);
+}
+inline QbFactors qb_blocked(const DenseMatrix& a, int b, int num_blocks, double tol, int q_power,
+                            int reorth_period, RngState& rng) {
+    DenseMatrix w = a;
+    return detail::qb_call(w, false, b, num_blocks, tol, q_power, reorth_period, rng);
+}
+
+inline SvdFactors svd_from_qb(const QbFactors& qb, int k, Vnum vnum) {
+    if (k < 0 || k > qb.ell) throw DimensionError(detail::msg("rank k = %d outside [0, rank(B) = %d]", k, qb.ell));
+    const int kk = k == 0 ? qb.ell : k;
+    SvdFactors f{DenseMatrix(qb.q.rows(), kk), std::vector<double>(kk), DenseMatrix(qb.b.cols(), kk), kk};
+    if (kk == 0) return f;
+    int ko = 0;
+    detail::check(rlra_svd_from_qb(detail::ctx(), RLRA_HOST, qb.q.data(), qb.q.rows(), std::max(1, qb.q.rows()),
+                                   qb.b.data(), qb.b.cols(), std::max(1, qb.b.rows()), qb.ell, k,
+                                   vnum == Vnum::kBbt ? RLRA_VNUM_BBT : RLRA_VNUM_QR, f.u.data(),
+                                   std::max(1, qb.q.rows()), f.sigma.data(), f.v.data(),
+                                   std::max(1, qb.b.cols()), &ko));
+    return f;
+}
+
+// ------------------------------------------------------------- interp ---
+struct IdFactors {
+    Permutation jc;
+    DenseMatrix v;
+    int k = 0;
+    double qr_residual = 0.0;
+    bool tolerance_reached = true;
+    bool clamped = false;
+};
+struct RowIdFactors {
+    Permutation jr;
+    DenseMatrix w;
+    int k = 0;
+    double qr_residual = 0.0;
+    bool tolerance_reached = true;
+    bool clamped = false;
+};
+struct TwoSidedIdFactors {
+    Permutation jr;
+    Permutation jc;
+    DenseMatrix w;
+    DenseMatrix v;
+    int k = 0;
+    double qr_residual = 0.0;
+    bool tolerance_reached = true;
+};
+struct CurFactors {
+    DenseMatrix c;
+    DenseMatrix u;
+    DenseMatrix r;
+    Permutation jr;
+    Permutation jc;
+    int k = 0;
+    double residual = 0.0;
+    double qr_residual = 0.0;
+    bool tolerance_reached = true;
+};
+
+inline IdFactors id_column(const DenseMatrix& a, int k, double tol = 0.0) {
+    const int m = a.rows(), n = a.cols();
+    const int kcap = (k == 0 && tol > 0.0) ? std::min(m, n) : std::max(k, 1);
+    std::vector<int> jc(n);
+    DenseMatrix v(n, kcap);
+    int ko = 0, reached = 0, cl = 0;
+    double res = 0.0;
+    detail::check(rlra_id_column(detail::ctx(), RLRA_HOST, a.data(), m, n, detail::ld(a), k, tol, jc.data(),
+                                 v.data(), std::max(1, n), &ko, &res, &reached, &cl));
+    IdFactors f;
+    f.jc = Permutation(std::move(jc));
+    f.v = submatrix(v, 0, n, 0, ko);
+    f.k = ko;
+    f.qr_residual = res;
+    f.tolerance_reached = reached != 0;
+    f.clamped = cl != 0;
+    return f;
+}
+inline RowIdFactors id_row(const DenseMatrix& a, int k, double tol = 0.0) {
+    IdFactors c = id_column(transpose(a), k, tol);
+    return RowIdFactors{std::move(c.jc), std::move(c.v), c.k, c.qr_residual, c.tolerance_reached, c.clamped};
+}
+
+namespace detail {
+inline TwoSidedIdFactors two_sided_from_column(const DenseMatrix& a, IdFactors col) {
+    TwoSidedIdFactors out;
+    out.jc = std::move(col.jc);
+    out.v = std::move(col.v);
+    out.k = col.k;
+    out.qr_residual = col.qr_residual;
+    out.tolerance_reached = col.tolerance_reached;
+    const int m = a.rows();
+    std::vector<int> jr(m);
+    out.w = DenseMatrix(m, out.k);
+    check(rlra_two_sided_from_column(ctx(), RLRA_HOST, a.data(), m, a.cols(), ld(a), out.jc.indices().data(),
+                                     out.k, jr.data(), out.w.data(), std::max(1, m)));
+    out.jr = Permutation(std::move(jr));
+    return out;
+}
+inline CurFactors cur_from_two_sided(const DenseMatrix& a, const TwoSidedIdFactors& ts) {
+    CurFactors out;
+    out.k = ts.k;
+    out.jc = ts.jc;
+    out.jr = ts.jr;
+    out.qr_residual = ts.qr_residual;
+    out.tolerance_reached = ts.tolerance_reached;
+    out.c = DenseMatrix(a.rows(), ts.k);
+    out.u = DenseMatrix(ts.k, ts.k);
+    out.r = DenseMatrix(ts.k, a.cols());
+    check(rlra_cur_from_two_sided(ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), ld(a), ts.jc.indices().data(),
+                                  ts.jr.indices().data(), ts.v.data(), std::max(1, ts.v.rows()), ts.k,
+                                  out.c.data(), std::max(1, a.rows()), out.u.data(), std::max(1, ts.k),
+                                  out.r.data(), std::max(1, ts.k), &out.residual));
+    return out;
+}
+}  // namespace detail
+
+inline TwoSidedIdFactors id_two_sided(const DenseMatrix& a, int k, double tol = 0.0) {
+    return detail::two_sided_from_column(a, id_column(a, k, tol));
+}
+inline CurFactors cur(const DenseMatrix& a, int k, double tol = 0.0) {
+    return detail::cur_from_two_sided(a, id_two_sided(a, k, tol));
+}
+inline IdFactors id_rand(const DenseMatrix& a, int k, int p, int q_power, int s, RngState& rng) {
+    const int n = a.cols();
+    std::vector<int> jc(n);
+    DenseMatrix v(n, std::max(k, 0));
+    double res = 0.0;
+    int cl = 0;
+    rlra_omega om = detail::omega_from(rng, false);
+    detail::check(rlra_id_rand(detail::ctx(), RLRA_HOST, a.data(), a.rows(), n, detail::ld(a), k, p, q_power, s,
+                               &om, jc.data(), v.data(), std::max(1, n), &res, &cl));
+    IdFactors f;
+    f.jc = Permutation(std::move(jc));
+    f.v = std::move(v);
+    f.k = k;
+    f.qr_residual = res;
+    f.clamped = cl != 0;
+    return f;
+}
+inline IdFactors id_from_qb(const QbFactors& qb, const DenseMatrix& a, int k) {
+    if (a.rows() != qb.q.rows() || a.cols() != qb.b.cols())
+        throw DimensionError(detail::msg("id_from_qb: matrix is %dx%d but the QB factors describe %dx%d", a.rows(),
+                                         a.cols(), qb.q.rows(), qb.b.cols()));
+    if (k < 1 || k > qb.ell) throw DimensionError(detail::msg("rank k = %d outside [1, rank(B) = %d]", k, qb.ell));
+    return id_column(qb.b, k, 0.0);
+}
+inline CurFactors cur_rand(const DenseMatrix& a, int k, int p, int q_power, int s, RngState& rng) {
+    IdFactors col = id_rand(a, k, p, q_power, s, rng);
+    return detail::cur_from_two_sided(a, detail::two_sided_from_column(a, std::move(col)));
+}
+
+}  // namespace rlra
