@@ -294,13 +294,16 @@ def main():
     value = world * F / (ms_step * 1e-3) / 1e12
 
     # dominant kernel: the DMMA GEMMs that stream A (M or K == m)
-    big = [r for r in prof if r["name"] == "dgemm" and (r["M"] == m or r["K"] == m)]
+    big = [r for r in prof if r["name"] in ("gemm_sketch", "gemm_power", "gemm_proj")]
     g_ms = sum(r["ms"] for r in big)
     g_fl = sum(r["flops"] for r in big)
+    # phases are nested intervals: orth contains chol and gemm_orth, chol contains gemm_chol
     phases = {}
     for r in prof:
-        key = r["name"] if r["name"] != "dgemm" else ("gemm_A" if r in big else "gemm_small")
-        phases[key] = phases.get(key, 0.0) + r["ms"] / args.steps
+        phases[r["name"]] = phases.get(r["name"], 0.0) + r["ms"] / args.steps
+    sweeps = [r["K"] for r in prof if r["name"] == "small_svd"]
+    if sweeps:
+        phases["small_svd_sweeps"] = sweeps[-1]
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
 
     # relative error of the last factorization (device reduction)

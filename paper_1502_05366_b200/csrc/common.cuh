@@ -84,6 +84,16 @@ struct Context {
         double flops;
     };
     std::vector<ProfRec> prof;
+    // label the profiler gives the next GEMM launches (see GemmTag)
+    const char* gemm_tag = "gemm";
+};
+
+// Scoped label for GEMM launches (profiling/accounting only).
+struct GemmTag {
+    Context& ctx;
+    const char* prev;
+    GemmTag(Context& c, const char* tag) : ctx(c), prev(c.gemm_tag) { c.gemm_tag = tag; }
+    ~GemmTag() { ctx.gemm_tag = prev; }
 };
 
 // Records one interval on ctx.stream when profiling is enabled.

@@ -66,6 +66,7 @@ double read_scalar(Context& ctx, const double* d) {
 void sketch(Context& ctx, Op op_a, const DMat& A, int l, OmegaSource& om, const DMat& Y) {
     const int rows = int(op_a == Op::N ? A.cols : A.rows);
     const int draw = om.next_draw++;
+    GemmTag tag(ctx, "gemm_sketch");
     if (om.o->mode == RLRA_OMEGA_PHILOX) {
         GemmOpts o;
         o.philox_b = true;
@@ -96,6 +97,7 @@ void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat
     Buf s(ctx, sizeof(double) * l);
     orth_inplace(ctx, Bt, &R.m);                       // compact_qr(bt)
     small_svd_tall(ctx, R, Uh, s.d(), Vh);             // small_svd(f.r)
+    GemmTag tag(ctx, "gemm_lift");
     gemm(ctx, Op::N, Op::N, 1.0, Q, Vh.m.block(0, 0, l, k), 0.0, U);   // (Q*Vhat)(:,1:k)
     gemm(ctx, Op::N, Op::N, 1.0, Bt, Uh.m.block(0, 0, l, k), 0.0, V);  // (Qhat*Uhat)(:,1:k)
     RLRA_CUDA(cudaMemcpyAsync(sigma, s.p, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -149,6 +151,7 @@ void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource&
     sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
     if (q == 0) return;
     DMatBuf Z(ctx, n, l);
+    GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
         if ((2 * j - 2) % s == 0) orth(ctx, Y);
         gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z);  // Z = A^T Y
@@ -162,6 +165,7 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
     sketch(ctx, Op::T, A, l, om, Yt);  // (A^T) * Omega~, Omega~ m x l
     if (q == 0) return;
     DMatBuf Z(ctx, m, l);
+    GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
         if ((2 * j - 2) % s == 0) orth(ctx, Yt);
         gemm(ctx, Op::N, Op::N, 1.0, A, Yt, 0.0, Z);  // (A^T)^T Yt
@@ -191,6 +195,7 @@ void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, 
     }
     sample_right(ctx, A, l, q, s, om, Y);
     orth(ctx, Y);
+    GemmTag tag(ctx, "gemm_proj");
     if (variant == RLRA_RSVD_V2) {
         DMatBuf Bt(ctx, n, l);
         gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Bt);  // Bt = A^T Q (rsvd.hpp:158)

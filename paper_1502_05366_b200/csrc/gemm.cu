@@ -1,4 +1,7 @@
 // gemm.cu — launcher for the FP64 DMMA GEMM family (see gemm.cuh).
+#include <cstdlib>
+#include <string>
+
 #include "gemm.cuh"
 #include "reduce.cuh"
 
@@ -6,11 +9,30 @@ namespace rlra_b200 {
 
 namespace {
 
+// 128x128 CTA tile, 8 warps of 64x32 (2 warps per scheduler)
 struct CfgBig {
     static constexpr int BM = 128, BN = 128, BK = 16, WM = 64, WN = 32, STAGES = 4;
+    static constexpr bool WS = true;
 };
+// 128x128 CTA tile, 16 warps of 32x32 (4 warps per scheduler: more DMMA
+// issue candidates per SMSP at the same shared-memory tile)
+struct CfgBig16 {
+    static constexpr int BM = 128, BN = 128, BK = 16, WM = 32, WN = 32, STAGES = 4;
+    static constexpr bool WS = false;
+};
+
+int big_cfg_choice() {
+    static int choice = [] {
+        const char* e = std::getenv("RLRA_GEMM_CFG");
+        if (e && std::string(e) == "w8") return 8;
+        if (e && std::string(e) == "w16") return 16;
+        return 8;
+    }();
+    return choice;
+}
 struct CfgSmall {
     static constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, STAGES = 4;
+    static constexpr bool WS = false;
 };
 
 template <class Cfg, bool A_KM, bool B_KM>
@@ -19,19 +41,43 @@ constexpr size_t smem_bytes() {
            (TileGeo<A_KM, Cfg::BM, Cfg::BK>::elems + TileGeo<B_KM, Cfg::BN, Cfg::BK>::elems);
 }
 
+bool ws_choice() {
+    static bool ws = [] {
+        const char* e = std::getenv("RLRA_GEMM_WS");
+        return !(e && std::string(e) == "0");
+    }();
+    return ws;
+}
+
 template <class Cfg, bool A_KM, bool B_KM, bool VEC, int EPI, bool PHILOX>
 void launch_cfg(Context& ctx, const GemmParams& p) {
-    auto kern = dgemm_kernel<Cfg::BM, Cfg::BN, Cfg::BK, Cfg::WM, Cfg::WN, Cfg::STAGES, A_KM, B_KM, VEC,
-                             EPI, PHILOX>;
     constexpr size_t smem = smem_bytes<Cfg, A_KM, B_KM>();
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr_set = true;
-    }
-    constexpr int threads = (Cfg::BM / Cfg::WM) * (Cfg::BN / Cfg::WN) * 32;
     const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
-    kern<<<dim3(unsigned(grid)), threads, smem, ctx.stream>>>(p);
+    constexpr int consumers = (Cfg::BM / Cfg::WM) * (Cfg::BN / Cfg::WN) * 32;
+    bool launched = false;
+    if constexpr (Cfg::WS) {
+      if (ws_choice()) {
+        auto kern = dgemm_ws_kernel<Cfg::BM, Cfg::BN, Cfg::BK, Cfg::WM, Cfg::WN, Cfg::STAGES, A_KM, B_KM,
+                                    VEC, EPI, PHILOX>;
+        static bool attr_set = false;  // per instantiation
+        if (!attr_set) {
+            RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr_set = true;
+        }
+        kern<<<dim3(unsigned(grid)), 128 + consumers, smem, ctx.stream>>>(p);
+        launched = true;
+      }
+    }
+    if (!launched) {
+        auto kern = dgemm_kernel<Cfg::BM, Cfg::BN, Cfg::BK, Cfg::WM, Cfg::WN, Cfg::STAGES, A_KM, B_KM, VEC,
+                                 EPI, PHILOX>;
+        static bool attr_set = false;  // per instantiation
+        if (!attr_set) {
+            RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr_set = true;
+        }
+        kern<<<dim3(unsigned(grid)), consumers, smem, ctx.stream>>>(p);
+    }
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
 }
@@ -153,14 +199,24 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
     int64_t tiles = int64_t(p.mt) * p.nt;
     if (o.upper_tiles_only) tiles = int64_t(p.mt) * (p.mt + 1) / 2;
     const int64_t cap = int64_t(ctx.num_sms) * per_sm;
+    // split-K only where it fixes wave quantization: pick the smallest split
+    // count whose CTA waves are fuller (by > 2%) than every smaller one.
     int splits = 1;
     if (o.epi != EPI_RESID && !o.tri_b_upper) {
         if (o.force_splits > 0) {
             splits = o.force_splits;
-        } else if (tiles < 2 * cap) {
-            const int64_t want = (2 * cap + tiles - 1) / tiles;
-            const int64_t kmaxs = std::max<int64_t>(1, K / (4 * BK));
-            splits = int(std::min<int64_t>(want, kmaxs));
+        } else {
+            auto eff = [&](int64_t s) {
+                const int64_t ctas = tiles * s;
+                return double(ctas) / double(((ctas + cap - 1) / cap) * cap);
+            };
+            const int64_t kmaxs = std::min<int64_t>(64, std::max<int64_t>(1, K / (8 * BK)));
+            double best = eff(1);
+            for (int64_t s = 2; s <= kmaxs; ++s)
+                if (eff(s) > best + 0.02) {
+                    best = eff(s);
+                    splits = int(s);
+                }
         }
     }
     int k_chunk = ceil_div(ceil_div(K, splits), BK) * BK;
@@ -183,8 +239,10 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
         parts = Buf(ctx, sizeof(double) * size_t(p.mt) * p.nt);
         p.partials = parts.d();
     }
-    ProfScope prof(ctx, "dgemm", M, N, K, 2.0 * M * double(N) * K);
-    if (big)
+    ProfScope prof(ctx, ctx.gemm_tag, M, N, K, 2.0 * M * double(N) * K);
+    if (big && big_cfg_choice() == 16)
+        launch_ops<CfgBig16>(ctx, opa, opb, vec, p, epi, o.philox_b);
+    else if (big)
         launch_ops<CfgBig>(ctx, opa, opb, vec, p, epi, o.philox_b);
     else
         launch_ops<CfgSmall>(ctx, opa, opb, vec, p, epi, o.philox_b);

@@ -301,6 +301,162 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) dgemm_kernel(co
     }
 }
 
+// --------------------------------------------- warp-specialized variant ---
+// Same tiles, fragments and epilogues as dgemm_kernel, but the CTA is split
+// into a producer warpgroup (cp.async for A and B, or in-register Philox for
+// Omega) and 2 consumer warpgroups (DMMA).  Stages are handed over through
+// mbarriers (full: producer -> consumers, empty: consumers -> producer), so
+// consumer warps never wait on each other and the Philox generation runs
+// concurrently with the tensor pipe instead of at the stage boundary.
+// setmaxnreg moves registers from the producer (56) to the consumers (224).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KM, bool B_KM, bool VEC,
+          int EPI, bool PHILOX>
+__global__ void __launch_bounds__(128 + (BM / WM) * (BN / WN) * 32, 1) dgemm_ws_kernel(const GemmParams p) {
+    constexpr int NWM = BM / WM, NWN = BN / WN;
+    constexpr int NCW = NWM * NWN;  // consumer warps
+    constexpr int MF = WM / 8, NF = WN / 8;
+    using GA = TileGeo<A_KM, BM, BK>;
+    using GB = TileGeo<B_KM, BN, BK>;
+    extern __shared__ __align__(16) double smem[];
+    double* sA = smem;
+    double* sB = smem + STAGES * GA::elems;
+    __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+    __shared__ double red[NCW];
+
+    const int tile = blockIdx.x;
+    const int nt_i = tile % p.nt;
+    const int rest = tile / p.nt;
+    const int mt_i = rest % p.mt;
+    const int split = rest / p.mt;
+    if (p.upper_tiles_only && mt_i > nt_i) return;
+    const int m0 = mt_i * BM, n0 = nt_i * BN;
+    const int k_begin = split * p.k_chunk;
+    int k_end = min(p.K, k_begin + p.k_chunk);
+    if (p.tri_b_upper) k_end = min(k_end, n0 + BN);
+    const int nk = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], PHILOX ? 256u : 128u);
+            mbar_init(&empty_bar[s], unsigned(NCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (threadIdx.x < 128) {
+        // ------------------------------------------------------ producer ---
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+        for (int kt = 0; kt < nk; ++kt) {
+            const int st = kt % STAGES;
+            if (kt >= STAGES) mbar_wait(&empty_bar[st], ((kt / STAGES) - 1) & 1);
+            const int k0 = k_begin + kt * BK;
+            load_tile<A_KM, BM, BK, 128, VEC>(sA + st * GA::elems, p.A, p.lda, m0, k0, p.M, k_end);
+            if (PHILOX) {
+                gen_omega_tile<BN, BK, 128>(sB + st * GB::elems, p, n0, k0, k_end);
+                mbar_arrive(&full_bar[st]);
+            } else {
+                load_tile<B_KM, BN, BK, 128, VEC>(sB + st * GB::elems, p.B, p.ldb, n0, k0, p.N, k_end);
+            }
+            mbar_arrive_cp_async(&full_bar[st]);
+        }
+        return;
+    }
+    // -------------------------------------------------------- consumers ---
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+    const int warp = (threadIdx.x >> 5) - 4, lane = threadIdx.x & 31;
+    const int wm = warp % NWM, wn = warp / NWM;
+    const int lr = lane >> 2, lc = lane & 3;
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % STAGES;
+        mbar_wait(&full_bar[st], (kt / STAGES) & 1);
+        const double* a_s = sA + st * GA::elems;
+        const double* b_s = sB + st * GB::elems;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[MF], bf[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) af[i] = a_s[GA::off(kk + lc, wm * WM + i * 8 + lr)];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bf[j] = b_s[GB::off(kk + lc, wn * WN + j * 8 + lr)];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+                for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+    }
+
+    double local = 0.0;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const int row = m0 + wm * WM + i * 8 + lr;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = n0 + wn * WN + j * 8 + lc * 2 + h;
+                if (row < p.M && col < p.N) {
+                    const double v = acc[i][j][h];
+                    if (EPI == EPI_STORE) {
+                        double* c = p.C + row + int64_t(col) * p.ldc;
+                        *c = p.beta == 0.0 ? p.alpha * v : p.alpha * v + p.beta * *c;
+                    } else if (EPI == EPI_SPLIT) {
+                        p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
+                    } else {
+                        const double d = p.R[row + int64_t(col) * p.ldr] - p.alpha * v;
+                        if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
+                        local += d * d;
+                    }
+                }
+            }
+        }
+    }
+    if (EPI == EPI_RESID) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if (lane == 0) red[warp] = local;
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32));
+        if (warp == 0 && lane == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) t += red[w];
+            p.partials[tile] = t;
+        }
+    }
+}
+
 // ------------------------------------------------------------ host side ---
 enum class Op { N = 0, T = 1 };
 

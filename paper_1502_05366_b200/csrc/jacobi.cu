@@ -96,6 +96,133 @@ __global__ void __launch_bounds__(kJacThreads) onesided_jacobi_kernel(OneSidedAr
     if (blockIdx.x == 0 && threadIdx.x == 0) flags[4] = sweep;
 }
 
+// ------------------------------------------------ block one-sided Jacobi ---
+// Columns are grouped into blocks of BW.  In each outer round every CTA takes
+// one block pair (I, J) from a round-robin tournament over the blocks, stages
+// the 2*BW columns of W in shared memory, runs one pass of the reference's
+// pairwise rotations over all column pairs inside the pair (an inner
+// round-robin, one warp per pair), writes the columns back and applies the
+// accumulated 2BW x 2BW rotation to the same columns of V.  One grid barrier
+// per outer round instead of one per column round; the rotation formula, the
+// skip rule and the "sweep without rotations" stop are the reference's
+// (core/jacobi.hpp:164-199).
+struct BlockJacArgs {
+    double* W;
+    int64_t ldw;
+    int m, n;
+    double* V;
+    int64_t ldv;
+    int nb;       // number of blocks (even)
+    int* flags;   // [0..2] rotated-in-sweep, [3] status, [4] sweeps used
+};
+
+template <int BW>
+__global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
+    constexpr int C2 = 2 * BW;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double bj_smem[];
+    double* Ws = bj_smem;                      // C2 columns of length m
+    double* Jm = bj_smem + size_t(C2) * a.m;   // C2 x C2 accumulated rotation
+    __shared__ int s_rot;
+    const int m = a.m, n = a.n, nb = a.nb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x;
+    const double eps = 1e-15;
+    volatile int* flags = a.flags;
+    int sweep = 0;
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            if (g == 0 && threadIdx.x == 0) flags[3] = RLRA_ECONV;
+            break;
+        }
+        if (g == 0 && threadIdx.x == 0) flags[(sweep + 1) % 3] = 0;
+        for (int r = 0; r < nb - 1; ++r) {
+            const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
+            const int bI = min(b1, b2), bJ = max(b1, b2);
+            auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
+            // stage W columns (zero-padded past n) and reset the rotation
+            for (int c = warp; c < C2; c += BW) {
+                const int gc = gcol(c);
+                for (int i = lane; i < m; i += 32)
+                    Ws[size_t(c) * m + i] = gc < n ? a.W[i + int64_t(gc) * a.ldw] : 0.0;
+            }
+            for (int e = threadIdx.x; e < C2 * C2; e += blockDim.x) Jm[e] = (e % C2 == e / C2) ? 1.0 : 0.0;
+            if (threadIdx.x == 0) s_rot = 0;
+            __syncthreads();
+            for (int ir = 0; ir < C2 - 1; ++ir) {
+                const int c1 = rr_col(warp, ir, C2), c2 = rr_col(C2 - 1 - warp, ir, C2);
+                const int p = min(c1, c2), q = max(c1, c2);
+                if (gcol(q) < n) {
+                    double* wp = Ws + size_t(p) * m;
+                    double* wq = Ws + size_t(q) * m;
+                    double app = 0.0, aqq = 0.0, apq = 0.0;
+                    for (int i = lane; i < m; i += 32) {
+                        const double xp = wp[i], xq = wq[i];
+                        app += xp * xp;
+                        aqq += xq * xq;
+                        apq += xp * xq;
+                    }
+                    app = warp_sum(app);
+                    aqq = warp_sum(aqq);
+                    apq = warp_sum(apq);
+                    if (app != 0.0 && aqq != 0.0 && fabs(apq) > eps * sqrt(app * aqq)) {
+                        const double zeta = (aqq - app) / (2.0 * apq);
+                        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                        const double c = 1.0 / sqrt(1.0 + t * t);
+                        const double s = t * c;
+                        for (int i = lane; i < m; i += 32) {
+                            const double xp = wp[i], xq = wq[i];
+                            wp[i] = c * xp - s * xq;
+                            wq[i] = s * xp + c * xq;
+                        }
+                        if (lane < C2) {
+                            const double xp = Jm[p * C2 + lane], xq = Jm[q * C2 + lane];
+                            Jm[p * C2 + lane] = c * xp - s * xq;
+                            Jm[q * C2 + lane] = s * xp + c * xq;
+                        }
+                        if (lane == 0) s_rot = 1;
+                    }
+                }
+                __syncthreads();
+            }
+            if (s_rot) {
+                for (int c = warp; c < C2; c += BW) {
+                    const int gc = gcol(c);
+                    if (gc < n)
+                        for (int i = lane; i < m; i += 32) a.W[i + int64_t(gc) * a.ldw] = Ws[size_t(c) * m + i];
+                }
+                // V(:, cols) <- V(:, cols) * Jm, one row per thread
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    double x[C2], y[C2];
+#pragma unroll
+                    for (int c = 0; c < C2; ++c) {
+                        const int gc = gcol(c);
+                        x[c] = gc < n ? a.V[i + int64_t(gc) * a.ldv] : 0.0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < C2; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int t = 0; t < C2; ++t) s += x[t] * Jm[c * C2 + t];
+                        y[c] = s;
+                    }
+#pragma unroll
+                    for (int c = 0; c < C2; ++c) {
+                        const int gc = gcol(c);
+                        if (gc < n) a.V[i + int64_t(gc) * a.ldv] = y[c];
+                    }
+                }
+                if (threadIdx.x == 0) flags[sweep % 3] = 1;
+            }
+            grid.sync();
+        }
+        const int rotated = flags[sweep % 3];
+        ++sweep;
+        if (!rotated || n < 2) break;
+    }
+    if (g == 0 && threadIdx.x == 0) flags[4] = sweep;
+}
+
 // sigma_j = ||W(:,j)||, one warp per column (fixed order)
 __global__ void colnorm_kernel(const double* W, int64_t ldw, int m, int n, double* out) {
     const int lane = threadIdx.x & 31;
@@ -395,11 +522,36 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     a.V = V.m.p;
     a.ldv = V.m.ld;
     a.flags = flags.i();
-    const int pairs = (n + 1) / 2;
-    const int G = coop_grid(ctx, (const void*)onesided_jacobi_kernel, ceil_div(pairs, kJacThreads / 32));
-    void* args[] = {&a};
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)onesided_jacobi_kernel, dim3(G), dim3(kJacThreads),
-                                          args, 0, ctx.stream));
+    constexpr int BW = 8;
+    const size_t bj_smem = sizeof(double) * (size_t(2 * BW) * m + 4 * BW * BW);
+    const int nblk = ceil_div(n, BW) + (ceil_div(n, BW) & 1);
+    int per_sm = 0;
+    if (bj_smem <= 200 * 1024 && n > 2 * BW) {
+        RLRA_CUDA(cudaFuncSetAttribute(block_jacobi_kernel<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(bj_smem)));
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_jacobi_kernel<BW>, BW * 32,
+                                                                bj_smem));
+    }
+    if (per_sm > 0 && nblk / 2 <= per_sm * ctx.num_sms) {
+        BlockJacArgs b;
+        b.W = W.m.p;
+        b.ldw = W.m.ld;
+        b.m = m;
+        b.n = n;
+        b.V = V.m.p;
+        b.ldv = V.m.ld;
+        b.nb = nblk;
+        b.flags = flags.i();
+        void* args[] = {&b};
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
+                                              args, bj_smem, ctx.stream));
+    } else {
+        const int pairs = (n + 1) / 2;
+        const int G = coop_grid(ctx, (const void*)onesided_jacobi_kernel, ceil_div(pairs, kJacThreads / 32));
+        void* args[] = {&a};
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)onesided_jacobi_kernel, dim3(G), dim3(kJacThreads),
+                                              args, 0, ctx.stream));
+    }
     ++ctx.launches;
     colnorm_kernel<<<ceil_div(n, 8), 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, sg.d());
     rank_desc_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(sg.d(), n, rank.i());
@@ -422,6 +574,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         if (ctx.h_flags[3] == RLRA_ECONV)
             raise(RLRA_ECONV, fmt("small_svd: no convergence after %d sweeps on %dx%d input",
                                   kOneSidedSweepCap, m, n));
+        if (prof.idx >= 0) ctx.prof[prof.idx].K = ctx.h_flags[4];  // sweeps used
         bool any = false;
         for (int j = 0; j < n; ++j) any |= h[j] != 0;
         if (any) {

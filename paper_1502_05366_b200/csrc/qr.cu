@@ -285,6 +285,8 @@ void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int 
 }
 
 bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
+    ProfScope prof(ctx, "chol", int(G.rows), int(G.rows), 0, 0.0);
+    GemmTag tag(ctx, "gemm_chol");
     const int n = int(G.rows);
     Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
     RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
@@ -381,6 +383,7 @@ QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R) {
 QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
     const int m = int(Y.rows), n = int(Y.cols);
     ProfScope prof(ctx, "orth", m, n, 0, 0.0);
+    GemmTag tag(ctx, "gemm_orth");
     if (m < n)
         raise(RLRA_EDIM, fmt("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
     QrResult res;
