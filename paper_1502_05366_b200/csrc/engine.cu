@@ -146,30 +146,43 @@ void build_interp(Context& ctx, const int* perm, const DMat& T, int n, int k, co
     ++ctx.launches;
 }
 
-void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y) {
+// Re-orthonormalisation between half-multiplies.  Every such basis is
+// consumed only through its span by the next product, so span_only callers
+// (rsvd, id_rand: the sample is never returned) use one CholQR pass; the
+// public sample_right/left keep the reference's fully orthonormal iterates.
+static void orth_mid(Context& ctx, const DMat& Y, bool span_only) {
+    if (span_only)
+        orth_span_inplace(ctx, Y);
+    else
+        orth_inplace(ctx, Y, nullptr);
+}
+
+void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
+                  bool span_only) {
     const int n = int(A.cols);
     sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
     if (q == 0) return;
     DMatBuf Z(ctx, n, l);
     GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
-        if ((2 * j - 2) % s == 0) orth(ctx, Y);
+        if ((2 * j - 2) % s == 0) orth_mid(ctx, Y, span_only);
         gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z);  // Z = A^T Y
-        if ((2 * j - 1) % s == 0) orth(ctx, Z);
+        if ((2 * j - 1) % s == 0) orth_mid(ctx, Z, span_only);
         gemm(ctx, Op::N, Op::N, 1.0, A, Z, 0.0, Y);  // Y = A Z
     }
 }
 
-void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt) {
+void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt,
+                   bool span_only) {
     const int m = int(A.rows);
     sketch(ctx, Op::T, A, l, om, Yt);  // (A^T) * Omega~, Omega~ m x l
     if (q == 0) return;
     DMatBuf Z(ctx, m, l);
     GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
-        if ((2 * j - 2) % s == 0) orth(ctx, Yt);
+        if ((2 * j - 2) % s == 0) orth_mid(ctx, Yt, span_only);
         gemm(ctx, Op::N, Op::N, 1.0, A, Yt, 0.0, Z);  // (A^T)^T Yt
-        if ((2 * j - 1) % s == 0) orth(ctx, Z);
+        if ((2 * j - 1) % s == 0) orth_mid(ctx, Z, span_only);
         gemm(ctx, Op::T, Op::N, 1.0, A, Z, 0.0, Yt);
     }
 }
@@ -193,7 +206,7 @@ void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, 
         RLRA_CUDA(cudaMemcpyAsync(sigma, sb.p, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx.stream));
         return;
     }
-    sample_right(ctx, A, l, q, s, om, Y);
+    sample_right(ctx, A, l, q, s, om, Y, /*span_only=*/true);
     orth(ctx, Y);
     GemmTag tag(ctx, "gemm_proj");
     if (variant == RLRA_RSVD_V2) {
@@ -219,15 +232,18 @@ QbOut qb_blocked(Context& ctx, const DMat& W, int blk, int num_blocks, double to
         if (width < 1) break;
         const DMat Qi = Q.block(0, out.ell, m, width);
         const DMat Zi = Z.m.block(0, 0, n, width);
+        // Q_i must leave this block orthonormal; every earlier orth only feeds
+        // the span of the next product (or of the reorth projection).
+        const bool reorth = (i % reorth_period == 0);
         sketch(ctx, Op::N, W, width, om, Qi);  // W * Omega_i (qb.hpp:119-121)
-        orth(ctx, Qi);
+        orth_mid(ctx, Qi, q_power > 0 || reorth);
         for (int j = 0; j < q_power; ++j) {
             gemm(ctx, Op::T, Op::N, 1.0, W, Qi, 0.0, Zi);
-            orth(ctx, Zi);
+            orth_mid(ctx, Zi, true);
             gemm(ctx, Op::N, Op::N, 1.0, W, Zi, 0.0, Qi);
-            orth(ctx, Qi);
+            orth_mid(ctx, Qi, j + 1 < q_power || reorth);
         }
-        if (i % reorth_period == 0) {  // qb.hpp:126-130
+        if (reorth) {  // qb.hpp:126-130
             if (out.ell > 0) {
                 const DMat Qp = Q.block(0, 0, m, out.ell);
                 const DMat Pi = P.m.block(0, 0, out.ell, width);
@@ -293,7 +309,7 @@ IdOut id_rand(Context& ctx, const DMat& A, int k, int p, int q, int s, OmegaSour
               const DMat& V) {
     const int n = int(A.cols), l = k + p;
     DMatBuf Yt(ctx, n, l), Y(ctx, l, n), S1(ctx, l, n);
-    sample_left_t(ctx, A, l, q, s, om, Yt);
+    sample_left_t(ctx, A, l, q, s, om, Yt, /*span_only=*/true);
     transpose_mat(ctx, Yt, Y);
     pivoted_qr(ctx, Y, l, 0.0, nullptr, S1, jc);  // interp.hpp:209
     IdOut out;

@@ -17,10 +17,14 @@ struct OmegaSource {
 };
 
 // sketch.hpp:44-60 — Y (m x l)
-void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y);
+// span_only: intermediate re-orthonormalisations keep the span but not an
+// orthonormal basis (callers that never expose the sample).
+void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
+                  bool span_only = false);
 // sketch.hpp:65-67 — returns Y^T (n x l) of the reference's l x n sample,
 // computed on A directly (the reference materialises A^T; we never do).
-void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt);
+void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt,
+                   bool span_only = false);
 
 // rsvd.hpp:127-160; U m x k, sigma (device) k, V n x k
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,

@@ -141,11 +141,22 @@ __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
             const int bI = min(b1, b2), bJ = max(b1, b2);
             auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
             // stage W columns (zero-padded past n) and reset the rotation
+            // cp.async so all of a column's loads are in flight at once
+            // (a load-then-store loop would serialise on L2 latency)
             for (int c = warp; c < C2; c += BW) {
                 const int gc = gcol(c);
-                for (int i = lane; i < m; i += 32)
-                    Ws[size_t(c) * m + i] = gc < n ? a.W[i + int64_t(gc) * a.ldw] : 0.0;
+                double* dst = Ws + size_t(c) * m;
+                if (gc < n) {
+                    const double* src = a.W + int64_t(gc) * a.ldw;
+                    for (int i = lane; i < m; i += 32) {
+                        const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src + i));
+                    }
+                } else {
+                    for (int i = lane; i < m; i += 32) dst[i] = 0.0;
+                }
             }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
             for (int e = threadIdx.x; e < C2 * C2; e += blockDim.x) Jm[e] = (e % C2 == e / C2) ? 1.0 : 0.0;
             if (threadIdx.x == 0) s_rot = 0;
             __syncthreads();

@@ -410,4 +410,27 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
     return res;
 }
 
+QrResult orth_span_inplace(Context& ctx, const DMat& Y) {
+    const int m = int(Y.rows), n = int(Y.cols);
+    ProfScope prof(ctx, "orth", m, n, 1, 0.0);
+    GemmTag tag(ctx, "gemm_orth");
+    if (m < n) return orth_inplace(ctx, Y, nullptr);
+    QrResult res;
+    if (n == 0) return res;
+    // one CholQR pass: Y <- Y R^{-1}.  range(Y R^{-1}) = range(Y) exactly;
+    // the basis is orthonormal to O(u kappa(Y)^2), which the pivot floor
+    // bounds; callers only use the span before the next full orth.
+    DMatBuf G1(ctx, n, n), R1i(ctx, n, n);
+    GemmOpts sy;
+    sy.upper_tiles_only = true;
+    gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G1, sy);
+    if (!chol_upper_inv(ctx, G1, R1i, ctx.cholqr_pivot_floor)) return orth_inplace(ctx, Y, nullptr);
+    DMatBuf Q1(ctx, m, n);
+    GemmOpts tri;
+    tri.tri_b_upper = true;
+    gemm(ctx, Op::N, Op::N, 1.0, Y, R1i, 0.0, Q1, tri);
+    copy_mat(ctx, Q1, Y);
+    return res;
+}
+
 }  // namespace rlra_b200

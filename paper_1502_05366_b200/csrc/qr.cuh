@@ -24,6 +24,13 @@ struct QrResult {
 // upper-triangular factor (diag >= 0, strictly lower part zeroed).
 QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R);
 
+// Re-orthonormalisation inside a power iteration, where only range(Y)
+// feeds the next product (sketch.hpp:53-58, qb.hpp:122-125): one CholQR pass,
+// span-exact; falls back to orth_inplace when the Gram is too ill-conditioned.
+// The basis handed to any consumer that needs orthonormality (the final Q,
+// the Q_i appended by QB) always comes from orth_inplace.
+QrResult orth_span_inplace(Context& ctx, const DMat& Y);
+
 // Always the Householder path (used for the fallback and for tests).
 QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R);
 
