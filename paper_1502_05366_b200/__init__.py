@@ -535,6 +535,39 @@ class Engine:
                                p, q, s, C.byref(om), C.c_void_p(u_ptr), _i64(m),
                                C.c_void_p(sigma_ptr), C.c_void_p(v_ptr), _i64(n)))
 
+    def device_qb_blocked(self, a_ptr, m, n, lda, inplace, b, num_blocks, tol, q_power,
+                          reorth_period, omega, q_ptr, ldq, b_ptr, ldb, cap):
+        """rlra_qb_blocked on device buffers; omega in callback mode must use
+        substreams (Omega.from_rng(rng, substream=True))."""
+        om = omega.struct()
+        hist = np.zeros(max(num_blocks, 1))
+        ell, nh, reached = C.c_int(0), C.c_int(0), C.c_int(0)
+        fin = C.c_double(0)
+        _check(lib().rlra_qb_blocked(self._ctx, DEVICE, C.c_void_p(a_ptr), m, n, _i64(lda),
+                                     int(inplace), b, num_blocks, C.c_double(tol), q_power,
+                                     reorth_period, C.byref(om), C.c_void_p(q_ptr), _i64(ldq),
+                                     C.c_void_p(b_ptr), _i64(ldb), cap, C.byref(ell), _d(hist),
+                                     C.byref(nh), C.byref(fin), C.byref(reached)))
+        return dict(ell=ell.value, history=hist[:nh.value].copy(), final_residual=fin.value,
+                    tolerance_reached=bool(reached.value))
+
+    def device_svd_from_qb(self, q_ptr, m, ldq, b_ptr, n, ldb, ell, k, vnum, u_ptr, ldu, s_ptr,
+                           v_ptr, ldv):
+        ko = C.c_int(0)
+        _check(lib().rlra_svd_from_qb(self._ctx, DEVICE, C.c_void_p(q_ptr), m, _i64(ldq),
+                                      C.c_void_p(b_ptr), n, _i64(ldb), ell, k, vnum,
+                                      C.c_void_p(u_ptr), _i64(ldu), C.c_void_p(s_ptr),
+                                      C.c_void_p(v_ptr), _i64(ldv), C.byref(ko)))
+        return ko.value
+
+    def device_id_rand(self, a_ptr, m, n, lda, k, p, q, s, omega, jc_ptr, v_ptr, ldv):
+        om = omega.struct()
+        res, cl = C.c_double(0), C.c_int(0)
+        _check(lib().rlra_id_rand(self._ctx, DEVICE, C.c_void_p(a_ptr), m, n, _i64(lda), k, p, q,
+                                  s, C.byref(om), C.c_void_p(jc_ptr), C.c_void_p(v_ptr),
+                                  _i64(ldv), C.byref(res), C.byref(cl)))
+        return dict(qr_residual=res.value, clamped=bool(cl.value))
+
     def device_matmul(self, ta, tb, a_ptr, ar, ac, lda, b_ptr, br, bc, ldb, c_ptr, ldc):
         _check(lib().rlra_matmul(self._ctx, DEVICE, int(ta), int(tb), C.c_void_p(a_ptr), ar, ac,
                                  _i64(lda), C.c_void_p(b_ptr), br, bc, _i64(ldb),
