@@ -229,6 +229,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--m", type=int, default=C5["m"])
     ap.add_argument("--n", type=int, default=C5["n"])
+    ap.add_argument("--dist", action="store_true",
+                    help="use the row-sharded NCCL path even at N=1 (exercises dist.py)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -239,33 +241,58 @@ def main():
     import paper_1502_05366_b200 as R
 
     rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # --dist at N=1: exercise the row-sharded path with a 1-rank NCCL group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=dev)
     eng = R.Engine(local)
     cfg = dict(C5)
     cfg["m"], cfg["n"] = args.m, args.n
     m, n, k, p, q, s = cfg["m"], cfg["n"], cfg["k"], cfg["p"], cfg["q"], cfg["s"]
-    l = k + p
-    # Row-sharded replicas: with N ranks each rank factors its own C5-sized
-    # problem?  No: C5 is strong-scaled; the multi-GPU row-sharded engine is
-    # not in this round, so N>1 runs replicas and says so in config.
-    A, sig_true = generate_c5(eng, torch, dev, m, n, SEED_GEN + 1000 * rank)
-    U = torch.empty(m * k, dtype=torch.float64, device=dev)
-    V = torch.empty(n * k, dtype=torch.float64, device=dev)
-    S = torch.empty(k, dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+    if not use_dist:
+        # one GPU: the whole factorization is one C-ABI call
+        m_loc, row0 = m, 0
+        A, sig_true = generate_c5(eng, torch, dev, m, n, SEED_GEN)
+        U = torch.empty(m * k, dtype=torch.float64, device=dev)
+        V = torch.empty(n * k, dtype=torch.float64, device=dev)
+        S = torch.empty(k, dtype=torch.float64, device=dev)
 
-    def step(seed):
-        eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, s, R.Omega.philox(seed),
-                        U.data_ptr(), S.data_ptr(), V.data_ptr())
+        def step(seed):
+            eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, s, R.Omega.philox(seed),
+                            U.data_ptr(), S.data_ptr(), V.data_ptr())
+    else:
+        # N GPUs: A row-sharded (strong scaling of the same C5 matrix), NCCL
+        # allreduce of the Grams and of the n x l partials (dist.py)
+        from paper_1502_05366_b200 import dist as D
+
+        be = D.GpuBackend(eng)
+        bounds = np.linspace(0, m, world + 1).astype(int)
+        row0, m_loc = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
+        Ad, sig_true = D.gen_test_matrix_rowsharded(be, n, row0, m_loc,
+                                                    np.exp(-np.arange(3685) / 100.0), SEED_GEN)
+        A = Ad.t
+        out = {}
+
+        def step(seed):
+            out["U"], out["S"], out["V"] = D.rsvd_v2_rowsharded(be, Ad, m, k, p, q, s,
+                                                                R.Omega.philox(seed))
 
     for w in range(args.warmup):
         step(SEED_OMEGA + w)
     eng.synchronize()
-    if world > 1:
+    if use_dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
 
@@ -285,13 +312,13 @@ def main():
     eng.profile(False)
     clk = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms_total], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     F = f_gemm(m, n, k, p, q)
-    value = world * F / (ms_step * 1e-3) / 1e12
+    value = F / (ms_step * 1e-3) / 1e12  # the whole job: one C5 factorization per step
 
     # dominant kernel: the DMMA GEMMs that stream A (M or K == m)
     big = [r for r in prof if r["name"] in ("gemm_sketch", "gemm_power", "gemm_proj")]
@@ -307,7 +334,15 @@ def main():
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
 
     # relative error of the last factorization (device reduction)
-    err = eng.device_rel_error(A.data_ptr(), m, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
+    if not use_dist:
+        err = eng.device_rel_error(A.data_ptr(), m, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
+    else:
+        U, S, V = out["U"].t, out["S"].t[:k], out["V"].t
+        e_loc = eng.device_rel_error(A.data_ptr(), m_loc, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
+        a2 = float(torch.sum(A ** 2))
+        tt = torch.tensor([e_loc ** 2 * a2, a2], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt)
+        err = float(torch.sqrt(tt[0] / tt[1]))
     sig = S.cpu().numpy()
     st = sig_true[:k].cpu().numpy()
     sig_rel = float(np.max(np.abs(sig[:100] - st[:100]) / st[:100]))
@@ -316,12 +351,14 @@ def main():
         "metric": "rsvd_v2 effective FP64 TFLOP/s (F_gemm = 4mnl(q+1) / time), C5 workload",
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if world == 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: A = U diag(exp(-j/100)) V^T, U,V orthonormalised Philox Gaussians "
                 "(3685 modes), generated on the GPU",
         "config": {"workload": f"C5 rsvd_v2 m={m} n={n} k={k} p={p} q={q} s={s}",
                    "omega": "philox in-register", "l2": "A (32 GB) >> L2; no flush needed",
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+                   "parallelism": "1 GPU" if not use_dist else
+                   f"A row-sharded over {world} GPUs ({m_loc} rows/rank), NCCL allreduce of "
+                   "Grams and n x l partials"},
         "time_s": ms_step / 1e3,
         "frac_of_fp64_peak": value / world / FP64_DMMA_PEAK_TFLOPS,
         "phases_ms": {k_: round(v_, 3) for k_, v_ in sorted(phases.items())},
@@ -337,29 +374,44 @@ def main():
 
     # ---------------------------------------------- e2e through the C-ABI --
     if not args.no_e2e:
-        Ah = torch.empty(m * n, dtype=torch.float64, pin_memory=True)
+        Ah = torch.empty(m_loc * n, dtype=torch.float64, pin_memory=True)
         Ah.copy_(A)
-        del A
-        torch.cuda.empty_cache()
-        Uh = torch.empty(m * k, dtype=torch.float64, pin_memory=True)
+        Uh = torch.empty(m_loc * k, dtype=torch.float64, pin_memory=True)
         Vh = torch.empty(n * k, dtype=torch.float64, pin_memory=True)
         Sh = torch.empty(k, dtype=torch.float64, pin_memory=True)
         e2e_steps = max(1, min(args.steps, 3))
+        if not use_dist:
+            del A
+            torch.cuda.empty_cache()
 
-        def estep(seed):
-            eng.host_rsvd_ptr(R.RSVD_V2, Ah.data_ptr(), m, n, m, k, p, q, s, R.Omega.philox(seed),
-                              Uh.data_ptr(), Sh.data_ptr(), Vh.data_ptr())
+            def estep(seed):  # the drop-in call with host buffers
+                eng.host_rsvd_ptr(R.RSVD_V2, Ah.data_ptr(), m, n, m, k, p, q, s,
+                                  R.Omega.philox(seed), Uh.data_ptr(), Sh.data_ptr(), Vh.data_ptr())
+            path = "rlra_rsvd(loc=RLRA_HOST), pinned host A"
+        else:
+            def estep(seed):  # each rank uploads its shard, factors, downloads its U rows
+                Ad.t.copy_(Ah)
+                step(seed)
+                Uh.copy_(out["U"].t[: m_loc * k])
+                Sh.copy_(out["S"].t[:k])
+                Vh.copy_(out["V"].t[: n * k])
+            path = "dist.rsvd_v2_rowsharded with per-rank pinned host shards"
 
         estep(SEED_OMEGA)
+        if use_dist:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         for i in range(e2e_steps):
             estep(SEED_OMEGA + 200 + i)
         te = (time.perf_counter() - t0) / e2e_steps
-        line["e2e"] = {"value": world * F / te / 1e12, "unit": "TFLOP/s",
+        if use_dist:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        line["e2e"] = {"value": F / te / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": 8 * m * n,
-                       "d2h_bytes_per_step": 8 * (m * k + n * k + k),
-                       "ms_per_step": te * 1e3, "steps": e2e_steps,
-                       "path": "rlra_rsvd(loc=RLRA_HOST), pinned host A"}
+                       "d2h_bytes_per_step": 8 * (m * k + world * (n * k + k)),
+                       "ms_per_step": te * 1e3, "steps": e2e_steps, "path": path}
 
     # ------------------------------------------------------ cpu baseline --
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -381,7 +433,7 @@ def main():
                                     "sample": f"failed: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
 
 

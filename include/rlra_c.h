@@ -156,6 +156,36 @@ rlra_status rlra_sym_eig(rlra_ctx* ctx, int loc, const double* t, int n, int64_t
 rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, int n,
                                 int64_t lda, double* out);
 
+/* ------------------------------------------ row-sharded building blocks ---
+ * The multi-GPU path (paper_1502_05366_b200/dist.py) row-shards A across
+ * ranks and runs these per-shard steps between NCCL collectives: the sketch
+ * with a global row offset (so every rank sees the same Philox Omega), the
+ * local Gram of a CholQR pass, the replicated Cholesky + inverse of the
+ * allreduced Gram, and the local triangular update. */
+
+/* Y = op(A) * Omega_draw.  trans = 0: A m x n, Omega n x l, Y m x l;
+ * trans = 1: A m x n, Omega m x l (rows row0.. of the global Omega), Y n x l. */
+rlra_status rlra_sketch(rlra_ctx* ctx, int loc, int trans, const double* a, int m, int n,
+                        int64_t lda, int l, const rlra_omega* omega, int draw, int64_t row0,
+                        double* y, int64_t ldy);
+
+/* G = Y^T Y (n x n, full symmetric) for Y m x n. */
+rlra_status rlra_gram(rlra_ctx* ctx, int loc, const double* y, int m, int n, int64_t ldy,
+                      double* g, int64_t ldg);
+
+/* Upper Cholesky G = R^T R and R^{-1} (both n x n, strictly lower parts 0).
+ * *ok = 0 when a pivot falls below floor * (original diagonal); then R and
+ * Rinv are unusable.  G is not modified. */
+rlra_status rlra_chol_inv(rlra_ctx* ctx, int loc, const double* g, int n, int64_t ldg,
+                          double floor, double* r, int64_t ldr, double* rinv, int64_t ldri,
+                          int* ok);
+
+/* out = Y * T for Y (m x n) and upper-triangular T (n x n); out may not
+ * alias Y. */
+rlra_status rlra_trmm_right_upper(rlra_ctx* ctx, int loc, const double* y, int m, int n,
+                                  int64_t ldy, const double* t, int64_t ldt, double* out,
+                                  int64_t ldo);
+
 /* ||A - X Y^T||_F for A (m x n), X (m x k), Y (n x k): the dense
  * reconstruction residual of report.hpp:97-113 (and of the CUR residual,
  * interp.hpp:175) as one fused GEMM + subtract + sum-of-squares pass that

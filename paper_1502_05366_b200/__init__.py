@@ -568,6 +568,41 @@ class Engine:
                                   _i64(ldv), C.byref(res), C.byref(cl)))
         return dict(qr_residual=res.value, clamped=bool(cl.value))
 
+    # -- row-sharded building blocks (dist.py) --------------------------------
+    def device_sketch(self, trans, a_ptr, m, n, lda, l, omega, draw, row0, y_ptr, ldy):
+        om = omega.struct()
+        _check(lib().rlra_sketch(self._ctx, DEVICE, int(trans), C.c_void_p(a_ptr), m, n, _i64(lda),
+                                 l, C.byref(om), draw, _i64(row0), C.c_void_p(y_ptr), _i64(ldy)))
+
+    def device_gram(self, y_ptr, m, n, ldy, g_ptr, ldg):
+        _check(lib().rlra_gram(self._ctx, DEVICE, C.c_void_p(y_ptr), m, n, _i64(ldy),
+                               C.c_void_p(g_ptr), _i64(ldg)))
+
+    def device_chol_inv(self, g_ptr, n, ldg, floor, r_ptr, ldr, ri_ptr, ldri):
+        ok = C.c_int(0)
+        _check(lib().rlra_chol_inv(self._ctx, DEVICE, C.c_void_p(g_ptr), n, _i64(ldg),
+                                   C.c_double(floor), C.c_void_p(r_ptr), _i64(ldr),
+                                   C.c_void_p(ri_ptr), _i64(ldri), C.byref(ok)))
+        return bool(ok.value)
+
+    def device_trmm_right_upper(self, y_ptr, m, n, ldy, t_ptr, ldt, o_ptr, ldo):
+        _check(lib().rlra_trmm_right_upper(self._ctx, DEVICE, C.c_void_p(y_ptr), m, n, _i64(ldy),
+                                           C.c_void_p(t_ptr), _i64(ldt), C.c_void_p(o_ptr),
+                                           _i64(ldo)))
+
+    def device_compact_qr(self, a_ptr, m, n, lda, q_ptr, ldq, r_ptr, ldr):
+        deg = C.c_int(0)
+        _check(lib().rlra_compact_qr(self._ctx, DEVICE, C.c_void_p(a_ptr), m, n, _i64(lda),
+                                     C.c_void_p(q_ptr), _i64(ldq),
+                                     C.c_void_p(r_ptr) if r_ptr else None, _i64(ldr),
+                                     C.byref(deg)))
+        return bool(deg.value)
+
+    def device_small_svd(self, a_ptr, m, n, lda, u_ptr, ldu, s_ptr, v_ptr, ldv):
+        _check(lib().rlra_small_svd(self._ctx, DEVICE, C.c_void_p(a_ptr), m, n, _i64(lda),
+                                    C.c_void_p(u_ptr), _i64(ldu), C.c_void_p(s_ptr),
+                                    C.c_void_p(v_ptr), _i64(ldv)))
+
     def device_matmul(self, ta, tb, a_ptr, ar, ac, lda, b_ptr, br, bc, ldb, c_ptr, ldc):
         _check(lib().rlra_matmul(self._ctx, DEVICE, int(ta), int(tb), C.c_void_p(a_ptr), ar, ac,
                                  _i64(lda), C.c_void_p(b_ptr), br, bc, _i64(ldb),

@@ -389,6 +389,82 @@ rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, 
     });
 }
 
+rlra_status rlra_sketch(rlra_ctx* ctx, int loc, int trans, const double* a, int m, int n, int64_t lda, int l,
+                        const rlra_omega* omega, int draw, int64_t row0, double* y, int64_t ldy) {
+    return guard(ctx, [&](Context& C) {
+        if (l < 1) raise(RLRA_EDIM, fmt("sketch: width %d", l));
+        const rlra_omega* o = omega;
+        if (!o) raise(RLRA_EINVAL, "null rlra_omega");
+        In A(C, loc, a, m, n, lda, "a");
+        const int orows = trans ? m : n, yrows = trans ? n : m;
+        Out Y(C, loc, y, yrows, l, ldy, "y");
+        GemmTag tag(C, "gemm_sketch");
+        if (o->mode == RLRA_OMEGA_PHILOX) {
+            GemmOpts g;
+            g.philox_b = true;
+            g.seed = o->seed;
+            g.draw = draw;
+            g.krow0 = row0;
+            gemm(C, trans ? Op::T : Op::N, Op::N, yrows, l, orows, 1.0, A.m.p, A.m.ld, nullptr, orows, 0.0,
+                 Y.m.p, Y.m.ld, g);
+        } else {
+            if (!o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
+            std::vector<double> h(size_t(orows) * l);
+            o->fill(o->user, draw, orows, l, h.data());
+            DMatBuf Om(C, orows, l);
+            RLRA_CUDA(cudaMemcpyAsync(Om.m.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
+                                      C.stream));
+            gemm(C, trans ? Op::T : Op::N, Op::N, 1.0, A.m, Om, 0.0, Y.m);
+            sync(C);
+        }
+        Y.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_gram(rlra_ctx* ctx, int loc, const double* y, int m, int n, int64_t ldy, double* g,
+                      int64_t ldg) {
+    return guard(ctx, [&](Context& C) {
+        In Y(C, loc, y, m, n, ldy, "y");
+        Out G(C, loc, g, n, n, ldg, "g");
+        GemmOpts sy;
+        sy.upper_tiles_only = true;
+        gemm(C, Op::T, Op::N, 1.0, Y.m, Y.m, 0.0, G.m, sy);
+        symmetrize_upper(C, G.m);
+        G.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_chol_inv(rlra_ctx* ctx, int loc, const double* g, int n, int64_t ldg, double floor, double* r,
+                          int64_t ldr, double* rinv, int64_t ldri, int* ok) {
+    return guard(ctx, [&](Context& C) {
+        In G(C, loc, g, n, n, ldg, "g");
+        Out Rm(C, loc, r, n, n, ldr, "r"), Ri(C, loc, rinv, n, n, ldri, "rinv");
+        copy_mat(C, G.m, Rm.m);
+        const bool good = chol_upper_inv(C, Rm.m, Ri.m, floor);
+        Rm.finish(C);
+        Ri.finish(C);
+        sync(C);
+        if (ok) *ok = good ? 1 : 0;
+    });
+}
+
+rlra_status rlra_trmm_right_upper(rlra_ctx* ctx, int loc, const double* y, int m, int n, int64_t ldy,
+                                  const double* t, int64_t ldt, double* out, int64_t ldo) {
+    return guard(ctx, [&](Context& C) {
+        if (y == out) raise(RLRA_EINVAL, "trmm_right_upper: out aliases y");
+        In Y(C, loc, y, m, n, ldy, "y"), T(C, loc, t, n, n, ldt, "t");
+        Out O(C, loc, out, m, n, ldo, "out");
+        GemmOpts tri;
+        tri.tri_b_upper = true;
+        GemmTag tag(C, "gemm_orth");
+        gemm(C, Op::N, Op::N, 1.0, Y.m, T.m, 0.0, O.m, tri);
+        O.finish(C);
+        sync(C);
+    });
+}
+
 rlra_status rlra_lowrank_residual(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                                   const double* x, int64_t ldx, const double* y, int64_t ldy, int k,
                                   double* out) {
