@@ -210,7 +210,11 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
                 const int64_t ctas = tiles * s;
                 return double(ctas) / double(((ctas + cap - 1) / cap) * cap);
             };
-            const int64_t kmaxs = std::min<int64_t>(64, std::max<int64_t>(1, K / (8 * BK)));
+            // at most 8 splits and 512 MB of partials: beyond that the extra
+            // workspace traffic outweighs the last percent of wave fill
+            const int64_t ws_cap = (int64_t(512) << 20) / (8 * int64_t(M) * N + 1);
+            const int64_t kmaxs = std::min<int64_t>(std::min<int64_t>(8, std::max<int64_t>(1, ws_cap)),
+                                                    std::max<int64_t>(1, K / (8 * BK)));
             double best = eff(1);
             for (int64_t s = 2; s <= kmaxs; ++s)
                 if (eff(s) > best + 0.02) {
