@@ -255,6 +255,18 @@ class Engine:
                                      _i64(max(1, m)), None, _i64(1), C.byref(deg)))
         return q
 
+    def chol_inv(self, g, floor=0.0):
+        """Upper Cholesky G = R^T R (upper triangle of g read) and R^{-1}:
+        the CholQR kernel (qr.cu).  Returns (R, R^{-1}, ok)."""
+        g = _F(g)
+        n = g.shape[0]
+        r = np.zeros((n, n), order="F")
+        ri = np.zeros((n, n), order="F")
+        ok = C.c_int(0)
+        _check(lib().rlra_chol_inv(self._ctx, HOST, _d(g), n, _i64(_ld(g)), C.c_double(floor), _d(r),
+                                   _i64(max(1, n)), _d(ri), _i64(max(1, n)), C.byref(ok)))
+        return r, ri, bool(ok.value)
+
     def pivoted_qr_partial(self, a, k, tol=0.0):
         a = _F(a)
         m, n = a.shape

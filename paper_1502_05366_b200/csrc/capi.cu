@@ -204,6 +204,8 @@ rlra_status rlra_ctx_create(int device, rlra_ctx** out) {
         RLRA_CUDA(cudaMemPoolSetAttribute(ctx->c.pool, cudaMemPoolAttrReleaseThreshold, &thr));
         RLRA_CUDA(cudaMallocHost(&ctx->c.h_scalars, 64 * sizeof(double)));
         RLRA_CUDA(cudaMallocHost(&ctx->c.h_flags, 64 * sizeof(int)));
+        RLRA_CUDA(cudaMalloc(&ctx->c.gbar, 64 * sizeof(unsigned)));
+        RLRA_CUDA(cudaMemset(ctx->c.gbar, 0, 64 * sizeof(unsigned)));
     } catch (const Error& e) {
         g_err = e.msg;
         delete ctx;
@@ -222,6 +224,7 @@ rlra_status rlra_ctx_destroy(rlra_ctx* ctx) {
     }
     if (ctx->c.h_scalars) cudaFreeHost(ctx->c.h_scalars);
     if (ctx->c.h_flags) cudaFreeHost(ctx->c.h_flags);
+    if (ctx->c.gbar) cudaFree(ctx->c.gbar);
     delete ctx;
     return RLRA_OK;
 }

@@ -73,8 +73,12 @@ struct Context {
     int* h_flags = nullptr;       // pinned, 64 ints
     // statistics: kernels launched by this context since last reset
     uint64_t launches = 0;
+    // device grid-barrier state for the cooperative kernels (see grid_sync)
+    unsigned* gbar = nullptr;
     // Cholesky-QR policy knobs (see qr.cu)
     double cholqr_pivot_floor = 1e-12;
+    // force the launch-per-block Cholesky (GEMM trailing updates) for every n
+    bool chol_blocked_gemm = false;
     // optional per-launch / per-phase timing with CUDA events on `stream`
     bool profile = false;
     struct ProfRec {
@@ -160,5 +164,36 @@ struct DMatBuf {
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+// Grid-wide barrier for kernels launched with cudaLaunchCooperativeKernel
+// (co-residency guaranteed).  bar[0] counts arrivals, bar[1] is the
+// generation; the last CTA to arrive resets the count and publishes the next
+// generation with a release store.  Waiters poll with relaxed loads and
+// __nanosleep back-off and take ONE acquire fence on exit, so 147 waiting SMs
+// do not saturate the L2 slice holding the flag (cooperative_groups'
+// grid.sync() re-issues an acquire load + L1 invalidate per poll).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        unsigned gen;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (atomicAdd(bar, 1u) == nb - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1u) : "memory");
+        } else {
+            unsigned cur, ns = 32;
+            for (;;) {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+                if (cur != gen) break;
+                __nanosleep(ns);
+                ns = ns < 256 ? ns * 2 : 256;
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+    }
+    __syncthreads();
+}
 
 }  // namespace rlra_b200

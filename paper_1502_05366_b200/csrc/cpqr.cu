@@ -32,6 +32,7 @@ __device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
 }
 
 struct CpqrArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     double* W;
     int64_t ldw;
     int m, n, kmax, rmax;
@@ -50,7 +51,6 @@ struct CpqrArgs {
 };
 
 __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ double sv[32], st[32];
     __shared__ int sp[32];
     __shared__ double shb[32];
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
         }
         publish(bv, bp, tr);
     }
-    grid.sync();
+    grid_sync(a.bar);
 
     int frank = 0;
     bool reached = false;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
                 if (zero) a.out[2] = 1;
             }
         }
-        grid.sync();
+        grid_sync(a.bar);
         // apply H_f to own trailing positions, downdate (core/qr.hpp:190-200)
         const double beta = a.beta[f];
         const double* v = a.Vst + int64_t(f) * m;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
         }
         publish(bv, bp, tr);
         ++frank;
-        grid.sync();
+        grid_sync(a.bar);
         if (a.tol_mode && frank < a.rmax) {
             double t = 0.0;
             for (int c = 0; c < G; ++c) t += a.slot_t[c];
@@ -369,6 +369,7 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     a.slot_t = stt.d();
     a.out = out.i();
     a.res = res.d();
+    a.bar = ctx.gbar;
     void* args[] = {&a};
     RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_coop_kernel, dim3(G), dim3(kCpqrThreads), args,
                                           0, ctx.stream));

@@ -199,28 +199,35 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
     int64_t tiles = int64_t(p.mt) * p.nt;
     if (o.upper_tiles_only) tiles = int64_t(p.mt) * (p.mt + 1) / 2;
     const int64_t cap = int64_t(ctx.num_sms) * per_sm;
-    // split-K only where it fixes wave quantization: pick the smallest split
-    // count whose CTA waves are fuller (by > 2%) than every smaller one.
+    // split-K where it pays against wave quantization.  Cost model per split
+    // count s: (CTA waves) x (one CTA's k-chunk at the DMMA rate) + the
+    // deterministic reduction ((s+1) M N doubles through HBM) + one launch.
     int splits = 1;
     if (o.epi != EPI_RESID && !o.tri_b_upper) {
         if (o.force_splits > 0) {
             splits = o.force_splits;
         } else {
-            auto eff = [&](int64_t s) {
-                const int64_t ctas = tiles * s;
-                return double(ctas) / double(((ctas + cap - 1) / cap) * cap);
+            const double cta_rate = 2.5e11 / per_sm;  // FP64 flop/s of one CTA (37 TF / 148 SMs)
+            const double hbm = 5.0e12;                // B/s, reduction traffic
+            auto model = [&](int64_t s) {
+                const int64_t kc = int64_t(ceil_div(ceil_div(K, int(s)), BK)) * BK;
+                const int64_t waves = (tiles * s + cap - 1) / cap;
+                double t = double(waves) * 2.0 * BM * BN * double(kc) / cta_rate;
+                if (s > 1) t += double(s + 1) * 8.0 * double(M) * N / hbm + 4e-6;
+                return t;
             };
-            // at most 8 splits and 512 MB of partials: beyond that the extra
-            // workspace traffic outweighs the last percent of wave fill
+            // at most 64 splits, 512 MB of partials and k-chunks of >= 8 BK
             const int64_t ws_cap = (int64_t(512) << 20) / (8 * int64_t(M) * N + 1);
-            const int64_t kmaxs = std::min<int64_t>(std::min<int64_t>(8, std::max<int64_t>(1, ws_cap)),
+            const int64_t kmaxs = std::min<int64_t>(std::min<int64_t>(64, std::max<int64_t>(1, ws_cap)),
                                                     std::max<int64_t>(1, K / (8 * BK)));
-            double best = eff(1);
-            for (int64_t s = 2; s <= kmaxs; ++s)
-                if (eff(s) > best + 0.02) {
-                    best = eff(s);
+            double best = model(1);
+            for (int64_t s = 2; s <= kmaxs; ++s) {
+                const double t = model(s);
+                if (t < best * 0.995) {
+                    best = t;
                     splits = int(s);
                 }
+            }
         }
     }
     int k_chunk = ceil_div(ceil_div(K, splits), BK) * BK;

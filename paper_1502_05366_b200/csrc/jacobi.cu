@@ -26,6 +26,7 @@ __device__ __forceinline__ int rr_col(int pos, int r, int n2) {
 }
 
 struct OneSidedArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     double* W;
     int64_t ldw;
     int m, n;
@@ -35,7 +36,6 @@ struct OneSidedArgs {
 };
 
 __global__ void __launch_bounds__(kJacThreads) onesided_jacobi_kernel(OneSidedArgs a) {
-    cg::grid_group grid = cg::this_grid();
     const int n = a.n, m = a.m;
     const int n2 = n + (n & 1);
     const int lane = threadIdx.x & 31;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kJacThreads) onesided_jacobi_kernel(OneSidedAr
                 }
                 if (lane == 0) flags[sweep % 3] = 1;
             }
-            grid.sync();
+            grid_sync(a.bar);
         }
         const int rotated = flags[sweep % 3];
         ++sweep;
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kJacThreads) onesided_jacobi_kernel(OneSidedAr
 // skip rule and the "sweep without rotations" stop are the reference's
 // (core/jacobi.hpp:164-199).
 struct BlockJacArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     double* W;
     int64_t ldw;
     int m, n;
@@ -119,7 +120,6 @@ struct BlockJacArgs {
 template <int BW>
 __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
     constexpr int C2 = 2 * BW;
-    cg::grid_group grid = cg::this_grid();
     extern __shared__ double bj_smem[];
     double* Ws = bj_smem;                      // C2 columns of length m
     double* Jm = bj_smem + size_t(C2) * a.m;   // C2 x C2 accumulated rotation
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
                 }
                 if (threadIdx.x == 0) flags[sweep % 3] = 1;
             }
-            grid.sync();
+            grid_sync(a.bar);
         }
         const int rotated = flags[sweep % 3];
         ++sweep;
@@ -379,6 +379,7 @@ int coop_grid(Context& ctx, const void* kern, int want_blocks) {
 
 // ---------------------------------------------------- two-sided Jacobi ---
 struct TwoSidedArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     double* M;
     int64_t ldm;
     int n;
@@ -391,7 +392,6 @@ struct TwoSidedArgs {
 };
 
 __global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedArgs a) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
     const int n = a.n, n2 = n + (n & 1);
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
@@ -410,11 +410,11 @@ __global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedAr
         }
         v = block_sum_fixed(v, sh);
         if (threadIdx.x == 0) a.part[blockIdx.x] = v;
-        grid.sync();
+        grid_sync(a.bar);
         double off = 0.0;
         for (int b = 0; b < int(gridDim.x); ++b) off += a.part[b];
         off = sqrt(off);
-        grid.sync();
+        grid_sync(a.bar);
         if (!(off > thr)) break;
         if (sweep++ >= kTwoSidedSweepCap) {
             if (gt == 0) *a.status = RLRA_ECONV;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedAr
                 a.cs[3 * pi + 1] = s;
                 a.cs[3 * pi + 2] = act;
             }
-            grid.sync();
+            grid_sync(a.bar);
             // columns of M and U
             for (int64_t e = gt; e < int64_t(n2 / 2) * n; e += nt) {
                 const int pi = int(e / n), i = int(e % n);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedAr
                 up[i] = c * yp - s * yq;
                 uq[i] = s * yp + c * yq;
             }
-            grid.sync();
+            grid_sync(a.bar);
             // rows of M
             for (int64_t e = gt; e < int64_t(n2 / 2) * n; e += nt) {
                 const int pi = int(e / n), i = int(e % n);
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kJacThreads) twosided_jacobi_kernel(TwoSidedAr
                 a.M[p + int64_t(i) * a.ldm] = c * xp - s * xq;
                 a.M[q + int64_t(i) * a.ldm] = s * xp + c * xq;
             }
-            grid.sync();
+            grid_sync(a.bar);
         }
     }
 }
@@ -553,12 +553,14 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         b.ldv = V.m.ld;
         b.nb = nblk;
         b.flags = flags.i();
+        b.bar = ctx.gbar;
         void* args[] = {&b};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
                                               args, bj_smem, ctx.stream));
     } else {
         const int pairs = (n + 1) / 2;
         const int G = coop_grid(ctx, (const void*)onesided_jacobi_kernel, ceil_div(pairs, kJacThreads / 32));
+        a.bar = ctx.gbar;
         void* args[] = {&a};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)onesided_jacobi_kernel, dim3(G), dim3(kJacThreads),
                                               args, 0, ctx.stream));
@@ -645,6 +647,7 @@ void sym_eig(Context& ctx, const DMat& T, double* values, const DMat& vectors) {
     a.part = part2.d();
     a.tnorm = tnorm;
     a.status = status.i();
+    a.bar = ctx.gbar;
     void* args[] = {&a};
     RLRA_CUDA(cudaLaunchCooperativeKernel((void*)twosided_jacobi_kernel, dim3(G), dim3(kJacThreads),
                                           args, 0, ctx.stream));

@@ -1,5 +1,6 @@
 // qr.cu — CholQR2 orthonormalization with a device Householder fallback.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "qr.cuh"
@@ -92,6 +93,7 @@ __global__ void zero_lower_kernel(double* G, int64_t ldg, int n) {
 // the sign convention (:113-119).  Rows are partitioned over CTAs; every
 // column costs three grid barriers (norm, dots, update).
 struct HhArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     double* W;
     int64_t ldw;
     int m, n;
@@ -122,7 +124,6 @@ __device__ double block_sum(double v, double* sh) {
 }
 
 __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
     const int G = gridDim.x, g = blockIdx.x;
     const int rows_per = (a.m + G - 1) / G;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
         }
         v = block_sum(v, sh);
         if (threadIdx.x == 0) a.part[g] = v;
-        grid.sync();
+        grid_sync(a.bar);
         // P2: reflector (every CTA computes the same scalars in the same order)
         double norm2 = 0.0;
         for (int c = 0; c < G; ++c) norm2 += a.part[c];
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
                 if (lane == 0) a.part[int64_t(G) + int64_t(g) * n + j] = s;
             }
         }
-        grid.sync();
+        grid_sync(a.bar);
         // P3: reduce the trailing dots, columns distributed over CTAs
         if (!zero) {
             for (int j = k + 1 + g * blockDim.x + threadIdx.x; j < n; j += G * blockDim.x) {
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
                 a.dots[j] = s;
             }
         }
-        grid.sync();
+        grid_sync(a.bar);
         // P4: apply H_k to own rows of the trailing columns, finish column k
         if (!zero) {
             for (int j = k + 1; j < n; ++j) {
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
 // reflectors (columns of V, scalars beta) applied in reverse order.  Rows are
 // partitioned over CTAs; two grid barriers per reflector.
 struct FormQArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
     const double* V;
     int64_t ldv;
     const double* beta;
@@ -208,7 +210,6 @@ struct FormQArgs {
 };
 
 __global__ void __launch_bounds__(256) formq_coop_kernel(FormQArgs a) {
-    cg::grid_group grid = cg::this_grid();
     const int G = gridDim.x, g = blockIdx.x;
     const int rows_per = (a.m + G - 1) / G;
     const int r0 = g * rows_per, r1 = min(a.m, r0 + rows_per);
@@ -227,13 +228,13 @@ __global__ void __launch_bounds__(256) formq_coop_kernel(FormQArgs a) {
             s = warp_sum(s);
             if (lane == 0) a.part[int64_t(g) * n + j] = s;
         }
-        grid.sync();
+        grid_sync(a.bar);
         for (int j = k + g * blockDim.x + threadIdx.x; j < n; j += G * blockDim.x) {
             double s = 0.0;
             for (int c = 0; c < G; ++c) s += a.part[int64_t(c) * n + j];
             a.dots[j] = s;
         }
-        grid.sync();
+        grid_sync(a.bar);
         for (int j = k; j < n; ++j) {
             const double f = beta * a.dots[j];
             for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x)
@@ -278,16 +279,297 @@ void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int 
     a.dots = dots.d();
     a.Q = Q.p;
     a.ldq = Q.ld;
+    a.bar = ctx.gbar;
     void* args[] = {&a};
     RLRA_CUDA(cudaLaunchCooperativeKernel((void*)formq_coop_kernel, dim3(G), dim3(256), args, 0,
                                           ctx.stream));
     ++ctx.launches;
 }
 
+namespace {
+
+// ------------------------------------------- one-launch blocked Cholesky ---
+// Right-looking blocked Cholesky G = R^T R with the inverse X = R^{-1} carried
+// along, as ONE cooperative kernel with three grid barriers per 64-column
+// block step, for the l x l Grams of the rsvd/QB path (l <= kCholCoopMax).
+// X is accumulated column-block by column-block from X R = I:
+//   X[:, J] = (E_J - sum_{K<J} X[:, K] R[K, J]) X_JJ,
+// the bracket ("acc") living in the X buffer and receiving rank-64 updates.
+// Per step J:
+//  A  CTA 0: diagonal block in shared memory, Schur-complement form (one
+//     barrier per column; pivot test against the original diagonal as the
+//     reference-order chol_diag_kernel), then R_JJ and X_JJ = R_JJ^{-1};
+//  B  warps: panel R[J, J+] = X_JJ^T G[J, J+] (a column per warp) and
+//     X[r, J] = acc[r, J] X_JJ for r < j0 (a row per warp);
+//  C  CTAs, 32 x 32 tiles with K = 64: Schur update G[J+, J+] -= R[J,J+]^T
+//     R[J,J+] (upper tiles) and acc[0:j1, J+] -= X[0:j1, J] R[J, J+].
+constexpr int kCholCoopMax = 1024;
+constexpr int kCP = kCholNB + 1;  // shared-memory pitch
+
+struct CholCoopArgs {
+    unsigned* bar;  // grid_sync state (Context::gbar)
+    double* G;
+    int64_t ldg;
+    int n;
+    double* Rinv;
+    int64_t ldr;
+    double* dorig;  // n
+    double floor;
+    int* flag;
+    unsigned long long* tprobe;  // optional phase timestamps (RLRA_CHOL_PROBE)
+};
+
+__device__ __forceinline__ void chol_probe(unsigned long long* tp, int idx) {
+    if (tp && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tp[idx] = t;
+    }
+}
+
+// out(32 x 32 tile) -= P^T Q with P, Q 64 x 32 staged in s0/s1 ([l][i]).
+__device__ __forceinline__ void chol_tile_update(double (*s0)[kCP], double (*s1)[kCP], int nb,
+                                                 double* out, int64_t ldo, int r0, int c0, int rmax,
+                                                 int cmax, bool upper_only) {
+    const int t = threadIdx.x, i = t & 31, jb = (t >> 5) * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < nb; ++l) {
+        const double av = s0[l][i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += av * s1[l][jb + u];
+    }
+    const int row = r0 + i;
+    double old[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int col = c0 + jb + u;
+        const bool in = row < rmax && col < cmax && (!upper_only || row <= col);
+        old[u] = in ? __ldcg(out + row + int64_t(col) * ldo) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int col = c0 + jb + u;
+        if (row < rmax && col < cmax && (!upper_only || row <= col)) out[row + int64_t(col) * ldo] = old[u] - acc[u];
+    }
+}
+
+__global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
+    extern __shared__ double chol_smem[];
+    double(*s0)[kCP] = reinterpret_cast<double(*)[kCP]>(chol_smem);
+    double(*s1)[kCP] = reinterpret_cast<double(*)[kCP]>(chol_smem + kCholNB * kCP);
+    __shared__ double piv[kCholNB], dref[kCholNB];
+    __shared__ int bad;
+    const int n = a.n, t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
+    double* G = a.G;
+    double* X = a.Rinv;
+    const int64_t ldg = a.ldg, ldr = a.ldr;
+
+    // phase 0: original diagonal, X = I (the accumulator), strictly lower G = 0
+    for (int j = blockIdx.x; j < n; j += gridDim.x)
+        for (int i = t; i < n; i += blockDim.x) {
+            X[i + j * ldr] = (i == j) ? 1.0 : 0.0;
+            if (i == j) a.dorig[i] = G[i + j * ldg];
+            if (i > j) G[i + j * ldg] = 0.0;
+        }
+    grid_sync(a.bar);
+    chol_probe(a.tprobe, 0);
+
+    for (int j0 = 0; j0 < n; j0 += kCholNB) {
+        const int nb = min(kCholNB, n - j0), j1 = j0 + nb, rest = n - j1;
+        // ---------------------------------------------------------- A ---
+        if (blockIdx.x == 0) {
+            const int cj = t & 63, rg = t >> 6;  // thread owns column cj, rows rg + 4u
+            if (t == 0) bad = 0;
+            if (t < kCholNB) dref[t] = t < nb ? a.floor * __ldcg(a.dorig + j0 + t) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = rg + 4 * u;
+                s0[i][cj] = (i <= cj && cj < nb) ? __ldcg(G + (j0 + i) + int64_t(j0 + cj) * ldg) : (i == cj ? 1.0 : 0.0);
+                s1[i][cj] = (i == cj) ? 1.0 : 0.0;
+            }
+            // Schur-complement elimination, column slices in registers:
+            // v[u] = s[rg + 4u][cj]; only the next pivot row is published
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = s0[rg + 4 * u][cj];
+            long long c_0 = clock64();
+            for (int k = 0; k < nb; ++k) {
+                __syncthreads();
+                double d = s0[k][k];
+                if (!(d > 0.0) || !(d >= dref[k])) {
+                    d = fmax(d, 1e-300);
+                    if (t == 0) bad = 1;
+                }
+                if (t == 0) piv[k] = d;
+                const double f = s0[k][cj] * (1.0 / d);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = rg + 4 * u;
+                    if (i > k && i <= cj) v[u] -= s0[k][i] * f;
+                }
+                const int kn = k + 1;
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (rg + 4 * u == kn) s0[kn][cj] = v[u];
+            }
+            __syncthreads();
+            long long c_1 = clock64();
+            // R = D^{-1/2} S (rows scaled), written back; X_JJ comes in phase B
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = rg + 4 * u;
+                if (i < nb && cj < nb)
+                    G[(j0 + i) + int64_t(j0 + cj) * ldg] = (i <= cj) ? v[u] / sqrt(piv[i]) : 0.0;
+            }
+            if (a.tprobe && t == 0 && j0 == 0) a.tprobe[50] = c_1 - c_0;
+            if (t == 0 && bad) *a.flag = 1;
+        }
+        grid_sync(a.bar);
+        chol_probe(a.tprobe, 1 + 3 * (j0 / kCholNB));
+        // ---------------------------------------------------------- B ---
+        // warp triangular solves against R_JJ (staged in s1, identity past nb):
+        //   panel   R_JJ^T R[J, c] = G[J, c]        (a column c per warp)
+        //   rows    X[r, J] R_JJ   = acc[r, J]      (a row r < j0 per warp)
+        //   X_JJ    R_JJ X[J, j]   = e_j            (a column j per warp)
+        for (int e = t; e < kCholNB * kCholNB; e += blockDim.x) {
+            const int i = e % kCholNB, j = e / kCholNB;
+            s1[i][j] = (i < nb && j < nb) ? (i <= j ? __ldcg(G + (j0 + i) + int64_t(j0 + j) * ldg) : 0.0)
+                                          : (i == j ? 1.0 : 0.0);
+        }
+        __syncthreads();
+        if (t < kCholNB) piv[t] = 1.0 / s1[t][t];
+        __syncthreads();
+        for (int it = gw; it < rest + j0 + nb; it += nw) {
+            if (it < rest + j0) {
+                // forward substitution y_i = (b_i - sum_{l<i} R[l][i] y_l) / R_ii
+                const bool panel = it < rest;
+                double* base = panel ? G + (j0 + int64_t(j1 + it) * ldg) : X + (int64_t(it - rest) + int64_t(j0) * ldr);
+                const int64_t st = panel ? 1 : ldr;
+                double b0 = lane < nb ? __ldcg(base + lane * st) : 0.0;
+                double b1 = lane + 32 < nb ? __ldcg(base + (lane + 32) * st) : 0.0;
+                for (int i = 0; i < nb; ++i) {
+                    const double yi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31) * piv[i];
+                    if (lane == (i & 31)) {
+                        if (i < 32) b0 = yi;
+                        else b1 = yi;
+                    }
+                    if (lane > i) b0 -= s1[i][lane] * yi;
+                    if (lane + 32 > i) b1 -= s1[i][lane + 32] * yi;
+                }
+                if (lane < nb) base[lane * st] = b0;
+                if (lane + 32 < nb) base[(lane + 32) * st] = b1;
+            } else {
+                // back substitution R_JJ x = e_j
+                const int j = it - rest - j0;
+                double b0 = lane == j ? 1.0 : 0.0, b1 = lane + 32 == j ? 1.0 : 0.0;
+                for (int l = j; l >= 0; --l) {
+                    const double xl = __shfl_sync(0xffffffffu, l < 32 ? b0 : b1, l & 31) * piv[l];
+                    if (lane == (l & 31)) {
+                        if (l < 32) b0 = xl;
+                        else b1 = xl;
+                    }
+                    if (lane < l) b0 -= s1[lane][l] * xl;
+                    if (lane + 32 < l) b1 -= s1[lane + 32][l] * xl;
+                }
+                if (lane < nb) X[(j0 + lane) + int64_t(j0 + j) * ldr] = b0;
+                if (lane + 32 < nb) X[(j0 + lane + 32) + int64_t(j0 + j) * ldr] = b1;
+            }
+        }
+        grid_sync(a.bar);
+        chol_probe(a.tprobe, 2 + 3 * (j0 / kCholNB));
+        // ---------------------------------------------------------- C ---
+        const int nt = (rest + 31) / 32, ntiles = nt * (nt + 1) / 2;
+        const int rt = (j1 + 31) / 32, natiles = rt * nt;
+        for (int it = blockIdx.x; it < ntiles + natiles; it += gridDim.x) {
+            __syncthreads();
+            if (it < ntiles) {  // Schur: G[c1, c2] -= R[J, c1]^T R[J, c2]
+                int ti = 0, r = it;
+                while (r >= nt - ti) {
+                    r -= nt - ti;
+                    ++ti;
+                }
+                const int c1 = j1 + ti * 32, c2 = j1 + (ti + r) * 32;
+                double p0[8], p1[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = t + u * 256, l = e % kCholNB, i = e / kCholNB;
+                    p0[u] = (l < nb && c1 + i < n) ? __ldcg(G + (j0 + l) + int64_t(c1 + i) * ldg) : 0.0;
+                    p1[u] = (l < nb && c2 + i < n) ? __ldcg(G + (j0 + l) + int64_t(c2 + i) * ldg) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = t + u * 256, l = e % kCholNB, i = e / kCholNB;
+                    s0[l][i] = p0[u];
+                    s1[l][i] = p1[u];
+                }
+                __syncthreads();
+                chol_tile_update(s0, s1, nb, G, ldg, c1, c2, n, n, true);
+            } else {  // acc[r, c] -= X[r, J] R[J, c]
+                const int q = it - ntiles, r0 = (q % rt) * 32, c0 = j1 + (q / rt) * 32;
+                double p0[8], p1[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = t + u * 256;
+                    const int i0 = e % 32, l0 = e / 32, l1 = e % kCholNB, i1 = e / kCholNB;
+                    p0[u] = (l0 < nb && r0 + i0 < j1) ? __ldcg(X + (r0 + i0) + int64_t(j0 + l0) * ldr) : 0.0;
+                    p1[u] = (l1 < nb && c0 + i1 < n) ? __ldcg(G + (j0 + l1) + int64_t(c0 + i1) * ldg) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = t + u * 256;
+                    s0[e / 32][e % 32] = p0[u];
+                    s1[e % kCholNB][e / kCholNB] = p1[u];
+                }
+                __syncthreads();
+                chol_tile_update(s0, s1, nb, X, ldr, r0, c0, j1, n, false);
+            }
+        }
+        grid_sync(a.bar);
+        chol_probe(a.tprobe, 3 + 3 * (j0 / kCholNB));
+    }
+}
+
+bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
+    const int n = int(G.rows);
+    constexpr int smem = 2 * kCholNB * kCP * sizeof(double);
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RLRA_CUDA(cudaFuncSetAttribute(chol_inv_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_inv_coop_kernel, 256, smem));
+        grid_cap = std::max(1, per_sm) * ctx.num_sms;
+    }
+    Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
+    RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    static unsigned long long* tprobe = nullptr;
+    static bool want_probe = getenv("RLRA_CHOL_PROBE") != nullptr;
+    if (want_probe && !tprobe) RLRA_CUDA(cudaMallocManaged(&tprobe, 64 * 8));
+    CholCoopArgs a{ctx.gbar, G.p, G.ld, n, Rinv.p, Rinv.ld, dorig.d(), floor, flag.i(), tprobe};
+    void* args[] = {&a};
+    static const int grid_env = getenv("RLRA_CHOL_GRID") ? atoi(getenv("RLRA_CHOL_GRID")) : 0;
+    const int grid = grid_env > 0 ? std::min(grid_env, grid_cap) : std::min(grid_cap, ctx.num_sms);
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)chol_inv_coop_kernel, dim3(grid), dim3(256), args, smem,
+                                          ctx.stream));
+    ++ctx.launches;
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (tprobe) fprintf(stderr, "phase A cycles: factor %llu\n", tprobe[50]);
+    if (tprobe) {
+        for (int i = 1; i <= 3 * ((n + kCholNB - 1) / kCholNB); ++i)
+            fprintf(stderr, "%s%.1f", i == 1 ? "chol probe us:" : " ", (tprobe[i] - tprobe[i - 1]) * 1e-3);
+        fprintf(stderr, "\n");
+    }
+    return ctx.h_flags[0] == 0;
+}
+
+}  // namespace
+
 bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
     ProfScope prof(ctx, "chol", int(G.rows), int(G.rows), 0, 0.0);
     GemmTag tag(ctx, "gemm_chol");
     const int n = int(G.rows);
+    if (n <= kCholCoopMax && !ctx.chol_blocked_gemm) return chol_upper_inv_coop(ctx, G, Rinv, floor);
     Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
     RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
     diag_copy_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(G.p, G.ld, n, dorig.d());
@@ -364,6 +646,7 @@ QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R) {
     a.part = part.d();
     a.dots = dots.d();
     a.degenerate = deg.i();
+    a.bar = ctx.gbar;
     void* args[] = {&a};
     RLRA_CUDA(cudaLaunchCooperativeKernel((void*)householder_coop_kernel, dim3(G), dim3(256), args, 0,
                                           ctx.stream));

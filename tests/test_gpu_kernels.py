@@ -213,3 +213,31 @@ def test_philox_omega_is_gaussian_and_deterministic(eng):
     h = eng.gaussian_philox(1000, 64, seed=12345, row0=1000)
     assert np.array_equal(h, g[1000:2000])
     assert not np.array_equal(eng.gaussian_philox(100, 8, seed=1), eng.gaussian_philox(100, 8, seed=2))
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 65, 200, 510, 1024, 1100])
+def test_chol_inv_one_launch_and_blocked(eng, n):
+    """CholQR's Cholesky + triangular inverse: the one-launch cooperative
+    kernel (n <= 1024) and the launch-per-block GEMM path (n > 1024) against
+    numpy's Cholesky of a well-conditioned Gram."""
+    rs = np.random.default_rng(n)
+    y = rs.standard_normal((3 * n + 10, n))
+    g = y.T @ y
+    g_in = np.triu(g) + np.tril(rs.standard_normal((n, n)), -1)  # lower triangle is never read
+    r, ri, ok = eng.chol_inv(g_in, 1e-12)
+    assert ok
+    assert np.array_equal(np.tril(r, -1), np.zeros((n, n)))
+    assert np.array_equal(np.tril(ri, -1), np.zeros((n, n)))
+    want = np.linalg.cholesky(g).T
+    assert np.linalg.norm(r - want) <= 1e-12 * np.linalg.norm(want)
+    assert np.linalg.norm(ri @ r - np.eye(n)) <= 1e-12 * np.sqrt(n)
+
+
+def test_chol_inv_flags_rank_deficiency(eng):
+    rs = np.random.default_rng(3)
+    y = rs.standard_normal((300, 100))
+    y[:, 70] = y[:, 3] + y[:, 9]  # exactly dependent column: pivot 70 collapses
+    _, _, ok = eng.chol_inv(y.T @ y, 1e-12)
+    assert not ok
+    _, _, ok = eng.chol_inv(-np.eye(4), 0.0)  # non-positive pivot
+    assert not ok
