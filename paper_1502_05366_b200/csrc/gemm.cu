@@ -2,7 +2,10 @@
 #include <cstdlib>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
 #include "reduce.cuh"
 
 namespace rlra_b200 {
@@ -109,6 +112,83 @@ void launch_ops(Context& ctx, Op opa, Op opb, bool vec, const GemmParams& p, int
     RLRA_DISPATCH(true, true)
     RLRA_DISPATCH(false, true)
 #undef RLRA_DISPATCH
+}
+
+// ------------------------------------------------------------- TMA path ---
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+bool tma_choice() {
+    static bool on = [] {
+        const char* e = std::getenv("RLRA_GEMM_TMA");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+// 2-D FP64 tensor map over a column-major matrix: dim0 contiguous (d0
+// elements), dim1 strided by ld; 128-byte swizzled boxes of b0 x b1.
+void encode_map(CUtensorMap* m, const double* base, int64_t d0, int64_t d1, int64_t ld, int b0, int b1) {
+    auto enc = tensor_map_encoder();
+    if (!enc) raise(RLRA_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const cuuint64_t dims[2] = {cuuint64_t(d0), cuuint64_t(d1)};
+    const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+    const cuuint32_t box[2] = {cuuint32_t(b0), cuuint32_t(b1)};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(RLRA_ECUDA, fmt("cuTensorMapEncodeTiled failed (%d)", int(r)));
+}
+
+// x-contiguous A (M x K, M % 16 == 0) as the 3-D tensor (16, K, M/16): a
+// (16, BK, 8) box is a 128 x BK slice in the eight-box swizzled layout.
+void encode_map3_km(CUtensorMap* m, const double* base, int64_t M, int64_t K, int64_t ld) {
+    auto enc = tensor_map_encoder();
+    if (!enc) raise(RLRA_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const cuuint64_t dims[3] = {16, cuuint64_t(K), cuuint64_t(M / 16)};
+    const cuuint64_t strides[2] = {cuuint64_t(ld) * 8, 128};
+    const cuuint32_t box[3] = {16, cuuint32_t(kTBK), cuuint32_t(kTBM / 16)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(RLRA_ECUDA, fmt("cuTensorMapEncodeTiled (3-D) failed (%d)", int(r)));
+}
+
+template <bool A_KM, int EPI, bool PHILOX>
+void launch_tma_cfg(Context& ctx, const GemmParams& p, const TmaPair& maps) {
+    auto kern = dgemm_tma_kernel<A_KM, EPI, PHILOX>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem)));
+        attr_set = true;
+    }
+    const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
+    kern<<<dim3(unsigned(grid)), 384, kTmaSmem, ctx.stream>>>(p, maps);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+}
+
+template <bool A_KM>
+void launch_tma_epi(Context& ctx, const GemmParams& p, const TmaPair& maps, int epi, bool philox) {
+    if (philox) {
+        if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, true>(ctx, p, maps);
+        if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, true>(ctx, p, maps);
+        raise(RLRA_EINVAL, "gemm: Philox B operand needs a store/split epilogue");
+    }
+    if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, false>(ctx, p, maps);
+    if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, false>(ctx, p, maps);
+    return launch_tma_cfg<A_KM, EPI_RESID, false>(ctx, p, maps);
 }
 
 __global__ void split_reduce_kernel(const double* ws, int splits, int M, int N, double alpha,
@@ -251,12 +331,34 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
         p.partials = parts.d();
     }
     ProfScope prof(ctx, ctx.gemm_tag, M, N, K, 2.0 * M * double(N) * K);
-    if (big && big_cfg_choice() == 16)
+    // TMA path: big tiles, B k-contiguous (op(B) = N) or generated, 16-byte
+    // aligned operands with 16-byte-multiple leading dimensions
+    const bool tma = big && vec && (opb == Op::N || o.philox_b) && tma_choice() && tensor_map_encoder();
+    if (tma) {
+        TmaPair maps;
+        maps.a3d = 0;
+        if (opa == Op::N && M % 16 == 0) {
+            encode_map3_km(&maps.a, A, M, K, lda);            // A (M x K): one (16, BK, 8) box per stage
+            maps.a3d = 1;
+        } else if (opa == Op::N)
+            encode_map(&maps.a, A, M, K, lda, 16, kTBK);      // A (M x K), eight 16-row boxes per stage
+        else
+            encode_map(&maps.a, A, K, M, lda, kTBK, kTBM);    // A^T: A is K x M, k-contiguous
+        if (o.philox_b)
+            maps.b = maps.a;
+        else
+            encode_map(&maps.b, B, K, N, ldb, kTBK, kTBN);    // B (K x N), k-contiguous
+        if (opa == Op::N)
+            launch_tma_epi<true>(ctx, p, maps, epi, o.philox_b);
+        else
+            launch_tma_epi<false>(ctx, p, maps, epi, o.philox_b);
+    } else if (big && big_cfg_choice() == 16) {
         launch_ops<CfgBig16>(ctx, opa, opb, vec, p, epi, o.philox_b);
-    else if (big)
+    } else if (big) {
         launch_ops<CfgBig>(ctx, opa, opb, vec, p, epi, o.philox_b);
-    else
+    } else {
         launch_ops<CfgSmall>(ctx, opa, opb, vec, p, epi, o.philox_b);
+    }
 
     if (epi == EPI_SPLIT) {
         const int64_t total = int64_t(M) * N;

@@ -64,6 +64,18 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
+// Exact float -> double widening with integer ops only (sign, exponent
+// re-bias, mantissa shift): bit-identical to double(f) for normal floats and
+// zero, and keeps the conversion off the FP64 pipe the DMMA sketch saturates.
+// (Box-Muller outputs are never subnormal, infinite or NaN.)
+__device__ __forceinline__ double f32_to_f64_bits(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t e = (u >> 23) & 0xffu;
+    const uint32_t hi = e ? ((u & 0x80000000u) | ((e + 896u) << 20) | ((u & 0x7fffffu) >> 3)) : (u & 0x80000000u);
+    const uint32_t lo = e ? (u << 29) : 0u;
+    return __hiloint2double(int(hi), int(lo));
+}
+
 // Four N(0,1) deviates for rows 4*(k>>2)+{0..3} of column n in draw `draw`.
 // Box-Muller in fp32 on the FP32/SFU pipes (the FP64 pipe is the bottleneck);
 // the deviates only need to be Gaussian, the product with them is exact FP64.
@@ -82,10 +94,10 @@ __device__ __forceinline__ void philox_normal4(uint64_t seed, int draw, int64_t 
     float sa, ca, sb, cb;
     __sincosf(6.283185307179586f * u2a, &sa, &ca);
     __sincosf(6.283185307179586f * u2b, &sb, &cb);
-    out[0] = double(ra * ca);
-    out[1] = double(ra * sa);
-    out[2] = double(rb * cb);
-    out[3] = double(rb * sb);
+    out[0] = f32_to_f64_bits(ra * ca);
+    out[1] = f32_to_f64_bits(ra * sa);
+    out[2] = f32_to_f64_bits(rb * cb);
+    out[3] = f32_to_f64_bits(rb * sb);
 }
 
 // ------------------------------------------------------------- cp.async ---

@@ -1,0 +1,264 @@
+// gemm_tma.cuh — TMA-staged, warp-specialized FP64 DMMA GEMM (the big-tile
+// path of gemm.cu: every product of the rsvd/QB/ID path whose operands are
+// 16-byte aligned and whose B is k-contiguous, i.e. all products that stream
+// A).
+//
+// One CTA computes a 128 x 128 tile of C = op(A) op(B):
+//   * producer warpgroup: one elected thread issues cp.async.bulk.tensor (TMA)
+//     loads of the A and B k-slices into a 6-stage shared-memory ring,
+//     completing on the stage's "full" mbarrier (expect_tx bytes); for the
+//     sketch the other producer threads generate the Philox Omega slice in
+//     registers and store it into the same swizzled layout;
+//   * 2 consumer warpgroups (8 warps of 64 x 32) read m8n8k4 fragments from
+//     shared memory and issue DMMA.8x8x4; each warp releases the stage on its
+//     "empty" mbarrier.
+// Shared-memory tiles use the 128-byte TMA swizzle (16-byte chunk index XOR
+// row index mod 8).  The fragment-row <-> matrix-row assignment is permuted so
+// that every half-warp's 16 fragment loads hit 16 distinct bank pairs (the
+// epilogue applies the same permutation when it writes C):
+//   k-contiguous operand ("XM", rows of 16 k-values = 128 B): fragment rows
+//     {0,2,4,6 | 1,3,5,7}, i.e. row(lr) = 2 (lr & 3) + (lr >> 2);
+//   x-contiguous operand ("KM", A of Y = A Z: 8 boxes of 16 x-values x BK):
+//     fragment f of a 16-row box takes rows
+//     (lr & 1) + 8 ((lr >> 1) & 1) + 4 (lr >> 2) + 2 f.
+#pragma once
+
+#include <cuda.h>
+
+#include "gemm.cuh"
+
+namespace rlra_b200 {
+
+struct TmaPair {
+    CUtensorMap a;  // op(A) slices
+    CUtensorMap b;  // B slices (unused for the Philox sketch)
+    int a3d;        // A (x-contiguous) as a 3-D (16, K, M/16) map: one box per stage
+};
+
+constexpr int kTBM = 128, kTBN = 128, kTBK = 16, kTWM = 64, kTWN = 32, kTStages = 6;
+constexpr int kTABytes = kTBM * kTBK * 8;  // 16 KB per stage
+constexpr int kTBBytes = kTBN * kTBK * 8;  // 16 KB per stage
+constexpr size_t kTmaSmem = size_t(kTStages) * (kTABytes + kTBBytes) + 1024;  // + 1 KB alignment slack
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+    return v;
+}
+
+// byte offset of element (k, x) in a swizzled stage tile
+__device__ __forceinline__ uint32_t tma_km_off(int k, int x) {  // 8 boxes [BK][16 x]
+    return uint32_t((x >> 4) * (kTBK * 128) + k * 128 + ((((x & 15) >> 1) ^ (k & 7)) << 4) + ((x & 1) << 3));
+}
+__device__ __forceinline__ uint32_t tma_xm_off(int k, int x) {  // [X][16 k] rows of 128 B
+    return uint32_t(x * 128 + ((((k >> 1) ^ (x & 7))) << 4) + ((k & 1) << 3));
+}
+// fragment-row permutations (see header)
+__device__ __forceinline__ int tma_xm_row(int lr) { return 2 * (lr & 3) + (lr >> 2); }
+__device__ __forceinline__ int tma_km_row(int lr, int f) {
+    return (lr & 1) + 8 * ((lr >> 1) & 1) + 4 * (lr >> 2) + 2 * f;
+}
+
+template <bool A_KM, int EPI, bool PHILOX>
+__global__ void __launch_bounds__(384, 1)
+    dgemm_tma_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ TmaPair maps) {
+    constexpr int NWM = kTBM / kTWM;  // 2
+    constexpr int NCW = 8;            // consumer warps
+    constexpr int MF = kTWM / 8, NF = kTWN / 8;
+    extern __shared__ uint8_t tma_smem_raw[];
+    // 1024-byte aligned ring (the 128-byte swizzle pattern repeats every 1 KB);
+    // offsetting the __shared__ array keeps the shared address space, so the
+    // fragment loads below compile to LDS, not generic loads
+    uint8_t* smem = tma_smem_raw + ((1024u - (smem_u32(tma_smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kTStages * kTABytes;
+    __shared__ __align__(8) uint64_t full_bar[kTStages], empty_bar[kTStages];
+    __shared__ double red[NCW];
+
+    const int tile = blockIdx.x;
+    const int nt_i = tile % p.nt;
+    const int rest = tile / p.nt;
+    const int mt_i = rest % p.mt;
+    const int split = rest / p.mt;
+    if (p.upper_tiles_only && mt_i > nt_i) return;
+    const int m0 = mt_i * kTBM, n0 = nt_i * kTBN;
+    const int k_begin = split * p.k_chunk;
+    int k_end = min(p.K, k_begin + p.k_chunk);
+    if (p.tri_b_upper) k_end = min(k_end, n0 + kTBN);
+    const int nk = k_end > k_begin ? (k_end - k_begin + kTBK - 1) / kTBK : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTStages; ++s) {
+            mbar_init(&full_bar[s], PHILOX ? 5u : 1u);  // TMA expect_tx (+ 4 Omega warps)
+            mbar_init(&empty_bar[s], unsigned(NCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.a)) : "memory");
+        if (!PHILOX) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.b)) : "memory");
+    }
+    __syncthreads();
+
+    if (threadIdx.x < 128) {
+        // ------------------------------------------------------ producer ---
+        if (PHILOX)
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n");
+        else
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+        if (!PHILOX && threadIdx.x != 0) return;
+        for (int kt = 0; kt < nk; ++kt) {
+            const int st = kt % kTStages;
+            if (kt >= kTStages) mbar_wait(&empty_bar[st], ((kt / kTStages) - 1) & 1);
+            const int k0 = k_begin + kt * kTBK;
+            uint8_t* a_st = sA + st * kTABytes;
+            uint8_t* b_st = sB + st * kTBBytes;
+            if (threadIdx.x == 0) {
+                mbar_arrive_expect_tx(&full_bar[st], PHILOX ? unsigned(kTABytes) : unsigned(kTABytes + kTBBytes));
+                if (A_KM) {
+                    if (maps.a3d) {
+                        // box (16, BK, 8) of the (16, K, M/16) view lands as
+                        // [8][BK][16], the layout of the eight 2-D boxes
+                        tma_load_3d(a_st, &maps.a, &full_bar[st], 0, k0, m0 / 16);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < kTBM / 16; ++b)
+                            tma_load_2d(a_st + b * (kTBK * 128), &maps.a, &full_bar[st], m0 + 16 * b, k0);
+                    }
+                } else {
+                    tma_load_2d(a_st, &maps.a, &full_bar[st], k0, m0);
+                }
+                if (!PHILOX) tma_load_2d(b_st, &maps.b, &full_bar[st], k0, n0);
+            }
+            if (PHILOX) {
+                // Omega(k, n) for this stage: 4 consecutive k of one column per call
+#pragma unroll
+                for (int it = 0; it < (kTBN * kTBK / 4) / 128; ++it) {
+                    const int g = it * 128 + threadIdx.x;
+                    const int nl = g / (kTBK / 4), kl = (g % (kTBK / 4)) * 4;
+                    const int n = n0 + nl, k = k0 + kl;
+                    double v[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (n < p.N && k < k_end) {
+                        philox_normal4(p.seed, p.draw, p.krow0 + k, n, v);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (k + t >= k_end) v[t] = 0.0;
+                    }
+                    uint8_t* row = b_st + nl * 128;
+                    *reinterpret_cast<double2*>(row + ((((kl >> 1)) ^ (nl & 7)) << 4)) = make_double2(v[0], v[1]);
+                    *reinterpret_cast<double2*>(row + ((((kl >> 1) + 1) ^ (nl & 7)) << 4)) = make_double2(v[2], v[3]);
+                }
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0) mbar_arrive(&full_bar[st]);
+            }
+        }
+        return;
+    }
+    // -------------------------------------------------------- consumers ---
+    if (PHILOX)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n");
+    else
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+    const int warp = (threadIdx.x >> 5) - 4, lane = threadIdx.x & 31;
+    const int wm = warp % NWM, wn = warp / NWM;
+    const int lr = lane >> 2, lc = lane & 3;
+    int arow[MF], bcol[NF];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+        arow[i] = A_KM ? wm * kTWM + (i >> 1) * 16 + tma_km_row(lr, i & 1) : wm * kTWM + i * 8 + tma_xm_row(lr);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) bcol[j] = wn * kTWN + j * 8 + tma_xm_row(lr);
+
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % kTStages;
+        mbar_wait(&full_bar[st], (kt / kTStages) & 1);
+        const uint32_t a_s = smem_u32(sA + st * kTABytes);
+        const uint32_t b_s = smem_u32(sB + st * kTBBytes);
+#pragma unroll
+        for (int kk = 0; kk < kTBK; kk += 4) {
+            const int k = kk + lc;
+            double af[MF], bf[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+                af[i] = lds_f64(a_s + (A_KM ? tma_km_off(k, arow[i]) : tma_xm_off(k, arow[i])));
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bf[j] = lds_f64(b_s + tma_xm_off(k, bcol[j]));
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+                for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+    }
+
+    // ---------------------------------------------------------- epilogue ---
+    // C element of acc[i][j][h]: row = arow[i] (this lane's lr), column = the
+    // B-fragment row that lane (lr' = 2 lc + h) holds
+    double local = 0.0;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const int row = m0 + arow[i];
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
+                if (row < p.M && col < p.N) {
+                    const double v = acc[i][j][h];
+                    if (EPI == EPI_STORE) {
+                        double* c = p.C + row + int64_t(col) * p.ldc;
+                        *c = p.beta == 0.0 ? p.alpha * v : p.alpha * v + p.beta * *c;
+                    } else if (EPI == EPI_SPLIT) {
+                        p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
+                    } else {
+                        const double d = p.R[row + int64_t(col) * p.ldr] - p.alpha * v;
+                        if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
+                        local += d * d;
+                    }
+                }
+            }
+        }
+    }
+    if (EPI == EPI_RESID) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if (lane == 0) red[warp] = local;
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32));
+        if (warp == 0 && lane == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) t += red[w];
+            p.partials[tile] = t;
+        }
+    }
+}
+
+}  // namespace rlra_b200

@@ -215,6 +215,31 @@ def test_philox_omega_is_gaussian_and_deterministic(eng):
     assert not np.array_equal(eng.gaussian_philox(100, 8, seed=1), eng.gaussian_philox(100, 8, seed=2))
 
 
+@pytest.mark.parametrize("ta", [0, 1])
+@pytest.mark.parametrize("m,n,k", [(2048, 200, 700), (2008, 130, 333), (4096, 510, 1500)])
+def test_matmul_tma_paths_vs_oracle(eng, orc, ta, m, n, k):
+    """The TMA-staged GEMM (gemm_tma.cuh): x-contiguous A as one 3-D box per
+    stage (M % 16 == 0) or eight 2-D boxes (M % 16 != 0), k-contiguous A^T,
+    split-K for the tall TN shapes; swizzled tiles and permuted fragment rows
+    must land every C element where the oracle puts it."""
+    rs = np.random.default_rng(m + n + k + ta)
+    a = rs.standard_normal((k, m) if ta else (m, k))
+    b = rs.standard_normal((k, n))
+    got = eng.matmul(a, b, bool(ta), False)
+    assert rel_fro(got, orc.matmul(a, b, ta, 0)) <= 1e-13
+
+
+def test_sketch_philox_in_register_equals_materialized(eng):
+    """The sketch GEMM's in-register Philox Omega is bit-identical to the
+    materialised Omega (rlra_gaussian_philox) multiplied by the same kernel."""
+    rs = np.random.default_rng(11)
+    m, n, l = 2048, 1000, 130
+    a = rs.standard_normal((m, n))
+    y = eng.sample_right(a, l, 0, 1, omega=R.Omega.philox(777))
+    om = eng.gaussian_philox(n, l, seed=777)
+    assert np.array_equal(y, eng.matmul(a, om))
+
+
 @pytest.mark.parametrize("n", [1, 5, 64, 65, 200, 510, 1024, 1100])
 def test_chol_inv_one_launch_and_blocked(eng, n):
     """CholQR's Cholesky + triangular inverse: the one-launch cooperative
