@@ -12,7 +12,9 @@ metric  : effective FP64 TFLOP/s = F_gemm / step time with
           F_gemm = 4 m n l (q+1) (SURVEY.md §8d; 2.448e13 flop for C5);
 value   : A resident in HBM, Omega generated in-register (Philox);
 e2e     : the same call through the C-ABI with HOST buffers (pinned A in,
-          U/sigma/V out), host<->device copies inside the timed region;
+          U/sigma/V out), host<->device copies inside the timed region; the
+          engine streams the 32 GB upload in row chunks on a copy stream
+          under the sketch GEMM (engine.cu upload_and_sketch);
 roofline: the dominant kernel is the FP64 DMMA GEMM; achieved = its
           algorithmic flops / its CUDA-event time on the engine stream over
           the timed region, against the measured DMMA peak
@@ -391,7 +393,7 @@ def main():
             def estep(seed):  # the drop-in call with host buffers
                 eng.host_rsvd_ptr(R.RSVD_V2, Ah.data_ptr(), m, n, m, k, p, q, s,
                                   R.Omega.philox(seed), Uh.data_ptr(), Sh.data_ptr(), Vh.data_ptr())
-            path = "rlra_rsvd(loc=RLRA_HOST), pinned host A"
+            path = "rlra_rsvd(loc=RLRA_HOST), pinned host A, row-chunked upload overlapped with the sketch"
         else:
             def estep(seed):  # each rank uploads its shard, factors, downloads its U rows
                 Ad.t.copy_(Ah)

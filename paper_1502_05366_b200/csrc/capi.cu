@@ -222,6 +222,7 @@ rlra_status rlra_ctx_destroy(rlra_ctx* ctx) {
         cudaStreamSynchronize(ctx->c.stream);
         cudaStreamDestroy(ctx->c.stream);
     }
+    if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
     if (ctx->c.h_scalars) cudaFreeHost(ctx->c.h_scalars);
     if (ctx->c.h_flags) cudaFreeHost(ctx->c.h_flags);
     if (ctx->c.gbar) cudaFree(ctx->c.gbar);
@@ -530,10 +531,19 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
         check_sample_rank(k, p, m, n);
         if (variant != RLRA_RSVD_BASIC) check_sample(k + p, q, s, m, n);
         OmegaSource om = omega_of(omega);
-        In A(C, loc, a, m, n, lda, "a");
         Out U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
         OutVec<double> S(C, loc, sigma, k, "sigma");
-        rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
+        if (loc == RLRA_HOST && m > 0 && n > 0) {
+            // host A: the upload streams in row chunks under the sketch GEMM
+            need(a, "a");
+            check_ld(lda, m, "a");
+            DMatBuf dA(C, m, n), Y(C, m, k + p);
+            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m);
+            rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m);
+        } else {
+            In A(C, loc, a, m, n, lda, "a");
+            rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
+        }
         U.finish(C);
         V.finish(C);
         S.finish(C);

@@ -67,6 +67,7 @@ struct Context {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host->device uploads overlapped with compute (lazy)
     cudaMemPool_t pool = nullptr;
     // pinned scalars for device->host flags without extra allocations
     double* h_scalars = nullptr;  // pinned, 64 doubles

@@ -158,9 +158,9 @@ static void orth_mid(Context& ctx, const DMat& Y, bool span_only) {
 }
 
 void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
-                  bool span_only) {
+                  bool span_only, bool sketched) {
     const int n = int(A.cols);
-    sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
+    if (!sketched) sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
     if (q == 0) return;
     DMatBuf Z(ctx, n, l);
     GemmTag tag(ctx, "gemm_power");
@@ -187,13 +187,72 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
     }
 }
 
+void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
+                       const DMat& Y) {
+    const int64_t m = dA.rows, n = dA.cols;
+    if (m <= 0 || n <= 0) return;
+    if (!ctx.copy_stream) RLRA_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+    // Omega once (callback mode: the reference's draw, uploaded; Philox: in-register)
+    const int draw = om.next_draw++;
+    DMatBuf Om;
+    std::vector<double> h;
+    if (om.o->mode != RLRA_OMEGA_PHILOX) {
+        if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
+        h.resize(size_t(n) * l);
+        om.o->fill(om.o->user, draw, int(n), l, h.data());
+        Om = DMatBuf(ctx, n, l);
+        RLRA_CUDA(cudaMemcpyAsync(Om.m.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
+                                  ctx.stream));
+    }
+    // row chunks of whole 128-row GEMM tiles, ~16 of them for a large A
+    const int64_t bytes = m * n * 8;
+    const int64_t nchunk = bytes >= (int64_t(256) << 20) ? 16 : 1;
+    const int64_t rows = std::max<int64_t>(128, ((m + nchunk - 1) / nchunk + 127) / 128 * 128);
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t ready;
+    RLRA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    RLRA_CUDA(cudaEventRecord(ready, ctx.stream));  // dA / Y / Omega allocations are stream-ordered
+    RLRA_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ready, 0));
+    GemmTag tag(ctx, "gemm_sketch");
+    for (int64_t r0 = 0; r0 < m; r0 += rows) {
+        const int64_t nr = std::min(rows, m - r0);
+        RLRA_CUDA(cudaMemcpy2DAsync(dA.p + r0, sizeof(double) * dA.ld, hA + r0, sizeof(double) * lda,
+                                    sizeof(double) * nr, n, cudaMemcpyHostToDevice, ctx.copy_stream));
+        cudaEvent_t e;
+        RLRA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        RLRA_CUDA(cudaEventRecord(e, ctx.copy_stream));
+        ev.push_back(e);
+        RLRA_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
+        const DMat Ar = dA.block(r0, 0, nr, n), Yr = Y.block(r0, 0, nr, l);
+        if (om.o->mode == RLRA_OMEGA_PHILOX) {
+            GemmOpts o;
+            o.philox_b = true;
+            o.seed = om.o->seed;
+            o.draw = draw;
+            gemm(ctx, Op::N, Op::N, int(nr), l, int(n), 1.0, Ar.p, Ar.ld, nullptr, n, 0.0, Yr.p, Yr.ld, o);
+        } else {
+            gemm(ctx, Op::N, Op::N, 1.0, Ar, Om.m, 0.0, Yr);
+        }
+    }
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));  // h (callback Omega) outlives its copy; events done
+    for (auto e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(ready);
+}
+
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
-          const DMat& U, double* sigma, const DMat& V) {
+          const DMat& U, double* sigma, const DMat& V, const DMat* sketched) {
     const int m = int(A.rows), n = int(A.cols), l = k + p;
-    DMatBuf Y(ctx, m, l);
+    DMatBuf Yown;
+    DMat Y;
+    if (sketched) {
+        Y = *sketched;
+    } else {
+        Yown = DMatBuf(ctx, m, l);
+        Y = Yown.m;
+    }
     if (variant == RLRA_RSVD_BASIC) {
         // rsvd.hpp:127-140 (Fig. 1): Y = A G, Q = orth(Y), B = Q^T A, small_svd(B)
-        sketch(ctx, Op::N, A, l, om, Y);
+        if (!sketched) sketch(ctx, Op::N, A, l, om, Y);
         orth(ctx, Y);
         DMatBuf B(ctx, l, n);
         gemm(ctx, Op::T, Op::N, 1.0, Y, A, 0.0, B);
@@ -206,7 +265,7 @@ void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, 
         RLRA_CUDA(cudaMemcpyAsync(sigma, sb.p, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx.stream));
         return;
     }
-    sample_right(ctx, A, l, q, s, om, Y, /*span_only=*/true);
+    sample_right(ctx, A, l, q, s, om, Y, /*span_only=*/true, /*sketched=*/sketched != nullptr);
     orth(ctx, Y);
     GemmTag tag(ctx, "gemm_proj");
     if (variant == RLRA_RSVD_V2) {

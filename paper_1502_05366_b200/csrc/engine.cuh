@@ -20,7 +20,14 @@ struct OmegaSource {
 // span_only: intermediate re-orthonormalisations keep the span but not an
 // orthonormal basis (callers that never expose the sample).
 void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
-                  bool span_only = false);
+                  bool span_only = false, bool sketched = false);
+
+// Host-resident A: upload it into the device buffer dA in row chunks on the
+// context's copy stream and compute the sketch Y = A Omega chunk by chunk as
+// the rows land (the chunk GEMMs are the unchunked GEMM's tiles, so Y is
+// bit-identical); consumes one Omega draw.
+void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
+                       const DMat& Y);
 // sketch.hpp:65-67 — returns Y^T (n x l) of the reference's l x n sample,
 // computed on A directly (the reference materialises A^T; we never do).
 void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt,
@@ -28,7 +35,7 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
 
 // rsvd.hpp:127-160; U m x k, sigma (device) k, V n x k
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
-          const DMat& U, double* sigma, const DMat& V);
+          const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr);
 
 struct QbOut {
     int ell = 0;
