@@ -165,30 +165,64 @@ void encode_map3_km(CUtensorMap* m, const double* base, int64_t M, int64_t K, in
     if (r != CUDA_SUCCESS) raise(RLRA_ECUDA, fmt("cuTensorMapEncodeTiled (3-D) failed (%d)", int(r)));
 }
 
-template <bool A_KM, int EPI, bool PHILOX>
+template <bool A_KM, int EPI, bool PHILOX, int CL>
 void launch_tma_cfg(Context& ctx, const GemmParams& p, const TmaPair& maps) {
-    auto kern = dgemm_tma_kernel<A_KM, EPI, PHILOX>;
+    auto kern = dgemm_tma_kernel<A_KM, EPI, PHILOX, CL>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem)));
         attr_set = true;
     }
-    const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
-    kern<<<dim3(unsigned(grid)), 384, kTmaSmem, ctx.stream>>>(p, maps);
+    if (CL == 1) {
+        const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
+        kern<<<dim3(unsigned(grid)), 384, kTmaSmem, ctx.stream>>>(p, maps);
+    } else {
+        const int64_t grid = int64_t(ceil_div(p.mt, CL)) * CL * p.nt * p.splits;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(384);
+        cfg.dynamicSmemBytes = kTmaSmem;
+        cfg.stream = ctx.stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RLRA_CUDA(cudaLaunchKernelEx(&cfg, kern, p, maps));
+    }
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
+}
+
+int omega_cluster_choice() {
+    static int cl = [] {
+        const char* e = std::getenv("RLRA_OMEGA_CLUSTER");
+        // pairs: 4-CTA clusters strand SMs of the 18-19-SM GPCs at 1 CTA/SM
+        return e ? std::atoi(e) : 2;
+    }();
+    return cl;
 }
 
 template <bool A_KM>
 void launch_tma_epi(Context& ctx, const GemmParams& p, const TmaPair& maps, int epi, bool philox) {
     if (philox) {
-        if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, true>(ctx, p, maps);
-        if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, true>(ctx, p, maps);
+        // >= 4 m-tiles: cluster pairs of m-tiles share each generated Omega slice
+        const int cl = p.mt >= 4 ? omega_cluster_choice() : 1;
+        if (epi == EPI_STORE)
+            return cl == 4 ? launch_tma_cfg<A_KM, EPI_STORE, true, 4>(ctx, p, maps)
+                 : cl == 2 ? launch_tma_cfg<A_KM, EPI_STORE, true, 2>(ctx, p, maps)
+                           : launch_tma_cfg<A_KM, EPI_STORE, true, 1>(ctx, p, maps);
+        if (epi == EPI_SPLIT)
+            return cl == 4 ? launch_tma_cfg<A_KM, EPI_SPLIT, true, 4>(ctx, p, maps)
+                 : cl == 2 ? launch_tma_cfg<A_KM, EPI_SPLIT, true, 2>(ctx, p, maps)
+                           : launch_tma_cfg<A_KM, EPI_SPLIT, true, 1>(ctx, p, maps);
         raise(RLRA_EINVAL, "gemm: Philox B operand needs a store/split epilogue");
     }
-    if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, false>(ctx, p, maps);
-    if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, false>(ctx, p, maps);
-    return launch_tma_cfg<A_KM, EPI_RESID, false>(ctx, p, maps);
+    if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, false, 1>(ctx, p, maps);
+    if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, false, 1>(ctx, p, maps);
+    return launch_tma_cfg<A_KM, EPI_RESID, false, 1>(ctx, p, maps);
 }
 
 __global__ void split_reduce_kernel(const double* ws, int splits, int M, int N, double alpha,

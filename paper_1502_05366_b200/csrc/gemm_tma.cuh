@@ -8,7 +8,11 @@
 //     loads of the A and B k-slices into a 6-stage shared-memory ring,
 //     completing on the stage's "full" mbarrier (expect_tx bytes); for the
 //     sketch the other producer threads generate the Philox Omega slice in
-//     registers and store it into the same swizzled layout;
+//     registers and store it into the same swizzled layout.  The sketch runs
+//     as clusters of CL CTAs (CL m-tiles of one n-tile; CL = 2 by default):
+//     each CTA generates 1/CL of the shared Omega slice and stores it into
+//     every ring of the cluster with st.async (DSMEM), completing
+//     transaction bytes on the peers' full mbarriers;
 //   * 2 consumer warpgroups (8 warps of 64 x 32) read m8n8k4 fragments from
 //     shared memory and issue DMMA.8x8x4; each warp releases the stage on its
 //     "empty" mbarrier.
@@ -63,6 +67,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// ---- cluster (DSMEM) helpers for the Omega-sharing sketch ----
+__device__ __forceinline__ uint32_t cluster_map(uint32_t local_addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_addr), "r"(rank));
+    return r;
+}
+// asynchronous store into a cluster peer's shared memory that completes 16
+// bytes of the peer's mbarrier transaction count (no fence needed: the data
+// is visible once the barrier phase completes, as with TMA)
+__device__ __forceinline__ void st_async_f64x2(uint32_t addr, double a, double b, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+                 "d"(a), "d"(b), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
@@ -82,9 +107,10 @@ __device__ __forceinline__ int tma_km_row(int lr, int f) {
     return (lr & 1) + 8 * ((lr >> 1) & 1) + 4 * (lr >> 2) + 2 * f;
 }
 
-template <bool A_KM, int EPI, bool PHILOX>
+template <bool A_KM, int EPI, bool PHILOX, int CL>
 __global__ void __launch_bounds__(384, 1)
     dgemm_tma_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ TmaPair maps) {
+    static_assert(CL == 1 || PHILOX, "clusters share the generated Omega slice only");
     constexpr int NWM = kTBM / kTWM;  // 2
     constexpr int NCW = 8;            // consumer warps
     constexpr int MF = kTWM / 8, NF = kTWN / 8;
@@ -99,11 +125,26 @@ __global__ void __launch_bounds__(384, 1)
     __shared__ double red[NCW];
 
     const int tile = blockIdx.x;
-    const int nt_i = tile % p.nt;
-    const int rest = tile / p.nt;
-    const int mt_i = rest % p.mt;
-    const int split = rest / p.mt;
-    if (p.upper_tiles_only && mt_i > nt_i) return;
+    int nt_i, mt_i, split, crank = 0;
+    if (CL == 1) {
+        nt_i = tile % p.nt;
+        const int rest = tile / p.nt;
+        mt_i = rest % p.mt;
+        split = rest / p.mt;
+        if (p.upper_tiles_only && mt_i > nt_i) return;
+    } else {
+        // clusters of CL consecutive m-tiles of one n-tile (the CTAs sharing
+        // an Omega slice); the nt clusters of an m-group are adjacent so the
+        // A rows they all read stay L2-resident.  m-tiles past mt are padding
+        // CTAs: they generate their share of Omega, load zeros, store nothing.
+        asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+        const int mg = (p.mt + CL - 1) / CL;
+        const int q = tile / CL;
+        nt_i = q % p.nt;
+        const int rest = q / p.nt;
+        mt_i = (rest % mg) * CL + (tile % CL);
+        split = rest / mg;
+    }
     const int m0 = mt_i * kTBM, n0 = nt_i * kTBN;
     const int k_begin = split * p.k_chunk;
     int k_end = min(p.K, k_begin + p.k_chunk);
@@ -112,14 +153,21 @@ __global__ void __launch_bounds__(384, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTStages; ++s) {
-            mbar_init(&full_bar[s], PHILOX ? 5u : 1u);  // TMA expect_tx (+ 4 Omega warps)
-            mbar_init(&empty_bar[s], unsigned(NCW));
+            // full: own expect_tx (+ the 4 Omega warps without a cluster; with
+            // one, the peers' Omega stores complete transaction bytes);
+            // empty: 8 consumer warps of every cluster CTA (a producer writes
+            // the Omega slice into all of them)
+            mbar_init(&full_bar[s], (PHILOX && CL == 1) ? 5u : 1u);
+            mbar_init(&empty_bar[s], unsigned(NCW * CL));
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.a)) : "memory");
         if (!PHILOX) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.b)) : "memory");
     }
-    __syncthreads();
+    if (CL > 1)
+        cluster_sync_all();  // every CTA's barriers exist before any remote arrive
+    else
+        __syncthreads();
 
     if (threadIdx.x < 128) {
         // ------------------------------------------------------ producer ---
@@ -128,14 +176,23 @@ __global__ void __launch_bounds__(384, 1)
         else
             asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
         if (!PHILOX && threadIdx.x != 0) return;
+        uint32_t rb[CL], rbar[CL];  // the cluster CTAs' Omega rings and full barriers
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+            rb[r] = CL > 1 ? cluster_map(smem_u32(sB), r) : 0u;
+            rbar[r] = CL > 1 ? cluster_map(smem_u32(&full_bar[0]), r) : 0u;
+        }
         for (int kt = 0; kt < nk; ++kt) {
             const int st = kt % kTStages;
-            if (kt >= kTStages) mbar_wait(&empty_bar[st], ((kt / kTStages) - 1) & 1);
+            if (kt >= kTStages) {
+                mbar_wait(&empty_bar[st], ((kt / kTStages) - 1) & 1);
+            }
             const int k0 = k_begin + kt * kTBK;
             uint8_t* a_st = sA + st * kTABytes;
             uint8_t* b_st = sB + st * kTBBytes;
             if (threadIdx.x == 0) {
-                mbar_arrive_expect_tx(&full_bar[st], PHILOX ? unsigned(kTABytes) : unsigned(kTABytes + kTBBytes));
+                mbar_arrive_expect_tx(&full_bar[st], (PHILOX && CL == 1) ? unsigned(kTABytes)
+                                                                          : unsigned(kTABytes + kTBBytes));
                 if (A_KM) {
                     if (maps.a3d) {
                         // box (16, BK, 8) of the (16, K, M/16) view lands as
@@ -152,10 +209,12 @@ __global__ void __launch_bounds__(384, 1)
                 if (!PHILOX) tma_load_2d(b_st, &maps.b, &full_bar[st], k0, n0);
             }
             if (PHILOX) {
-                // Omega(k, n) for this stage: 4 consecutive k of one column per call
+                // Omega(k, n) for this stage, 4 consecutive k of one column per
+                // call; with a cluster each CTA generates 1/CL of the slice and
+                // stores it into every cluster CTA's ring (DSMEM)
 #pragma unroll
-                for (int it = 0; it < (kTBN * kTBK / 4) / 128; ++it) {
-                    const int g = it * 128 + threadIdx.x;
+                for (int it = 0; it < (kTBN * kTBK / 4) / (128 * CL); ++it) {
+                    const int g = (it * CL + crank) * 128 + threadIdx.x;
                     const int nl = g / (kTBK / 4), kl = (g % (kTBK / 4)) * 4;
                     const int n = n0 + nl, k = k0 + kl;
                     double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -165,14 +224,28 @@ __global__ void __launch_bounds__(384, 1)
                         for (int t = 0; t < 4; ++t)
                             if (k + t >= k_end) v[t] = 0.0;
                     }
-                    uint8_t* row = b_st + nl * 128;
-                    *reinterpret_cast<double2*>(row + ((((kl >> 1)) ^ (nl & 7)) << 4)) = make_double2(v[0], v[1]);
-                    *reinterpret_cast<double2*>(row + ((((kl >> 1) + 1) ^ (nl & 7)) << 4)) = make_double2(v[2], v[3]);
+                    const uint32_t o0 = uint32_t(st * kTBBytes + nl * 128 + (((kl >> 1) ^ (nl & 7)) << 4));
+                    const uint32_t o1 = uint32_t(st * kTBBytes + nl * 128 + ((((kl >> 1) + 1) ^ (nl & 7)) << 4));
+                    if (CL == 1) {
+                        uint8_t* row = b_st + nl * 128;
+                        *reinterpret_cast<double2*>(row + ((((kl >> 1)) ^ (nl & 7)) << 4)) = make_double2(v[0], v[1]);
+                        *reinterpret_cast<double2*>(row + ((((kl >> 1) + 1) ^ (nl & 7)) << 4)) =
+                            make_double2(v[2], v[3]);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < CL; ++r) {
+                            st_async_f64x2(rb[r] + o0, v[0], v[1], rbar[r] + 8u * st);
+                            st_async_f64x2(rb[r] + o1, v[2], v[3], rbar[r] + 8u * st);
+                        }
+                    }
                 }
-                __syncwarp();
-                if ((threadIdx.x & 31) == 0) mbar_arrive(&full_bar[st]);
+                if (CL == 1) {
+                    __syncwarp();
+                    if ((threadIdx.x & 31) == 0) mbar_arrive(&full_bar[st]);
+                }
             }
         }
+        if (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
         return;
     }
     // -------------------------------------------------------- consumers ---
@@ -196,6 +269,9 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    uint32_t rempty[CL];
+#pragma unroll
+    for (int r = 0; r < CL; ++r) rempty[r] = CL > 1 ? cluster_map(smem_u32(&empty_bar[0]), r) : 0u;
     for (int kt = 0; kt < nk; ++kt) {
         const int st = kt % kTStages;
         mbar_wait(&full_bar[st], (kt / kTStages) & 1);
@@ -216,7 +292,14 @@ __global__ void __launch_bounds__(384, 1)
                 for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[st]);
+        if (lane == 0) {
+            if (CL == 1) {
+                mbar_arrive(&empty_bar[st]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < CL; ++r) mbar_arrive_cluster(rempty[r] + 8u * st);
+            }
+        }
     }
 
     // ---------------------------------------------------------- epilogue ---
@@ -259,6 +342,7 @@ __global__ void __launch_bounds__(384, 1)
             p.partials[tile] = t;
         }
     }
+    if (CL > 1) cluster_sync_all();
 }
 
 }  // namespace rlra_b200
