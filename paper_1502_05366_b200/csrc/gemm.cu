@@ -1,4 +1,5 @@
 // gemm.cu — launcher for the FP64 DMMA GEMM family (see gemm.cuh).
+#include <climits>
 #include <cstdlib>
 #include <string>
 
@@ -127,6 +128,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+bool tail_choice() {
+    static bool on = [] {
+        const char* e = std::getenv("RLRA_GEMM_TAIL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 bool tma_choice() {
     static bool on = [] {
         const char* e = std::getenv("RLRA_GEMM_TMA");
@@ -174,7 +183,8 @@ void launch_tma_cfg(Context& ctx, const GemmParams& p, const TmaPair& maps) {
         attr_set = true;
     }
     if (CL == 1) {
-        const int64_t grid = int64_t(p.mt) * p.nt * p.splits;
+        int64_t grid = int64_t(p.mt) * p.nt * p.splits;
+        if (p.tail_base != INT_MAX) grid = p.tail_base + (grid - p.tail_base) * p.tail_split;
         kern<<<dim3(unsigned(grid)), 384, kTmaSmem, ctx.stream>>>(p, maps);
     } else {
         const int64_t grid = int64_t(ceil_div(p.mt, CL)) * CL * p.nt * p.splits;
@@ -223,6 +233,23 @@ void launch_tma_epi(Context& ctx, const GemmParams& p, const TmaPair& maps, int 
     if (epi == EPI_STORE) return launch_tma_cfg<A_KM, EPI_STORE, false, 1>(ctx, p, maps);
     if (epi == EPI_SPLIT) return launch_tma_cfg<A_KM, EPI_SPLIT, false, 1>(ctx, p, maps);
     return launch_tma_cfg<A_KM, EPI_RESID, false, 1>(ctx, p, maps);
+}
+
+// C tile = alpha * sum of the tail parts + beta * C, for the tail tiles
+__global__ void tail_reduce_kernel(const double* ws, int split, int tail_base, int ntail, int mt, int nt, int M,
+                                   int N, double alpha, double beta, double* C, int64_t ldc) {
+    const int64_t per = int64_t(kTBM) * kTBN;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(ntail) * per;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int t = int(e / per), li = int(e % per);
+        const int tile = tail_base + t;
+        const int row = (tile / nt) % mt * kTBM + li % kTBM, col = tile % nt * kTBN + li / kTBM;
+        if (row >= M || col >= N) continue;
+        double s = 0.0;
+        for (int q = 0; q < split; ++q) s += ws[(int64_t(t) * split + q) * per + li];
+        double* c = C + row + int64_t(col) * ldc;
+        *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
+    }
 }
 
 __global__ void split_reduce_kernel(const double* ws, int splits, int M, int N, double alpha,
@@ -309,6 +336,8 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
     p.krow0 = o.krow0;
     p.R = o.R;
     p.ldr = o.ldr;
+    p.tail_base = INT_MAX;
+    p.tail_split = 1;
 
     int64_t tiles = int64_t(p.mt) * p.nt;
     if (o.upper_tiles_only) tiles = int64_t(p.mt) * (p.mt + 1) / 2;
@@ -368,6 +397,24 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
     // TMA path: big tiles, B k-contiguous (op(B) = N) or generated, 16-byte
     // aligned operands with 16-byte-multiple leading dimensions
     const bool tma = big && vec && (opb == Op::N || o.philox_b) && tma_choice() && tensor_map_encoder();
+    Buf tail_ws;
+    int ntail = 0;
+    if (tma && epi == EPI_STORE && splits == 1 && !o.philox_b && !o.upper_tiles_only && !o.tri_b_upper &&
+        tail_choice()) {
+        // the last partial wave runs its tiles as tail_split k-chunks each
+        const int64_t full = (tiles / cap) * cap;
+        ntail = int(tiles - full);
+        const int s_t = ntail > 0 ? int(std::min<int64_t>(8, cap / ntail)) : 1;
+        if (full > 0 && ntail > 0 && s_t >= 2 && K >= 8 * kTBK * s_t) {
+            p.tail_base = int(full);
+            p.tail_split = s_t;
+            p.tail_kchunk = ceil_div(ceil_div(K, s_t), kTBK) * kTBK;
+            tail_ws = Buf(ctx, sizeof(double) * size_t(ntail) * s_t * kTBM * kTBN);
+            p.tail_ws = tail_ws.d();
+        } else {
+            ntail = 0;
+        }
+    }
     if (tma) {
         TmaPair maps;
         maps.a3d = 0;
@@ -386,6 +433,14 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
             launch_tma_epi<true>(ctx, p, maps, epi, o.philox_b);
         else
             launch_tma_epi<false>(ctx, p, maps, epi, o.philox_b);
+        if (ntail > 0) {
+            const int64_t tot = int64_t(ntail) * kTBM * kTBN;
+            tail_reduce_kernel<<<int(std::min<int64_t>((tot + 255) / 256, int64_t(ctx.num_sms) * 8)), 256, 0,
+                                 ctx.stream>>>(p.tail_ws, p.tail_split, p.tail_base, ntail, p.mt, p.nt, M, N, alpha,
+                                               beta, C, ldc);
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+        }
     } else if (big && big_cfg_choice() == 16) {
         launch_ops<CfgBig16>(ctx, opa, opb, vec, p, epi, o.philox_b);
     } else if (big) {

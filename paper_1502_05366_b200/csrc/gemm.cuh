@@ -47,6 +47,13 @@ struct GemmParams {
     const double* R;
     int64_t ldr;
     double* partials;  // one per tile
+    // tail-wave split (TMA path, EPI_STORE, splits == 1): CTAs from tail_base
+    // on cover the last partial wave's tiles, each tile cut into tail_split
+    // k-chunks of tail_kchunk whose partials go to tail_ws (reduced after)
+    int tail_base;     // first tail CTA (INT_MAX: none)
+    int tail_split;
+    int tail_kchunk;
+    double* tail_ws;   // [tail tile][part][128 x 128]
 };
 
 // ---------------------------------------------------------------- philox ---

@@ -124,8 +124,14 @@ __global__ void __launch_bounds__(384, 1)
     __shared__ __align__(8) uint64_t full_bar[kTStages], empty_bar[kTStages];
     __shared__ double red[NCW];
 
-    const int tile = blockIdx.x;
+    int tile = blockIdx.x;
     int nt_i, mt_i, split, crank = 0;
+    int tpart = -1;  // >= 0: this CTA computes k-chunk tpart of a tail tile
+    if (EPI == EPI_STORE && CL == 1 && tile >= p.tail_base) {
+        const int q = tile - p.tail_base;
+        tile = p.tail_base + q / p.tail_split;
+        tpart = q % p.tail_split;
+    }
     if (CL == 1) {
         nt_i = tile % p.nt;
         const int rest = tile / p.nt;
@@ -146,8 +152,12 @@ __global__ void __launch_bounds__(384, 1)
         split = rest / mg;
     }
     const int m0 = mt_i * kTBM, n0 = nt_i * kTBN;
-    const int k_begin = split * p.k_chunk;
+    int k_begin = split * p.k_chunk;
     int k_end = min(p.K, k_begin + p.k_chunk);
+    if (tpart >= 0) {
+        k_begin = tpart * p.tail_kchunk;
+        k_end = min(p.K, k_begin + p.tail_kchunk);
+    }
     if (p.tri_b_upper) k_end = min(k_end, n0 + kTBN);
     const int nk = k_end > k_begin ? (k_end - k_begin + kTBK - 1) / kTBK : 0;
 
@@ -262,6 +272,15 @@ __global__ void __launch_bounds__(384, 1)
         arow[i] = A_KM ? wm * kTWM + (i >> 1) * 16 + tma_km_row(lr, i & 1) : wm * kTWM + i * 8 + tma_xm_row(lr);
 #pragma unroll
     for (int j = 0; j < NF; ++j) bcol[j] = wn * kTWN + j * 8 + tma_xm_row(lr);
+    // fragment byte offsets at kk = 0; the later k-steps are an XOR of the
+    // swizzle bits (4..6) with a constant (+ a row immediate for KM):
+    //   XM: off(kk) = off(0) ^ (kk << 3)
+    //   KM: off(kk) = (off(0) ^ ((kk & 4) << 4)) + kk * 128
+    uint32_t offa[MF], offb[NF];
+#pragma unroll
+    for (int i = 0; i < MF; ++i) offa[i] = A_KM ? tma_km_off(lc, arow[i]) : tma_xm_off(lc, arow[i]);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) offb[j] = tma_xm_off(lc, bcol[j]);
 
     double acc[MF][NF][2];
 #pragma unroll
@@ -272,20 +291,27 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t rempty[CL];
 #pragma unroll
     for (int r = 0; r < CL; ++r) rempty[r] = CL > 1 ? cluster_map(smem_u32(&empty_bar[0]), r) : 0u;
+    const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
+    int st = 0;
+    uint32_t phase = 0;
     for (int kt = 0; kt < nk; ++kt) {
-        const int st = kt % kTStages;
-        mbar_wait(&full_bar[st], (kt / kTStages) & 1);
-        const uint32_t a_s = smem_u32(sA + st * kTABytes);
-        const uint32_t b_s = smem_u32(sB + st * kTBBytes);
+        mbar_wait(&full_bar[st], phase);
+        const uint32_t a_s = sa0 + uint32_t(st * kTABytes);
+        const uint32_t b_s = sb0 + uint32_t(st * kTBBytes);
+        uint32_t fa[MF], fb[NF];
+#pragma unroll
+        for (int i = 0; i < MF; ++i) fa[i] = a_s + offa[i];
+#pragma unroll
+        for (int j = 0; j < NF; ++j) fb[j] = b_s + offb[j];
 #pragma unroll
         for (int kk = 0; kk < kTBK; kk += 4) {
-            const int k = kk + lc;
             double af[MF], bf[NF];
 #pragma unroll
             for (int i = 0; i < MF; ++i)
-                af[i] = lds_f64(a_s + (A_KM ? tma_km_off(k, arow[i]) : tma_xm_off(k, arow[i])));
+                af[i] = A_KM ? lds_f64((fa[i] ^ uint32_t((kk & 4) << 4)) + uint32_t(kk * 128))
+                             : lds_f64(fa[i] ^ uint32_t(kk << 3));
 #pragma unroll
-            for (int j = 0; j < NF; ++j) bf[j] = lds_f64(b_s + tma_xm_off(k, bcol[j]));
+            for (int j = 0; j < NF; ++j) bf[j] = lds_f64(fb[j] ^ uint32_t(kk << 3));
 #pragma unroll
             for (int i = 0; i < MF; ++i)
 #pragma unroll
@@ -299,6 +325,10 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int r = 0; r < CL; ++r) mbar_arrive_cluster(rempty[r] + 8u * st);
             }
+        }
+        if (++st == kTStages) {
+            st = 0;
+            phase ^= 1u;
         }
     }
 
@@ -316,7 +346,10 @@ __global__ void __launch_bounds__(384, 1)
                 const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
                 if (row < p.M && col < p.N) {
                     const double v = acc[i][j][h];
-                    if (EPI == EPI_STORE) {
+                    if (EPI == EPI_STORE && tpart >= 0) {
+                        const int64_t slot = int64_t(tile - p.tail_base) * p.tail_split + tpart;
+                        p.tail_ws[slot * (kTBM * kTBN) + (row - m0) + (col - n0) * kTBM] = v;
+                    } else if (EPI == EPI_STORE) {
                         double* c = p.C + row + int64_t(col) * p.ldc;
                         *c = p.beta == 0.0 ? p.alpha * v : p.alpha * v + p.beta * *c;
                     } else if (EPI == EPI_SPLIT) {

@@ -229,6 +229,18 @@ def test_matmul_tma_paths_vs_oracle(eng, orc, ta, m, n, k):
     assert rel_fro(got, orc.matmul(a, b, ta, 0)) <= 1e-13
 
 
+@pytest.mark.parametrize("ta", [0, 1])
+def test_matmul_tail_wave_split_vs_oracle(eng, orc, ta):
+    """150 tiles on 148 SMs: the 2 tail tiles run as 8 k-chunks each
+    (gemm.cu tail split) and are reduced with alpha/beta afterwards."""
+    rs = np.random.default_rng(5 + ta)
+    m, n, k = 19200, 100, 1500
+    a = rs.standard_normal((k, m) if ta else (m, k))
+    b = rs.standard_normal((k, n))
+    got = eng.matmul(a, b, bool(ta), False)
+    assert rel_fro(got, orc.matmul(a, b, ta, 0)) <= 1e-13
+
+
 def test_sketch_philox_in_register_equals_materialized(eng):
     """The sketch GEMM's in-register Philox Omega is bit-identical to the
     materialised Omega (rlra_gaussian_philox) multiplied by the same kernel."""
