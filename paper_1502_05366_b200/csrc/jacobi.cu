@@ -1,5 +1,6 @@
 // jacobi.cu — one-sided Jacobi SVD and two-sided Jacobi eigensolver.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "jacobi.cuh"
 #include "reduce.cuh"
@@ -370,6 +371,247 @@ __global__ void completion_kernel(double* U, int64_t ldu, int m, int n, const in
     }
 }
 
+// ------------------------------------ Gram block one-sided Jacobi (large m) ---
+// For inputs whose column pairs do not fit shared memory (the C2 R-hat is
+// 6100 x 6100): columns in blocks of kGB; each outer round one CTA per block
+// pair (I, J) (round-robin tournament over the blocks):
+//   1. G = W_p^T W_p (64 x 64) streamed over the rows (DMMA, 8 warps of 16x32);
+//   2. inner cyclic Jacobi sweeps on G, the reference rotation formula and
+//      skip rule applied to (G_pp, G_qq, G_pq) — the same dot products the
+//      reference's one-sided sweep forms — accumulating J (64 x 64);
+//   3. W_p <- W_p J and V_p <- V_p J (streamed row chunks, DMMA).
+// One grid barrier per outer round; a sweep with no rotation in any pair
+// stops (reference core/jacobi.hpp:164-199 stop rule, on fresh Grams).
+constexpr int kGB = 32;
+constexpr int kGP = 2 * kGB;
+constexpr int kGPitch = kGP + 1;
+constexpr int kGChunk = 32;
+constexpr int kGCP = kGChunk + 4;   // chunk pitch: m8n8k4 fragment loads conflict-free
+constexpr int kGJP = kGP + 4;       // J copy for the DMMA apply, same reason
+constexpr int kGInnerCap = 1;  // one inner sweep per visit: fastest overall (C2: 1 -> 3.0 s, 3 -> 3.7 s)
+constexpr size_t kGramJacSmem = sizeof(double) * (2 * kGP * kGPitch + kGP * kGCP + kGP * kGJP);
+
+__device__ __forceinline__ void jac_dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+struct GramJacArgs {
+    unsigned* bar;
+    double* W;
+    int64_t ldw;
+    int m, n;
+    double* V;
+    int64_t ldv;
+    int nb;      // column blocks (even)
+    int* flags;  // [0..2] rotated-in-sweep, [3] status, [4] sweeps used
+    int inner_cap;
+};
+
+__global__ void __launch_bounds__(256) gram_jacobi_kernel(GramJacArgs a) {
+    extern __shared__ double gsm[];
+    double(*G)[kGPitch] = reinterpret_cast<double(*)[kGPitch]>(gsm);
+    double(*J)[kGPitch] = reinterpret_cast<double(*)[kGPitch]>(gsm + kGP * kGPitch);
+    double(*Cb)[kGCP] = reinterpret_cast<double(*)[kGCP]>(gsm + 2 * kGP * kGPitch);
+    double(*Jb)[kGJP] = reinterpret_cast<double(*)[kGJP]>(gsm + 2 * kGP * kGPitch + kGP * kGCP);
+    __shared__ double rcs[kGB], rsn[kGB];
+    __shared__ int ract[kGB];
+    __shared__ int s_any, s_rot;
+    const int t = threadIdx.x;
+    const int m = a.m, n = a.n, nb = a.nb;
+    const double eps = 1e-15;
+    volatile int* flags = a.flags;
+    int sweep = 0;
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            if (blockIdx.x == 0 && t == 0) flags[3] = RLRA_ECONV;
+            break;
+        }
+        if (blockIdx.x == 0 && t == 0) flags[(sweep + 1) % 3] = 0;
+        for (int r = 0; r < nb - 1; ++r) {
+            for (int g = blockIdx.x; g < nb / 2; g += gridDim.x) {
+                const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
+                const int bI = min(b1, b2), bJ = max(b1, b2);
+                auto gcol = [&](int c) { return c < kGB ? bI * kGB + c : bJ * kGB + (c - kGB); };
+                // ---- 1. Gram of the 64 columns on DMMA ----------------------
+                // warp (wi, wj) owns G[wi*16 .. +16][wj*32 .. +32]
+                const int warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+                const int wi = warp & 3, wj = warp >> 2;
+                double acc[2][4][2];
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                    for (int g2 = 0; g2 < 4; ++g2) acc[f][g2][0] = acc[f][g2][1] = 0.0;
+                double pre[8];
+                auto load_chunk = [&](int k0) {
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int e = t + it * 256, c = e >> 5, k = e & 31;
+                        const int gc = gcol(c);
+                        pre[it] = (gc < n && k0 + k < m) ? a.W[(k0 + k) + int64_t(gc) * a.ldw] : 0.0;
+                    }
+                };
+                load_chunk(0);
+                for (int k0 = 0; k0 < m; k0 += kGChunk) {
+                    __syncthreads();
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int e = t + it * 256;
+                        Cb[e >> 5][e & 31] = pre[it];
+                    }
+                    __syncthreads();
+                    if (k0 + kGChunk < m) load_chunk(k0 + kGChunk);
+#pragma unroll
+                    for (int kk = 0; kk < kGChunk; kk += 4) {
+                        double af[2], bf[4];
+#pragma unroll
+                        for (int f = 0; f < 2; ++f) af[f] = Cb[wi * 16 + f * 8 + lr][kk + lc];
+#pragma unroll
+                        for (int g2 = 0; g2 < 4; ++g2) bf[g2] = Cb[wj * 32 + g2 * 8 + lr][kk + lc];
+#pragma unroll
+                        for (int f = 0; f < 2; ++f)
+#pragma unroll
+                            for (int g2 = 0; g2 < 4; ++g2) jac_dmma(acc[f][g2][0], acc[f][g2][1], af[f], bf[g2]);
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                    for (int g2 = 0; g2 < 4; ++g2)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) G[wi * 16 + f * 8 + lr][wj * 32 + g2 * 8 + 2 * lc + h] = acc[f][g2][h];
+                for (int e = t; e < kGP * kGP; e += 256) J[e / kGP][e % kGP] = (e / kGP == e % kGP) ? 1.0 : 0.0;
+                if (t == 0) s_rot = 0;
+                __syncthreads();
+                // ---- 2. inner Jacobi sweeps on G, accumulating J -------------
+                for (int isw = 0; isw < a.inner_cap; ++isw) {
+                    if (t == 0) s_any = 0;
+                    __syncthreads();
+                    for (int ir = 0; ir < kGP - 1; ++ir) {
+                        if (t < kGB) {
+                            const int c1 = rr_col(t, ir, kGP), c2 = rr_col(kGP - 1 - t, ir, kGP);
+                            const int p = min(c1, c2), q = max(c1, c2);
+                            int act = 0;
+                            double c = 1.0, sn = 0.0;
+                            if (gcol(q) < n && gcol(p) < n) {
+                                const double app = G[p][p], aqq = G[q][q], apq = G[p][q];
+                                if (app != 0.0 && aqq != 0.0 && fabs(apq) > eps * sqrt(app * aqq)) {
+                                    const double zeta = (aqq - app) / (2.0 * apq);
+                                    const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                                    c = 1.0 / sqrt(1.0 + tt * tt);
+                                    sn = tt * c;
+                                    act = 1;
+                                    s_any = 1;
+                                }
+                            }
+                            rcs[t] = c;
+                            rsn[t] = sn;
+                            ract[t] = act;
+                        }
+                        __syncthreads();
+                        // columns of G and J
+                        for (int e = t; e < kGB * kGP; e += 256) {
+                            const int pi = e / kGP, i = e % kGP;
+                            if (!ract[pi]) continue;
+                            const int c1 = rr_col(pi, ir, kGP), c2 = rr_col(kGP - 1 - pi, ir, kGP);
+                            const int p = min(c1, c2), q = max(c1, c2);
+                            const double c = rcs[pi], sn = rsn[pi];
+                            const double gp = G[i][p], gq = G[i][q];
+                            G[i][p] = c * gp - sn * gq;
+                            G[i][q] = sn * gp + c * gq;
+                            const double jp = J[i][p], jq = J[i][q];
+                            J[i][p] = c * jp - sn * jq;
+                            J[i][q] = sn * jp + c * jq;
+                        }
+                        __syncthreads();
+                        // rows of G
+                        for (int e = t; e < kGB * kGP; e += 256) {
+                            const int pi = e / kGP, i = e % kGP;
+                            if (!ract[pi]) continue;
+                            const int c1 = rr_col(pi, ir, kGP), c2 = rr_col(kGP - 1 - pi, ir, kGP);
+                            const int p = min(c1, c2), q = max(c1, c2);
+                            const double c = rcs[pi], sn = rsn[pi];
+                            const double gp = G[p][i], gq = G[q][i];
+                            G[p][i] = c * gp - sn * gq;
+                            G[q][i] = sn * gp + c * gq;
+                        }
+                        __syncthreads();
+                    }
+                    if (!s_any) break;
+                    if (t == 0) s_rot = 1;
+                }
+                __syncthreads();
+                if (!s_rot) continue;  // uniform across the CTA
+                if (t == 0) flags[sweep % 3] = 1;
+                // ---- 3. W_p <- W_p J, V_p <- V_p J on DMMA (row chunks) -------
+                for (int e = t; e < kGP * kGP; e += 256) Jb[e / kGP][e % kGP] = J[e / kGP][e % kGP];
+                // warp (wr, wc) owns out[wr*16 .. +16][wc*16 .. +16] of a 32 x 64 chunk
+                const int wr = warp & 1, wc = warp >> 1;
+                for (int mat = 0; mat < 2; ++mat) {
+                    double* X = mat == 0 ? a.W : a.V;
+                    const int64_t ldx = mat == 0 ? a.ldw : a.ldv;
+                    const int rows = mat == 0 ? m : n;
+                    auto load_x = [&](int k0) {
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int e = t + it * 256, c = e >> 5, k = e & 31, gc = gcol(c);
+                            pre[it] = (gc < n && k0 + k < rows) ? X[(k0 + k) + int64_t(gc) * ldx] : 0.0;
+                        }
+                    };
+                    load_x(0);
+                    for (int k0 = 0; k0 < rows; k0 += kGChunk) {
+                        __syncthreads();
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int e = t + it * 256;
+                            Cb[e >> 5][e & 31] = pre[it];
+                        }
+                        __syncthreads();
+                        // the next chunk's rows are disjoint from this chunk's outputs
+                        if (k0 + kGChunk < rows) load_x(k0 + kGChunk);
+                        double o[2][2][2];
+#pragma unroll
+                        for (int f = 0; f < 2; ++f)
+#pragma unroll
+                            for (int g2 = 0; g2 < 2; ++g2) o[f][g2][0] = o[f][g2][1] = 0.0;
+#pragma unroll
+                        for (int kk = 0; kk < kGP; kk += 4) {
+                            double af[2], bf[2];
+#pragma unroll
+                            for (int f = 0; f < 2; ++f) af[f] = Cb[kk + lc][wr * 16 + f * 8 + lr];
+#pragma unroll
+                            for (int g2 = 0; g2 < 2; ++g2) bf[g2] = Jb[kk + lc][wc * 16 + g2 * 8 + lr];
+#pragma unroll
+                            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                                for (int g2 = 0; g2 < 2; ++g2) jac_dmma(o[f][g2][0], o[f][g2][1], af[f], bf[g2]);
+                        }
+#pragma unroll
+                        for (int f = 0; f < 2; ++f) {
+                            const int k = k0 + wr * 16 + f * 8 + lr;
+#pragma unroll
+                            for (int g2 = 0; g2 < 2; ++g2)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) {
+                                    const int gj = gcol(wc * 16 + g2 * 8 + 2 * lc + h);
+                                    if (gj < n && k < rows) X[k + int64_t(gj) * ldx] = o[f][g2][h];
+                                }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            grid_sync(a.bar);
+        }
+        const int rotated = flags[sweep % 3];
+        ++sweep;
+        if (!rotated || n < 2) break;
+    }
+    if (blockIdx.x == 0 && t == 0) flags[4] = sweep;
+}
+
 int coop_grid(Context& ctx, const void* kern, int want_blocks) {
     int per_sm = 0;
     RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kJacThreads, 0));
@@ -557,6 +799,31 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         void* args[] = {&b};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
                                               args, bj_smem, ctx.stream));
+    } else if (n > 2 * kGB) {
+        // columns too long for shared memory: Gram block Jacobi
+        static int gram_cap = 0;
+        if (!gram_cap) {
+            RLRA_CUDA(cudaFuncSetAttribute(gram_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kGramJacSmem)));
+            int per = 0;
+            RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gram_jacobi_kernel, 256, kGramJacSmem));
+            gram_cap = std::max(1, per) * ctx.num_sms;
+        }
+        GramJacArgs g;
+        g.bar = ctx.gbar;
+        g.W = W.m.p;
+        g.ldw = W.m.ld;
+        g.m = m;
+        g.n = n;
+        g.V = V.m.p;
+        g.ldv = V.m.ld;
+        g.nb = ceil_div(n, kGB) + (ceil_div(n, kGB) & 1);
+        g.flags = flags.i();
+        g.inner_cap = kGInnerCap;
+        void* args[] = {&g};
+        const int grid = std::min(g.nb / 2, gram_cap);
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)gram_jacobi_kernel, dim3(grid), dim3(256), args, kGramJacSmem,
+                                              ctx.stream));
     } else {
         const int pairs = (n + 1) / 2;
         const int G = coop_grid(ctx, (const void*)onesided_jacobi_kernel, ceil_div(pairs, kJacThreads / 32));

@@ -172,6 +172,25 @@ def test_small_svd_vs_oracle(eng, orc, m, n):
     assert match_columns_up_to_sign(u, uo) <= 1e-8
 
 
+@pytest.mark.parametrize("m,n,decay", [(2000, 120, 0.0), (1800, 200, 30.0)])
+def test_small_svd_gram_block_jacobi_vs_oracle(eng, orc, m, n, decay):
+    """Columns too long for shared memory (16 x m doubles > 200 KB) take the
+    Gram block Jacobi kernel: same sigma as the reference's one-sided sweep
+    (graded spectra included), orthonormal factors, reconstruction."""
+    rs = np.random.default_rng(m + n)
+    a = rs.standard_normal((m, n))
+    if decay:
+        q1, _ = np.linalg.qr(rs.standard_normal((m, n)))
+        q2, _ = np.linalg.qr(rs.standard_normal((n, n)))
+        a = (q1 * np.exp(-np.arange(n) / decay)) @ q2.T
+    u, s, v = eng.small_svd(a)
+    uo, so, vo = orc.small_svd(a)
+    assert np.all(np.diff(s) <= 0)
+    assert np.max(np.abs(s - so) / so) <= 1e-10
+    assert rel_fro((u * s) @ v.T, a) <= 1e-12
+    assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
+
+
 def test_small_svd_kats(eng):
     _, s, _ = eng.small_svd(np.diag([2.0, -3.0]))
     assert np.allclose(s, [3.0, 2.0], rtol=1e-15)  # test_jacobi.cpp:95-101
