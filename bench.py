@@ -286,10 +286,10 @@ def main():
                                                     np.exp(-np.arange(3685) / 100.0), SEED_GEN)
         A = Ad.t
         out = {}
+        comm = D.NcclComm(eng)  # the C++ driver's own NCCL communicator
 
-        def step(seed):
-            out["U"], out["S"], out["V"] = D.rsvd_v2_rowsharded(be, Ad, m, k, p, q, s,
-                                                                R.Omega.philox(seed))
+        def step(seed):  # csrc/dist.cu through rlra_rsvd_rowsharded
+            out["U"], out["S"], out["V"] = D.rsvd_v2_native(comm, Ad, m, k, p, q, s, R.Omega.philox(seed))
 
     for w in range(args.warmup):
         step(SEED_OMEGA + w)
@@ -359,8 +359,8 @@ def main():
         "config": {"workload": f"C5 rsvd_v2 m={m} n={n} k={k} p={p} q={q} s={s}",
                    "omega": "philox in-register", "l2": "A (32 GB) >> L2; no flush needed",
                    "parallelism": "1 GPU" if not use_dist else
-                   f"A row-sharded over {world} GPUs ({m_loc} rows/rank), NCCL allreduce of "
-                   "Grams and n x l partials"},
+                   f"A row-sharded over {world} GPUs ({m_loc} rows/rank), C++ driver "
+                   "(rlra_rsvd_rowsharded) with NCCL allreduce of Grams and n x l partials"},
         "time_s": ms_step / 1e3,
         "frac_of_fp64_peak": value / world / FP64_DMMA_PEAK_TFLOPS,
         "phases_ms": {k_: round(v_, 3) for k_, v_ in sorted(phases.items())},
@@ -402,7 +402,7 @@ def main():
                 Uh.copy_(out["U"].t[: m_loc * k])
                 Sh.copy_(out["S"].t[:k])
                 Vh.copy_(out["V"].t[: n * k])
-            path = "dist.rsvd_v2_rowsharded with per-rank pinned host shards"
+            path = "rlra_rsvd_rowsharded with per-rank pinned host shards"
 
         estep(SEED_OMEGA)
         if use_dist:
@@ -441,6 +441,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if use_dist:
+        comm.close()
         torch.distributed.destroy_process_group()
 
 

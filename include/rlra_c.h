@@ -118,6 +118,28 @@ rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap,
 /* The cudaStream_t the context launches on (for event timing by callers). */
 void* rlra_ctx_stream(const rlra_ctx* ctx);
 const char* rlra_last_error(void);
+
+/* ------------------------------------------------- row-sharded multi-GPU ---
+ * One process (one rlra_ctx) per GPU; A (m_total x n) split by rows.  The
+ * collectives are NCCL (loaded at run time from libnccl.so.2) on the context
+ * stream over NVLink: allreduce of the l x l CholQR Grams and of the n x l
+ * partials A^T Y / A^T Q (BASELINE north_star).  Launcher: rank 0 calls
+ * rlra_comm_unique_id and distributes the 128 bytes (MPI, torch.distributed,
+ * a file); every rank calls rlra_comm_create with its rank.  Replaces the
+ * reference's single-address-space rsvd_v2 (rsvd.hpp:154-160) for
+ * multi-GPU callers; single-GPU callers keep rlra_rsvd. */
+typedef struct rlra_comm rlra_comm;
+rlra_status rlra_comm_unique_id(unsigned char id[128]);
+rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nranks, int rank, rlra_comm** out);
+rlra_status rlra_comm_destroy(rlra_comm* comm);
+/* rsvd_v2 with A's rows [row0, row0 + m_local) on this rank (a: m_local x n,
+ * loc host or device); U: this rank's m_local x k rows of U; sigma (k) and V
+ * (n x k) replicated.  Omega: Philox (identical on every rank) or a callback
+ * that draws the same n x l matrix on every rank. */
+rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                 int64_t lda, int64_t m_total, int k, int p, int q, int s,
+                                 const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,
+                                 int64_t ldv);
 const char* rlra_version(void);
 
 /* -------------------------------------------------------- kernel level --- */

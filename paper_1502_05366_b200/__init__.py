@@ -92,6 +92,7 @@ def lib():
         L.rlra_rng_next_u64.restype = C.c_uint64
         L.rlra_rng_next_gaussian.restype = C.c_double
         L.rlra_rng_seed.argtypes = [C.c_void_p, C.c_uint64]
+        L.rlra_comm_destroy.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -538,6 +539,33 @@ class Engine:
         _check(lib().rlra_rsvd(self._ctx, DEVICE, variant, C.c_void_p(a_ptr), m, n, _i64(lda), k,
                                p, q, s, C.byref(om), C.c_void_p(u_ptr), _i64(m),
                                C.c_void_p(sigma_ptr), C.c_void_p(v_ptr), _i64(n)))
+
+    # -- row-sharded multi-GPU path (C++ driver + NCCL, csrc/dist.cu) ----------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """rlra_comm_unique_id: the 128-byte NCCL id rank 0 distributes."""
+        buf = (C.c_ubyte * 128)()
+        _check(lib().rlra_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_create(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != 128:
+            raise RlraError("NCCL unique id must be 128 bytes")
+        h = C.c_void_p()
+        _check(lib().rlra_comm_create(self._ctx, (C.c_ubyte * 128).from_buffer_copy(uid), nranks, rank,
+                                      C.byref(h)))
+        return h
+
+    @staticmethod
+    def comm_destroy(h):
+        lib().rlra_comm_destroy(h)
+
+    def device_rsvd_rowsharded(self, comm, a_ptr, m_local, n, lda, m_total, k, p, q, s, omega, u_ptr, ldu,
+                               sigma_ptr, v_ptr, ldv):
+        om = omega.struct()
+        _check(lib().rlra_rsvd_rowsharded(self._ctx, comm, DEVICE, C.c_void_p(a_ptr), m_local, n, _i64(lda),
+                                          _i64(m_total), k, p, q, s, C.byref(om), C.c_void_p(u_ptr), _i64(ldu),
+                                          C.c_void_p(sigma_ptr), C.c_void_p(v_ptr), _i64(ldv)))
 
     def host_rsvd_ptr(self, variant, a_ptr, m, n, lda, k, p, q, s, omega, u_ptr, sigma_ptr, v_ptr):
         """rlra_rsvd with HOST pointers (pinned or pageable): the drop-in call

@@ -12,6 +12,9 @@
 
 #include "../../include/rlra_c.h"
 #include "cpqr.cuh"
+#include <climits>
+
+#include "dist.cuh"
 #include "engine.cuh"
 #include "gemm.cuh"
 #include "jacobi.cuh"
@@ -544,6 +547,65 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
             In A(C, loc, a, m, n, lda, "a");
             rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
         }
+        U.finish(C);
+        V.finish(C);
+        S.finish(C);
+        sync(C);
+    });
+}
+
+struct rlra_comm {
+    Comm c;
+};
+
+rlra_status rlra_comm_unique_id(unsigned char id[128]) {
+    try {
+        if (!id) raise(RLRA_EINVAL, "null id buffer");
+        comm_unique_id(id);
+        return RLRA_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<rlra_status>(e.status);
+    }
+}
+
+rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nranks, int rank, rlra_comm** out) {
+    return guard(ctx, [&](Context& C) {
+        if (!out || !id) raise(RLRA_EINVAL, "null argument to rlra_comm_create");
+        *out = nullptr;
+        auto* cm = new rlra_comm();
+        try {
+            comm_init(C, cm->c, id, nranks, rank);
+        } catch (...) {
+            delete cm;
+            throw;
+        }
+        *out = cm;
+    });
+}
+
+rlra_status rlra_comm_destroy(rlra_comm* comm) {
+    if (!comm) return RLRA_OK;
+    comm_destroy(comm->c);
+    delete comm;
+    return RLRA_OK;
+}
+
+rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                 int64_t lda, int64_t m_total, int k, int p, int q, int s,
+                                 const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,
+                                 int64_t ldv) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        if (m_total < m_local || m_total > INT32_MAX)
+            raise(RLRA_EDIM, fmt("rsvd_rowsharded: m_total %lld, local rows %d", (long long)m_total, m_local));
+        check_sample_rank(k, p, int(m_total), n);
+        check_sample(k + p, q, s, int(m_total), n);
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m_local, n, lda, "a");
+        Out U(C, loc, u, m_local, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
+        OutVec<double> S(C, loc, sigma, k, "sigma");
+        rsvd_v2_rowsharded(C, comm->c, A.m, m_total, k, p, q, s, om, U.m, S.d, V.m);
         U.finish(C);
         V.finish(C);
         S.finish(C);

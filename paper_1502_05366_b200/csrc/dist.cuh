@@ -1,0 +1,25 @@
+// dist.cuh — row-sharded multi-GPU path (dist.cu): NCCL communicator and the
+// row-sharded rsvd_v2 driver.
+#pragma once
+
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace rlra_b200 {
+
+struct Comm {
+    void* handle = nullptr;  // ncclComm_t
+    int nranks = 1, rank = 0, device = 0;
+};
+
+void comm_unique_id(unsigned char out[128]);
+void comm_init(Context& ctx, Comm& cm, const unsigned char id[128], int nranks, int rank);
+void comm_destroy(Comm& cm);
+
+// rsvd_v2 on the row block A_g (m_g x n) of an m_total x n matrix held by the
+// ranks of cm; U_g (m_g x k) row-sharded like A, sigma (device, k) and V
+// (n x k) replicated on every rank.
+void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
+                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V);
+
+}  // namespace rlra_b200

@@ -63,6 +63,8 @@ double read_scalar(Context& ctx, const double* d) {
 // Y = A * Omega_draw (op_a = N, Omega n x l) or Y = A^T * Omega_draw (op_a =
 // T, Omega m x l).  Philox Omega is generated inside the GEMM; callback Omega
 // is drawn on the host in the reference's order and uploaded.
+}  // namespace
+
 void sketch(Context& ctx, Op op_a, const DMat& A, int l, OmegaSource& om, const DMat& Y) {
     const int rows = int(op_a == Op::N ? A.cols : A.rows);
     const int draw = om.next_draw++;
@@ -102,6 +104,8 @@ void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat
     gemm(ctx, Op::N, Op::N, 1.0, Bt, Uh.m.block(0, 0, l, k), 0.0, V);  // (Qhat*Uhat)(:,1:k)
     RLRA_CUDA(cudaMemcpyAsync(sigma, s.p, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx.stream));
 }
+
+namespace {
 
 // rsvd.hpp:115-140 finish_qb_bbt: Q m x l, B l x n
 void finish_bbt(Context& ctx, const DMat& Q, const DMat& B, int k, const DMat& U, double* sigma,

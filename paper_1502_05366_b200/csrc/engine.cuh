@@ -33,6 +33,14 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
 void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt,
                    bool span_only = false);
 
+// Y = A Omega (op(A) = A or A^T), one Omega draw from om
+enum class Op;
+void sketch(Context& ctx, Op op_a, const DMat& A, int l, OmegaSource& om, const DMat& Y);
+
+// rsvd.hpp:144-156 finish_qb_qr_bt: Q m x l, Bt n x l (overwritten by Qhat)
+void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat& U, double* sigma,
+                  const DMat& V);
+
 // rsvd.hpp:127-160; U m x k, sigma (device) k, V n x k
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
           const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr);

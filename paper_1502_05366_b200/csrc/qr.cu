@@ -670,6 +670,14 @@ __global__ void add_diag_kernel(double* G, int64_t ldg, int n, double s) {
 }
 }  // namespace
 
+void add_diag(Context& ctx, const DMat& G, double s) {
+    const int n = int(std::min(G.rows, G.cols));
+    if (n <= 0) return;
+    add_diag_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(G.p, G.ld, n, s);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+}
+
 // Shifted CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020):
 // G = Y^T Y + s I with s = 11 (m n + n (n+1)) u ||Y||^2, R1 = chol(G),
 // Y1 = Y R1^{-1} has condition number O(u^{-1/2}) for any kappa(Y) < u^{-1},

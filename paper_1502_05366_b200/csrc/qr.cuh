@@ -44,4 +44,7 @@ void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int 
 // when a pivot fell below floor * original diagonal (or was not positive).
 bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor);
 
+// G(i, i) += s
+void add_diag(Context& ctx, const DMat& G, double s);
+
 }  // namespace rlra_b200

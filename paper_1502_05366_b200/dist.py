@@ -19,10 +19,14 @@ the exchanges are the small ones north_star names:
 The algorithm is the reference's rsvd_v2 (rsvd.hpp:154-160, sketch.hpp:44-60)
 with the same Omega; only the association order of the sums changes.
 
-The orchestration is written against a small backend interface so the same
-code runs on the CUDA engine (GpuBackend, the product) and, in the test-suite,
-on a numpy stand-in over gloo (tests/_dist_numpy.py) to check the collective
-logic at world size 2 without GPUs.
+The product path is the C++ driver (csrc/dist.cu, C-ABI rlra_rsvd_rowsharded)
+with its own NCCL communicator: `NcclComm` below creates it (rank 0's
+unique id travels over the torch.distributed group) and `rsvd_v2_native`
+calls it.  The Python orchestration further down restates the same algorithm
+against a small backend interface so the collective logic also runs, in the
+test-suite, on a numpy stand-in over gloo (tests/_dist_numpy.py) at world
+size 2 without GPUs; `GpuBackend` runs that restatement on the engine's
+shard primitives.
 """
 from __future__ import annotations
 
@@ -137,6 +141,56 @@ class GpuBackend:
         t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
+
+
+# ------------------------------------------------ native C++/NCCL driver --
+class NcclComm:
+    """The engine's NCCL communicator (rlra_comm) for the ranks of a
+    torch.distributed group: rank 0 draws the unique id, the group broadcasts
+    it, every rank joins."""
+
+    def __init__(self, eng, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.eng = eng
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = eng.comm_unique_id() if self.rank == 0 else bytes(128)
+        if self.world > 1:
+            dev = torch.device("cuda", eng.device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+            t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            uid = bytes(t.cpu().tolist())
+        self.handle = eng.comm_create(uid, self.world, self.rank)
+
+    def close(self):
+        if self.handle:
+            self.eng.comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def rsvd_v2_native(comm, A, m_total, k, p, q, s, omega):
+    """rsvd_v2 on this rank's row block A (DM, m_g x n) through the C++
+    driver; returns (U_g, sigma, V) as DMs (U row-sharded, sigma and V
+    replicated)."""
+    import torch
+
+    eng = comm.eng
+    n = A.cols
+    dev = torch.device("cuda", eng.device)
+    U = DM(torch.empty(max(A.rows * k, 1), dtype=torch.float64, device=dev), A.rows, k)
+    S = DM(torch.empty(k, dtype=torch.float64, device=dev), k, 1)
+    V = DM(torch.empty(n * k, dtype=torch.float64, device=dev), n, k)
+    eng.device_rsvd_rowsharded(comm.handle, A.ptr, A.rows, n, A.ld, m_total, k, p, q, s, omega, U.ptr, U.ld,
+                               S.ptr, V.ptr, V.ld)
+    return U, S, V
 
 
 # ----------------------------------------------------------- orchestration --

@@ -47,3 +47,59 @@ def test_rowsharded_rsvd_nccl_world1_matches_engine():
         assert rel <= 1.01 * rel_e
     finally:
         dist.destroy_process_group()
+
+
+def test_native_rowsharded_rsvd_world1_matches_engine():
+    """The C++ row-sharded driver (csrc/dist.cu) with a real 1-rank NCCL
+    communicator: every collective runs through NCCL; the result matches the
+    single-GPU engine (same Philox Omega)."""
+    import torch
+
+    from paper_1502_05366_b200 import dist as D
+    from paper_1502_05366_b200.testmat import gen_test_matrix_device
+
+    eng = R.Engine(0)
+    torch.cuda.set_device(0)
+    m, n, k, p, q = 6000, 3000, 100, 10, 2
+    A, st = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(1500) / 30.0), seed=9)
+    comm = D.NcclComm(eng)
+    try:
+        U, S, V = D.rsvd_v2_native(comm, D.DM(A, m, n), m, k, p, q, 1, R.Omega.philox(4242))
+    finally:
+        comm.close()
+    Ue = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    Ve = torch.empty(n * k, dtype=torch.float64, device="cuda")
+    Se = torch.empty(k, dtype=torch.float64, device="cuda")
+    eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, 1, R.Omega.philox(4242), Ue.data_ptr(),
+                    Se.data_ptr(), Ve.data_ptr())
+    s_d, s_e = S.t.cpu().numpy(), Se.cpu().numpy()
+    assert np.max(np.abs(s_d - s_e) / s_e) <= 1e-10
+    stn = st.cpu().numpy()
+    assert np.max(np.abs(s_d[:20] - stn[:20]) / stn[:20]) <= 1e-10
+    rel = eng.device_rel_error(A.data_ptr(), m, n, U.ptr, S.ptr, V.ptr, k)
+    rel_e = eng.device_rel_error(A.data_ptr(), m, n, Ue.data_ptr(), Se.data_ptr(), Ve.data_ptr(), k)
+    assert rel <= 1.01 * rel_e
+
+
+def test_native_rowsharded_row_permutation_invariance():
+    """The sharded driver's sums are row-order independent: permuting A's
+    rows (what a different row partition does to the association order)
+    leaves sigma unchanged to rounding."""
+    import torch
+
+    from paper_1502_05366_b200 import dist as D
+    from paper_1502_05366_b200.testmat import gen_test_matrix_device
+
+    eng = R.Engine(0)
+    m, n, k, p, q = 4096, 2000, 64, 8, 1
+    A, _ = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(1000) / 20.0), seed=3)
+    perm = torch.randperm(m, generator=torch.Generator().manual_seed(0)).cuda()
+    Ap = A.view(n, m)[:, perm].contiguous().view(-1)
+    comm = D.NcclComm(eng)
+    try:
+        _, S1, _ = D.rsvd_v2_native(comm, D.DM(A, m, n), m, k, p, q, 1, R.Omega.philox(5))
+        _, S2, _ = D.rsvd_v2_native(comm, D.DM(Ap, m, n), m, k, p, q, 1, R.Omega.philox(5))
+    finally:
+        comm.close()
+    s1, s2 = S1.t.cpu().numpy(), S2.t.cpu().numpy()
+    assert np.max(np.abs(s1 - s2) / s1) <= 1e-10
