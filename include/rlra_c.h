@@ -136,6 +136,24 @@ rlra_status rlra_comm_destroy(rlra_comm* comm);
  * loc host or device); U: this rank's m_local x k rows of U; sigma (k) and V
  * (n x k) replicated.  Omega: Philox (identical on every rank) or a callback
  * that draws the same n x l matrix on every rank. */
+/* id_rand (interp.hpp:203-223) with A row-sharded: jc (n, 0-based column
+ * permutation, first k the skeleton) and V (n x k) replicated; the sketch is
+ * an allreduce of n x l partials.  Omega~ is m_total x l (Philox counter =
+ * global row), this rank using rows [row0, row0 + m_local). */
+rlra_status rlra_id_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                    int64_t lda, int64_t row0, int64_t m_total, int k, int p, int q, int s,
+                                    const rlra_omega* omega, int* jc, double* v, int64_t ldv,
+                                    double* qr_residual, int* clamped);
+/* cur_rand (interp.hpp:240-244) with A row-sharded: the row ID of C = A(:,Jc)
+ * is a column-pivoted QR whose pivot statistics are allgathered each step
+ * (north_star).  jc, v (n x k), jr (k global rows), u (k x k), r (k x n)
+ * replicated; w (m_local x k) and c (m_local x k) this rank's rows;
+ * residual = ||A - C U R||_F over all ranks. */
+rlra_status rlra_cur_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                     int64_t lda, int64_t row0, int64_t m_total, int k, int p, int q, int s,
+                                     const rlra_omega* omega, int* jc, int* jr, double* v, int64_t ldv, double* w,
+                                     int64_t ldw, double* c, int64_t ldc, double* u, int64_t ldu, double* r,
+                                     int64_t ldr, double* residual, double* qr_residual);
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,

@@ -567,6 +567,40 @@ class Engine:
                                           _i64(m_total), k, p, q, s, C.byref(om), C.c_void_p(u_ptr), _i64(ldu),
                                           C.c_void_p(sigma_ptr), C.c_void_p(v_ptr), _i64(ldv)))
 
+    def id_rand_rowsharded(self, comm, a_local, row0, m_total, k, p, q_power, s, rng=None, omega=None):
+        """rlra_id_rand_rowsharded with host buffers: a_local is this rank's
+        rows [row0, row0 + m_local) of A."""
+        a = _F(a_local)
+        mg, n = a.shape
+        om = _omega(omega, rng).struct()
+        jc = np.zeros(n, dtype=np.int32)
+        v = np.zeros((n, k), order="F")
+        res, cl = C.c_double(0), C.c_int(0)
+        _check(lib().rlra_id_rand_rowsharded(self._ctx, comm, HOST, _d(a), mg, n, _i64(_ld(a)), _i64(row0),
+                                             _i64(m_total), k, p, q_power, s, C.byref(om), _i(jc), _d(v),
+                                             _i64(max(1, n)), C.byref(res), C.byref(cl)))
+        return dict(jc=jc, v=v, k=k, qr_residual=res.value, clamped=bool(cl.value))
+
+    def cur_rand_rowsharded(self, comm, a_local, row0, m_total, k, p, q_power, s, rng=None, omega=None):
+        """rlra_cur_rand_rowsharded with host buffers (this rank's rows)."""
+        a = _F(a_local)
+        mg, n = a.shape
+        om = _omega(omega, rng).struct()
+        jc = np.zeros(n, dtype=np.int32)
+        jr = np.zeros(k, dtype=np.int32)
+        v = np.zeros((n, k), order="F")
+        w = np.zeros((mg, k), order="F")
+        c = np.zeros((mg, k), order="F")
+        u = np.zeros((k, k), order="F")
+        r = np.zeros((k, n), order="F")
+        res, qres = C.c_double(0), C.c_double(0)
+        _check(lib().rlra_cur_rand_rowsharded(self._ctx, comm, HOST, _d(a), mg, n, _i64(_ld(a)), _i64(row0),
+                                              _i64(m_total), k, p, q_power, s, C.byref(om), _i(jc), _i(jr),
+                                              _d(v), _i64(max(1, n)), _d(w), _i64(max(1, mg)), _d(c),
+                                              _i64(max(1, mg)), _d(u), _i64(max(1, k)), _d(r), _i64(max(1, k)),
+                                              C.byref(res), C.byref(qres)))
+        return dict(jc=jc, jr=jr, v=v, w=w, c=c, u=u, r=r, k=k, residual=res.value, qr_residual=qres.value)
+
     def host_rsvd_ptr(self, variant, a_ptr, m, n, lda, k, p, q, s, omega, u_ptr, sigma_ptr, v_ptr):
         """rlra_rsvd with HOST pointers (pinned or pageable): the drop-in call
         a reference user makes, H2D/D2H inside the call."""

@@ -613,6 +613,63 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
     });
 }
 
+rlra_status rlra_id_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                    int64_t lda, int64_t row0, int64_t m_total, int k, int p, int q, int s,
+                                    const rlra_omega* omega, int* jc, double* v, int64_t ldv,
+                                    double* qr_residual, int* clamped) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
+            raise(RLRA_EDIM, fmt("id_rand_rowsharded: rows [%lld, %lld) of %lld", (long long)row0,
+                                 (long long)(row0 + m_local), (long long)m_total));
+        check_sample_rank(k, p, int(m_total), n);
+        check_sample(k + p, q, s, n, int(m_total));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m_local, n, lda, "a");
+        OutVec<int> J(C, loc, jc, n, "jc");
+        Out V(C, loc, v, n, k, ldv, "v");
+        IdOut r = id_rand_rowsharded(C, comm->c, A.m, row0, m_total, k, p, q, s, om, J.d, V.m);
+        V.finish(C);
+        J.finish(C);
+        sync(C);
+        if (qr_residual) *qr_residual = r.qr_residual;
+        if (clamped) *clamped = r.clamped ? 1 : 0;
+    });
+}
+
+rlra_status rlra_cur_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
+                                     int64_t lda, int64_t row0, int64_t m_total, int k, int p, int q, int s,
+                                     const rlra_omega* omega, int* jc, int* jr, double* v, int64_t ldv, double* w,
+                                     int64_t ldw, double* c, int64_t ldc, double* u, int64_t ldu, double* r,
+                                     int64_t ldr, double* residual, double* qr_residual) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
+            raise(RLRA_EDIM, fmt("cur_rand_rowsharded: rows [%lld, %lld) of %lld", (long long)row0,
+                                 (long long)(row0 + m_local), (long long)m_total));
+        check_sample_rank(k, p, int(m_total), n);
+        check_sample(k + p, q, s, n, int(m_total));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m_local, n, lda, "a");
+        OutVec<int> Jc(C, loc, jc, n, "jc"), Jr(C, loc, jr, k, "jr");
+        Out V(C, loc, v, n, k, ldv, "v"), W(C, loc, w, m_local, k, ldw, "w"), Cm(C, loc, c, m_local, k, ldc, "c"),
+            U(C, loc, u, k, k, ldu, "u"), R(C, loc, r, k, n, ldr, "r");
+        IdOut idr;
+        const double res = cur_rand_rowsharded(C, comm->c, A.m, row0, m_total, k, p, q, s, om, Jc.d, V.m, Jr.d, W.m,
+                                               Cm.m, U.m, R.m, &idr);
+        V.finish(C);
+        W.finish(C);
+        Cm.finish(C);
+        U.finish(C);
+        R.finish(C);
+        Jc.finish(C);
+        Jr.finish(C);
+        sync(C);
+        if (residual) *residual = res;
+        if (qr_residual) *qr_residual = idr.qr_residual;
+    });
+}
+
 rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int64_t lda, int inplace,
                             int blk, int num_blocks, double tol, int q_power, int reorth_period,
                             const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,

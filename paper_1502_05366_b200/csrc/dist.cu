@@ -25,8 +25,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cfloat>
+#include <climits>
 #include <cstring>
 
+#include "cpqr.cuh"
 #include "dist.cuh"
 #include "engine.cuh"
 #include "gemm.cuh"
@@ -41,6 +44,7 @@ struct NcclApi {
     decltype(&ncclGetUniqueId) get_unique_id = nullptr;
     decltype(&ncclCommInitRank) comm_init_rank = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
 };
@@ -54,9 +58,11 @@ const NcclApi& nccl() {
         a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
         a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.comm_destroy || !a.error_string)
+        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.all_gather || !a.comm_destroy ||
+            !a.error_string)
             raise(RLRA_ENCCL, "libnccl.so.2 lacks a required symbol");
         return a;
     }();
@@ -72,6 +78,11 @@ void allreduce(Context& ctx, Comm& cm, double* p, size_t count) {
     if (count == 0) return;  // a 1-rank communicator still runs the collective (tests the plumbing)
     nccl_check(nccl().all_reduce(p, p, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(cm.handle), ctx.stream),
                "ncclAllReduce");
+}
+
+void allgather(Context& ctx, Comm& cm, const double* send, double* recv, size_t count) {
+    nccl_check(nccl().all_gather(send, recv, count, ncclFloat64, static_cast<ncclComm_t>(cm.handle), ctx.stream),
+               "ncclAllGather");
 }
 
 double allreduce_scalar(Context& ctx, Comm& cm, double x) {
@@ -192,6 +203,422 @@ void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, 
         allreduce(ctx, cm, Bt.m.p, size_t(n) * l);
     }
     finish_qr_bt(ctx, Y.m, Bt.m, k, U, sigma, V);              // replicated QR + Jacobi, local lift
+}
+
+
+// ------------------------------------------------ distributed CPQR (K8d) ---
+// Businger-Golub column-pivoted QR of X = C^T (k x m_total) whose columns
+// (the rows of C) are sharded over the ranks: the reference's
+// pivoted_qr_partial (core/qr.hpp:140-236) with the columns kept where they
+// live and their global positions tracked instead of swapping data.  Per step:
+//   local best (value, position) -> allgather of the per-rank records (the
+//   pivot statistics, north_star) -> every rank picks the same winner with
+//   the reference tie-break (largest value, earliest position) -> the owner
+//   contributes the pivot column to an allreduce (zeros elsewhere) -> every
+//   CTA rebuilds the same Householder reflector and applies it to its own
+//   trailing columns, downdating (and recomputing below 1e-6) the norms.
+namespace {
+
+constexpr int kDcThreads = 256;
+
+__device__ __forceinline__ bool dc_better(double v, double p, double bv, double bp) {
+    return v > bv || (v == bv && p < bp);
+}
+
+// record = (value, position, global index, local index) as doubles
+struct DcArgs {
+    double* X;      // k x mg, ld k (this rank's columns of C^T)
+    int k, mg;
+    int64_t row0;   // global index of local column 0
+    double* pos;    // mg global positions
+    double* cn;     // mg downdated squared norms
+    double* rn;     // mg reference norms
+    double* slots;  // per-CTA best (value, position, local)
+    double* rec;    // this rank's record (4)
+    double* all;    // world x 4 records
+    double* pc;     // k: pivot column (allreduced)
+    double* S11;    // k x k (ld k), replicated
+    int* jr;        // k global pivot indices (device)
+    int* win;       // [0] winner local index on this rank or -1
+    int rank, world;
+};
+
+__device__ void dc_block_best(double v, double p, double j, double* out) {
+    __shared__ double sv[32], sp[32], sj[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o), op = __shfl_xor_sync(0xffffffffu, p, o),
+                     oj = __shfl_xor_sync(0xffffffffu, j, o);
+        if (dc_better(ov, op, v, p)) {
+            v = ov;
+            p = op;
+            j = oj;
+        }
+    }
+    if (lane == 0) {
+        sv[warp] = v;
+        sp[warp] = p;
+        sj[warp] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bv = -DBL_MAX, bp = DBL_MAX, bj = -1;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w)
+            if (dc_better(sv[w], sp[w], bv, bp)) {
+                bv = sv[w];
+                bp = sp[w];
+                bj = sj[w];
+            }
+        out[0] = bv;
+        out[1] = bp;
+        out[2] = bj;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double dc_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// squared norms, positions, per-CTA best (core/qr.hpp:157-161)
+__global__ void __launch_bounds__(kDcThreads) dc_init_kernel(DcArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double bv = -DBL_MAX, bp = DBL_MAX, bj = -1;
+    for (int j = blockIdx.x * nw + warp; j < a.mg; j += gridDim.x * nw) {
+        double s = 0.0;
+        for (int i = lane; i < a.k; i += 32) {
+            const double x = a.X[i + int64_t(j) * a.k];
+            s += x * x;
+        }
+        s = dc_warp_sum(s);
+        const double p = double(a.row0 + j);
+        if (lane == 0) {
+            a.pos[j] = p;
+            a.cn[j] = s;
+            a.rn[j] = s;
+        }
+        if (dc_better(s, p, bv, bp)) {
+            bv = s;
+            bp = p;
+            bj = j;
+        }
+    }
+    dc_block_best(bv, bp, bj, a.slots + 3 * blockIdx.x);
+}
+
+// this rank's record from the CTA slots
+__global__ void dc_record_kernel(DcArgs a, int nslots) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double bv = -DBL_MAX, bp = DBL_MAX, bj = -1;
+    for (int c = 0; c < nslots; ++c)
+        if (dc_better(a.slots[3 * c], a.slots[3 * c + 1], bv, bp)) {
+            bv = a.slots[3 * c];
+            bp = a.slots[3 * c + 1];
+            bj = a.slots[3 * c + 2];
+        }
+    a.rec[0] = bv;
+    a.rec[1] = bp;
+    a.rec[2] = bj >= 0 ? double(a.row0) + bj : -1.0;
+    a.rec[3] = bj;
+}
+
+// winner over the ranks, pivot column staging, position swap (qr.hpp:179-187)
+__global__ void __launch_bounds__(1024) dc_select_kernel(DcArgs a, int f) {
+    __shared__ int s_wr, s_wj;
+    __shared__ double s_wp, s_wg;
+    if (threadIdx.x == 0) {
+        double bv = -DBL_MAX, bp = DBL_MAX, bg = -1, bj = -1;
+        int br = -1;
+        for (int r = 0; r < a.world; ++r) {
+            const double* q = a.all + 4 * r;
+            if (q[3] >= 0 && dc_better(q[0], q[1], bv, bp)) {
+                bv = q[0];
+                bp = q[1];
+                bg = q[2];
+                bj = q[3];
+                br = r;
+            }
+        }
+        s_wr = br;
+        s_wj = int(bj);
+        s_wp = bp;
+        s_wg = bg;
+        a.jr[f] = int(bg);
+        a.win[0] = (br == a.rank) ? int(bj) : -1;
+    }
+    __syncthreads();
+    const bool mine = s_wr == a.rank;
+    for (int i = threadIdx.x; i < a.k; i += blockDim.x)
+        a.pc[i] = mine ? a.X[i + int64_t(s_wj) * a.k] : 0.0;
+    // the column at position f moves to the winner's position
+    for (int j = threadIdx.x; j < a.mg; j += blockDim.x)
+        if (a.pos[j] == double(f)) a.pos[j] = s_wp;
+    __syncthreads();
+    if (mine && threadIdx.x == 0) a.pos[s_wj] = double(f);
+}
+
+// reflector from the pivot column, applied to the own trailing columns
+// (core/qr.hpp:44-66, 190-200), per-CTA best for the next step
+__global__ void __launch_bounds__(kDcThreads) dc_apply_kernel(DcArgs a, int f) {
+    extern __shared__ double dsm[];
+    double* v = dsm;  // k
+    __shared__ double red[32];
+    __shared__ double s_alpha, s_beta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5, k = a.k;
+    double s = 0.0;
+    for (int i = f + threadIdx.x; i < k; i += blockDim.x) s += a.pc[i] * a.pc[i];
+    s = dc_warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double norm2 = 0.0;
+        for (int w = 0; w < nw; ++w) norm2 += red[w];
+        const double x1 = a.pc[f], norm = sqrt(norm2);
+        const bool zero = norm < 1e-300;
+        const double alpha = x1 >= 0.0 ? -norm : norm;
+        s_alpha = zero ? 0.0 : alpha;
+        s_beta = zero ? 0.0 : 2.0 / (2.0 * (norm2 - alpha * x1));
+    }
+    __syncthreads();
+    const double alpha = s_alpha, beta = s_beta;
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        v[i] = i > f ? a.pc[i] : (i == f ? a.pc[f] - (beta != 0.0 ? alpha : 0.0) : 0.0);
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < k; i += blockDim.x)
+            a.S11[i + int64_t(f) * k] = i < f ? a.pc[i] : (i == f ? alpha : 0.0);
+    __syncthreads();
+    const int wj = a.win[0];
+    double bv = -DBL_MAX, bp = DBL_MAX, bj = -1;
+    for (int j = blockIdx.x * nw + warp; j < a.mg; j += gridDim.x * nw) {
+        double* x = a.X + int64_t(j) * k;
+        if (j == wj) {  // the pivot column becomes (.., alpha, 0, ..)
+            for (int i = f + lane; i < k; i += 32) x[i] = (i == f) ? alpha : 0.0;
+            continue;
+        }
+        const double p = a.pos[j];
+        if (p <= double(f)) continue;
+        if (beta != 0.0) {
+            double d = 0.0;
+            for (int i = f + lane; i < k; i += 32) d += v[i] * x[i];
+            const double fct = beta * dc_warp_sum(d);
+            for (int i = f + lane; i < k; i += 32) x[i] -= fct * v[i];
+            __syncwarp();
+        }
+        const double xf = x[f];
+        double c = a.cn[j] - xf * xf;
+        double rr = a.rn[j];
+        if (c < 1e-6 * rr) {
+            double q = 0.0;
+            for (int i = f + 1 + lane; i < k; i += 32) q += x[i] * x[i];
+            q = dc_warp_sum(q);
+            c = q;
+            rr = q;
+        }
+        if (lane == 0) {
+            a.cn[j] = c;
+            a.rn[j] = rr;
+        }
+        if (dc_better(c, p, bv, bp)) {
+            bv = c;
+            bp = p;
+            bj = j;
+        }
+    }
+    dc_block_best(bv, bp, bj, a.slots + 3 * blockIdx.x);
+}
+
+// sign fix of row i by sign(S11(i, i)) (qr.hpp:212-217), on S11 and X; the
+// signs are read first (sgn) so no thread sees a flipped diagonal
+__global__ void dc_sign_kernel(const double* S11, int k, double* sgn) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+        sgn[i] = S11[i + int64_t(i) * k] < 0.0 ? -1.0 : 1.0;
+}
+
+__global__ void dc_signfix_kernel(double* S11, double* X, int k, int mg, const double* sgn) {
+    const int64_t tot = int64_t(k) * (k + mg);
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % k);
+        const int64_t c = e / k;
+        if (sgn[i] > 0.0) continue;
+        if (c < k)
+            S11[i + c * k] = -S11[i + c * k];
+        else
+            X[i + (c - k) * k] = -X[i + (c - k) * k];
+    }
+}
+
+// W_g(j, :) = e_pos (skeleton row) or T(:, j)^T (interp.hpp:65-72, sharded)
+__global__ void dc_interp_kernel(const double* pos, const double* T, int k, int mg, double* W, int64_t ldw) {
+    const int64_t tot = int64_t(mg) * k;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(e % mg), c = int(e / mg);
+        const double p = pos[j];
+        W[j + int64_t(c) * ldw] = p < double(k) ? (p == double(c) ? 1.0 : 0.0) : T[c + int64_t(j) * k];
+    }
+}
+
+// R(f, :) = A_g(jr[f] - row0, :) where this rank owns the row, else 0
+__global__ void gather_owned_rows_kernel(const double* A, int64_t lda, int mg, int n, const int* jr, int k,
+                                         int64_t row0, double* R, int64_t ldr) {
+    const int64_t tot = int64_t(k) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int f = int(e % k), c = int(e / k);
+        const int64_t r = int64_t(jr[f]) - row0;
+        R[f + int64_t(c) * ldr] = (r >= 0 && r < mg) ? A[r + int64_t(c) * lda] : 0.0;
+    }
+}
+
+int dc_blocks(Context& ctx, int64_t work) {
+    return int(std::max<int64_t>(1, std::min<int64_t>(int64_t(ctx.num_sms) * 4, (work + 255) / 256)));
+}
+
+// id_row on the row-sharded C (m_g x k): jr (device, k, global rows), W_g
+// (m_g x k).  Returns whether the tri-solve clamped.
+bool row_id_rowsharded(Context& ctx, Comm& cm, const DMat& Cg, int64_t row0, int k, int* jr, const DMat& Wg) {
+    const int mg = int(Cg.rows);
+    DMatBuf X(ctx, k, std::max(mg, 1)), S11(ctx, k, k), T(ctx, k, std::max(mg, 1));
+    if (mg > 0) transpose_mat(ctx, Cg, X.m);
+    const int nblk = std::max(1, std::min(ctx.num_sms, ceil_div(std::max(mg, 1), kDcThreads / 32)));
+    Buf pos(ctx, sizeof(double) * std::max(mg, 1)), cn(ctx, sizeof(double) * std::max(mg, 1)),
+        rn(ctx, sizeof(double) * std::max(mg, 1)), slots(ctx, sizeof(double) * 3 * nblk), rec(ctx, sizeof(double) * 4),
+        all(ctx, sizeof(double) * 4 * cm.nranks), pc(ctx, sizeof(double) * k), win(ctx, sizeof(int));
+    zero_mat(ctx, S11.m);
+    DcArgs a{X.m.p, k, mg, row0, pos.d(), cn.d(), rn.d(), slots.d(), rec.d(), all.d(), pc.d(), S11.m.p, jr,
+             win.i(), cm.rank, cm.nranks};
+    dc_init_kernel<<<nblk, kDcThreads, 0, ctx.stream>>>(a);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    const size_t vsm = sizeof(double) * size_t(k);
+    if (vsm > 48 * 1024)
+        RLRA_CUDA(cudaFuncSetAttribute(dc_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsm)));
+    for (int f = 0; f < k; ++f) {
+        dc_record_kernel<<<1, 32, 0, ctx.stream>>>(a, nblk);
+        allgather(ctx, cm, a.rec, a.all, 4);
+        dc_select_kernel<<<1, 1024, 0, ctx.stream>>>(a, f);
+        allreduce(ctx, cm, a.pc, size_t(k));
+        dc_apply_kernel<<<nblk, kDcThreads, vsm, ctx.stream>>>(a, f);
+        RLRA_LAUNCH_CHECK();
+        ctx.launches += 3;
+    }
+    {
+        Buf sgn(ctx, sizeof(double) * k);
+        dc_sign_kernel<<<ceil_div(k, 256), 256, 0, ctx.stream>>>(S11.m.p, k, sgn.d());
+        dc_signfix_kernel<<<dc_blocks(ctx, int64_t(k) * (k + mg)), 256, 0, ctx.stream>>>(S11.m.p, X.m.p, k, mg,
+                                                                                        sgn.d());
+        RLRA_LAUNCH_CHECK();
+        ctx.launches += 2;
+    }
+    bool clamped = false;
+    if (mg > 0) clamped = upper_tri_solve(ctx, S11.m, X.m.block(0, 0, k, mg), T.m.block(0, 0, k, mg));
+    if (mg > 0) {
+        dc_interp_kernel<<<dc_blocks(ctx, int64_t(mg) * k), 256, 0, ctx.stream>>>(pos.d(), T.m.p, k, mg, Wg.p,
+                                                                                  Wg.ld);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+    }
+    return clamped;
+}
+
+// Y^T (n x l) = A^T Omega~ with A row-sharded: this rank's rows [row0,
+// row0 + m_g) of the m_total x l Omega~, summed over the ranks
+void sketch_left_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, int64_t m_total, int l,
+                            OmegaSource& om, const DMat& Yt) {
+    const int mg = int(A.rows), n = int(A.cols);
+    const int draw = om.next_draw++;
+    GemmTag tag(ctx, "gemm_sketch");
+    if (om.o->mode == RLRA_OMEGA_PHILOX) {
+        GemmOpts o;
+        o.philox_b = true;
+        o.seed = om.o->seed;
+        o.draw = draw;
+        o.krow0 = row0;
+        gemm(ctx, Op::T, Op::N, n, l, mg, 1.0, A.p, A.ld, nullptr, mg, 0.0, Yt.p, Yt.ld, o);
+    } else {
+        if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
+        std::vector<double> h(size_t(m_total) * l);
+        om.o->fill(om.o->user, draw, int(m_total), l, h.data());  // the same draw on every rank
+        DMatBuf Om(ctx, mg, l);
+        RLRA_CUDA(cudaMemcpy2DAsync(Om.m.p, sizeof(double) * Om.m.ld, h.data() + row0, sizeof(double) * m_total,
+                                    sizeof(double) * mg, l, cudaMemcpyHostToDevice, ctx.stream));
+        gemm(ctx, Op::T, Op::N, 1.0, A, Om.m, 0.0, Yt);
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    allreduce(ctx, cm, Yt.p, size_t(n) * l);
+}
+
+}  // namespace
+
+IdOut id_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, int64_t m_total, int k, int p,
+                         int q, int s, OmegaSource& om, int* jc, const DMat& V) {
+    const int n = int(A.cols), mg = int(A.rows), l = k + p;
+    DMatBuf Yt(ctx, n, l), Z(ctx, std::max(mg, 1), l), Y(ctx, l, n), S1(ctx, l, n);
+    sketch_left_rowsharded(ctx, cm, A, row0, m_total, l, om, Yt.m);  // sketch.hpp:65-67
+    const DMat Zm = Z.m.block(0, 0, mg, l);
+    {
+        GemmTag tag(ctx, "gemm_power");
+        for (int j = 1; j <= q; ++j) {
+            if ((2 * j - 2) % s == 0) orth_span_inplace(ctx, Yt.m);        // replicated n x l
+            gemm(ctx, Op::N, Op::N, 1.0, A, Yt.m, 0.0, Zm);                 // Z_g = A_g Yt (local)
+            if ((2 * j - 1) % s == 0) orth_rowsharded(ctx, cm, Zm, m_total, true);
+            gemm(ctx, Op::T, Op::N, 1.0, A, Zm, 0.0, Yt.m);                 // Yt = sum_g A_g^T Z_g
+            allreduce(ctx, cm, Yt.m.p, size_t(n) * l);
+        }
+    }
+    transpose_mat(ctx, Yt.m, Y.m);
+    pivoted_qr(ctx, Y.m, l, 0.0, nullptr, S1.m, jc);  // interp.hpp:209, replicated
+    IdOut out;
+    out.k = k;
+    {
+        Buf sq(ctx, sizeof(double));
+        sum_squares(ctx, S1.m.block(k, k, l - k, n - k), sq.d());  // interp.hpp:213
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        out.qr_residual = std::sqrt(ctx.h_scalars[0]);
+    }
+    DMatBuf T(ctx, k, std::max(1, n - k));
+    if (n > k)
+        out.clamped = upper_tri_solve(ctx, S1.m.block(0, 0, k, k), S1.m.block(0, k, k, n - k), T.m.block(0, 0, k, n - k));
+    build_interp(ctx, jc, T, n, k, V);
+    return out;
+}
+
+double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, int64_t m_total, int k, int p,
+                           int q, int s, OmegaSource& om, int* jc, const DMat& V, int* jr, const DMat& Wg,
+                           const DMat& Cg, const DMat& U, const DMat& R, IdOut* id_out) {
+    const int mg = int(A.rows), n = int(A.cols);
+    *id_out = id_rand_rowsharded(ctx, cm, A, row0, m_total, k, p, q, s, om, jc, V);  // interp.hpp:241
+    if (mg > 0) gather_cols(ctx, A, jc, k, Cg);                                       // C = A(:, Jc)
+    row_id_rowsharded(ctx, cm, Cg, row0, k, jr, Wg);                                  // id_row(C, k)
+    // R = A(Jr, :): the owners contribute their skeleton rows
+    gather_owned_rows_kernel<<<dc_blocks(ctx, int64_t(k) * n), 256, 0, ctx.stream>>>(A.p, A.ld, mg, n, jr, k, row0,
+                                                                                    R.p, R.ld);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    allreduce(ctx, cm, R.p, size_t(k) * n);
+    std::vector<int> jr_host(k);
+    RLRA_CUDA(cudaMemcpyAsync(jr_host.data(), jr, sizeof(int) * k, cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    cur_linkage(ctx, R, V, k, U, jr_host.data());  // replicated
+    // ||A - C U R||_F: local fused residual, scalar allreduce
+    double loc = 0.0;
+    if (mg > 0) {
+        DMatBuf UR(ctx, k, n);
+        gemm(ctx, Op::N, Op::N, 1.0, U, R, 0.0, UR);
+        Buf sq(ctx, sizeof(double));
+        GemmOpts o;
+        o.epi = EPI_RESID;
+        o.R = A.p;
+        o.ldr = A.ld;
+        o.resid_sq = sq.d();
+        gemm(ctx, Op::N, Op::N, mg, n, k, 1.0, Cg.p, Cg.ld, UR.m.p, UR.m.ld, 0.0, nullptr, 0, o);
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        loc = ctx.h_scalars[0];
+    }
+    return std::sqrt(allreduce_scalar(ctx, cm, loc));
 }
 
 }  // namespace rlra_b200

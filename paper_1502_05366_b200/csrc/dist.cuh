@@ -22,4 +22,19 @@ void comm_destroy(Comm& cm);
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
                         OmegaSource& om, const DMat& U, double* sigma, const DMat& V);
 
+// id_rand (interp.hpp:203-223) on the row-sharded A: jc (device, n) and V
+// (n x k) replicated.  Omega~ is m_total x l, this rank using rows
+// [row0, row0 + m_g).
+IdOut id_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, int64_t m_total, int k, int p,
+                         int q, int s, OmegaSource& om, int* jc, const DMat& V);
+
+// cur_rand (interp.hpp:240-244) on the row-sharded A: the column ID as above,
+// the row ID of C = A(:, Jc) by a column-pivoted QR whose pivot statistics
+// are allgathered every step, R = A(Jr, :) assembled by allreduce, the
+// linkage replicated.  jc, V, jr (global rows), U, R replicated; W_g and C_g
+// this rank's rows.  Returns ||A - C U R||_F.
+double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, int64_t m_total, int k, int p,
+                           int q, int s, OmegaSource& om, int* jc, const DMat& V, int* jr, const DMat& Wg,
+                           const DMat& Cg, const DMat& U, const DMat& R, IdOut* id_out);
+
 }  // namespace rlra_b200

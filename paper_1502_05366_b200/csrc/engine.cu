@@ -398,12 +398,10 @@ void two_sided_from_column(Context& ctx, const DMat& A, const int* jc, int k, in
     id_column(ctx, Ct, k, 0.0, jr, Wr);  // id_row(c, k) = id_column(c^T, k)
 }
 
-double cur_from_two_sided(Context& ctx, const DMat& A, const int* jc, const int* jr, const DMat& V,
-                          int k, const DMat& C, const DMat& U, const DMat& R, const int* jr_host) {
-    const int m = int(A.rows), n = int(A.cols);
-    gather_cols(ctx, A, jc, k, C);
-    gather_rows(ctx, A, jr, k, R);
-    // cur_linkage (interp.hpp:143-156): compact_qr(R^T), rank check, solve
+// cur_linkage (interp.hpp:143-156): U = argmin ||U R - V^T||_F via
+// compact_qr(R^T), the skeleton-row rank check, and a triangular solve
+void cur_linkage(Context& ctx, const DMat& R, const DMat& V, int k, const DMat& U, const int* jr_host) {
+    const int n = int(R.cols);
     DMatBuf Rt(ctx, n, k), Rh(ctx, k, k), X(ctx, k, k), T(ctx, k, k);
     transpose_mat(ctx, R, Rt);
     orth_inplace(ctx, Rt, &Rh.m);
@@ -423,6 +421,14 @@ double cur_from_two_sided(Context& ctx, const DMat& A, const int* jc, const int*
     gemm(ctx, Op::T, Op::N, 1.0, Rt, V, 0.0, X);  // Qhat^T V
     upper_tri_solve(ctx, Rh, X, T);
     transpose_mat(ctx, T, U);
+}
+
+double cur_from_two_sided(Context& ctx, const DMat& A, const int* jc, const int* jr, const DMat& V,
+                          int k, const DMat& C, const DMat& U, const DMat& R, const int* jr_host) {
+    const int m = int(A.rows), n = int(A.cols);
+    gather_cols(ctx, A, jc, k, C);
+    gather_rows(ctx, A, jr, k, R);
+    cur_linkage(ctx, R, V, k, U, jr_host);
     // ||A - C (U R)||_F, fused GEMM + subtract + sum of squares (K10)
     DMatBuf UR(ctx, k, n);
     gemm(ctx, Op::N, Op::N, 1.0, U, R, 0.0, UR);

@@ -76,6 +76,9 @@ void two_sided_from_column(Context& ctx, const DMat& A, const int* jc, int k, in
 double cur_from_two_sided(Context& ctx, const DMat& A, const int* jc, const int* jr, const DMat& V,
                           int k, const DMat& C, const DMat& U, const DMat& R, const int* jr_host);
 
+// interp.hpp:143-156 — U (k x k) from the skeleton rows R (k x n) and V (n x k)
+void cur_linkage(Context& ctx, const DMat& R, const DMat& V, int k, const DMat& U, const int* jr_host);
+
 // ||A||_F (device-side deterministic reduction, read back)
 double frobenius(Context& ctx, const DMat& A);
 

@@ -104,3 +104,82 @@ class NumpyBackend:
         t = torch.tensor([x], dtype=torch.float64)
         dist.all_reduce(t)
         return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# numpy mirror of csrc/dist.cu row_id_rowsharded (the distributed column-
+# pivoted QR of C^T whose columns -- the rows of C -- are sharded): the same
+# per-step record allgather, winner rule, position bookkeeping, allreduced
+# pivot column and reflector/downdate arithmetic, with gloo collectives.
+def _better(v, p, bv, bp):
+    return v > bv or (v == bv and p < bp)
+
+
+def row_id_rowsharded(Cg, row0, k):
+    """Returns (jr: k global pivot rows, W_g: this rank's rows of W)."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    X = np.array(Cg.T, dtype=np.float64, order="F")  # k x mg
+    mg = X.shape[1]
+    pos = np.arange(row0, row0 + mg, dtype=np.float64)
+    cn = (X * X).sum(0)
+    rn = cn.copy()
+    S11 = np.zeros((k, k))
+    jr = np.zeros(k, dtype=np.int64)
+    for f in range(k):
+        bv, bp, bj = -np.inf, np.inf, -1
+        for j in range(mg):
+            if pos[j] >= f and _better(cn[j], pos[j], bv, bp):
+                bv, bp, bj = cn[j], pos[j], j
+        rec = torch.tensor([bv if bj >= 0 else -np.inf, bp, row0 + bj if bj >= 0 else -1.0, float(bj)],
+                           dtype=torch.float64)
+        recs = [torch.zeros(4, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(recs, rec) if world > 1 else recs.__setitem__(0, rec)
+        wv, wp, wg, wj, wr = -np.inf, np.inf, -1, -1, -1
+        for r, q in enumerate(recs):
+            q = q.numpy()
+            if q[3] >= 0 and _better(q[0], q[1], wv, wp):
+                wv, wp, wg, wj, wr = q[0], q[1], q[2], int(q[3]), r
+        jr[f] = int(wg)
+        me = dist.get_rank() if world > 1 else 0
+        pc = torch.tensor(X[:, wj] if wr == me else np.zeros(k), dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(pc)
+        pc = pc.numpy()
+        pos[pos == f] = wp
+        if wr == me:
+            pos[wj] = f
+        norm2 = float(np.sum(pc[f:] ** 2))
+        x1, norm = pc[f], np.sqrt(norm2)
+        zero = norm < 1e-300
+        alpha = -norm if x1 >= 0 else norm
+        beta = 0.0 if zero else 2.0 / (2.0 * (norm2 - alpha * x1))
+        alpha = 0.0 if zero else alpha
+        v = np.zeros(k)
+        v[f] = pc[f] - (alpha if beta != 0.0 else 0.0)
+        v[f + 1:] = pc[f + 1:]
+        S11[:f, f] = pc[:f]
+        S11[f, f] = alpha
+        for j in range(mg):
+            if wr == me and j == wj:
+                X[f, j] = alpha
+                X[f + 1:, j] = 0.0
+                continue
+            if pos[j] <= f:
+                continue
+            if beta != 0.0:
+                X[f:, j] -= beta * float(v[f:] @ X[f:, j]) * v[f:]
+            c = cn[j] - X[f, j] ** 2
+            if c < 1e-6 * rn[j]:
+                c = float(np.sum(X[f + 1:, j] ** 2))
+                rn[j] = c
+            cn[j] = c
+    sg = np.where(np.diag(S11) < 0, -1.0, 1.0)
+    S11 = S11 * sg[:, None]
+    X = X * sg[:, None]
+    T = np.linalg.solve(S11, X) if mg else X
+    if np.max(np.abs(np.diag(S11))) / np.min(np.abs(np.diag(S11))) > 1e12:
+        T = np.clip(T, -1e4, 1e4)
+    W = np.zeros((mg, k))
+    for j in range(mg):
+        W[j] = np.eye(k)[int(pos[j])] if pos[j] < k else T[:, j]
+    return jr, W

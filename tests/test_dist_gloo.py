@@ -86,3 +86,48 @@ def test_rowsharded_rsvd_world2_matches_world1(tmp_path):
     assert np.linalg.norm(a - Q2 @ (Q2.T @ a)) <= 1e-12 * np.linalg.norm(a)
     # the exchanges are the small ones: Gram and n x l partials only
     assert int(parts[0]["allreduces"]) > 0
+
+
+def _rowid_worker(rank, world, port, m, k, out_dir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from _dist_numpy import row_id_rowsharded
+
+    rs = np.random.default_rng(3)
+    c = rs.standard_normal((m, k)) * np.exp(-np.arange(k) / 4.0)  # graded, distinct pivot gaps
+    bounds = np.linspace(0, m, world + 1).astype(int)
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    jr, W = row_id_rowsharded(c[r0:r1], r0, k)
+    np.savez(os.path.join(out_dir, f"rid{rank}.npz"), jr=jr, W=W, c=c)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_rowsharded_row_id_pivot_statistics_match_oracle(tmp_path, world):
+    """The distributed column-pivoted QR behind the sharded CUR (csrc/dist.cu
+    row_id_rowsharded, mirrored in numpy over gloo): allgathered pivot
+    statistics and position bookkeeping reproduce the reference's pivots and
+    interpolation matrix of id_row(C, k) for any row partition."""
+    import _oracle
+
+    m, k = 90, 12
+    port = _free_port()
+    mp.spawn(_rowid_worker, args=(world, port, m, k, str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(os.path.join(tmp_path, f"rid{r}.npz")) for r in range(world)]
+    jr = parts[0]["jr"]
+    for x in parts[1:]:
+        assert np.array_equal(x["jr"], jr)  # replicated decision
+    W = np.vstack([x["W"] for x in parts])
+    c = parts[0]["c"]
+    orc = _oracle.orc()
+    ref = orc.id_column(np.asfortranarray(c.T), k)  # id_row(c, k) = id_column(c^T, k)
+    assert np.array_equal(jr, ref["jc"][:k])
+    assert np.max(np.abs(W - ref["v"])) <= 1e-10

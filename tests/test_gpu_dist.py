@@ -103,3 +103,40 @@ def test_native_rowsharded_row_permutation_invariance():
         comm.close()
     s1, s2 = S1.t.cpu().numpy(), S2.t.cpu().numpy()
     assert np.max(np.abs(s1 - s2) / s1) <= 1e-10
+
+
+def _world1_comm(eng):
+    from paper_1502_05366_b200 import dist as D
+
+    return D.NcclComm(eng)
+
+
+@pytest.mark.parametrize("m,n,k,p", [(1500, 900, 60, 10), (3000, 1200, 120, 10)])
+def test_native_rowsharded_id_cur_world1_match_engine_and_oracle(orc, m, n, k, p):
+    """The row-sharded ID/CUR driver (csrc/dist.cu) on a 1-rank NCCL
+    communicator: the distributed column-pivoted QR of C^T (allgathered pivot
+    statistics, allreduced pivot column, positions tracked instead of column
+    swaps) picks the reference's skeleton rows; jc/jr identical to the oracle
+    with the reference's Omega injected."""
+    from helpers import make_test_matrix, rel_fro
+
+    eng = R.Engine(0)
+    a = make_test_matrix(m, n, 10.0 ** (-8.0 * np.arange(min(m, n) // 2) / (min(m, n) // 2)), seed=11)
+    comm = _world1_comm(eng)
+    try:
+        idg = eng.id_rand_rowsharded(comm.handle, a, 0, m, k, p, 2, 1, rng=R.Rng(12345))
+        cg = eng.cur_rand_rowsharded(comm.handle, a, 0, m, k, p, 2, 1, rng=R.Rng(12345))
+    finally:
+        comm.close()
+    ido = orc.id_rand(a, k, p, 2, 1, orc.rng(12345))
+    co = orc.cur_rand(a, k, p, 2, 1, orc.rng(12345))
+    np.testing.assert_array_equal(idg["jc"][:k], ido["jc"][:k])
+    assert rel_fro(idg["v"], ido["v"]) <= 1e-8
+    np.testing.assert_array_equal(cg["jc"][:k], co["jc"][:k])
+    np.testing.assert_array_equal(cg["jr"], co["jr"][:k])
+    assert abs(cg["residual"] - co["residual"]) <= 1e-6 * co["residual"] + 1e-12
+    np.testing.assert_array_equal(cg["c"], a[:, cg["jc"][:k]])
+    np.testing.assert_array_equal(cg["r"], a[cg["jr"], :])
+    assert rel_fro(cg["u"], co["u"]) <= 1e-6
+    # W: skeleton rows are exactly the identity
+    np.testing.assert_array_equal(cg["w"][cg["jr"], :], np.eye(k))
