@@ -119,6 +119,30 @@ rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap,
 void* rlra_ctx_stream(const rlra_ctx* ctx);
 const char* rlra_last_error(void);
 
+/* ------------------------------------------- I/O, generator, verifier ---
+ * Binary matrix files in the reference format (io.hpp:40-109): int32 rows,
+ * int32 cols (little-endian), then rows*cols doubles row by row; exactly
+ * 8 + 8*rows*cols bytes; every value finite.  Errors are RLRA_EIO with the
+ * reference's messages.  rlra_load_binary reads rows [row0, row0 + rows) — a
+ * row shard — into a column-major (host or device) buffer, transposing on the
+ * GPU as the chunks stream in. */
+rlra_status rlra_binary_header(const char* path, int* rows, int* cols);
+rlra_status rlra_load_binary(rlra_ctx* ctx, int loc, const char* path, int64_t row0, int rows, double* a, int64_t lda);
+rlra_status rlra_save_binary(rlra_ctx* ctx, int loc, const char* path, const double* a, int m, int n, int64_t lda);
+/* gen_test_matrix (testmat.hpp:65-74): A = U diag(sigma[0..r)) V^T + noise*G
+ * with U, V orthonormalised Philox Gaussians of `seed` (not the reference's
+ * RngState bits; the spectrum is what the configs specify). */
+rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const double* sigma, int r, uint64_t seed,
+                                 double noise, double* a, int64_t lda);
+/* verify(a, SvdFactors, sigma_true) (report.hpp:97-138): out[0] relative
+ * Frobenius error, out[1] relative spectral error (60-step power estimates,
+ * start vectors from RngState 0x5bd1e995 as the reference), out[2..4] the
+ * Frobenius floor, spectral floor and sketch bound (NaN without sigma_true,
+ * r = 0). */
+rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* u,
+                            int64_t ldu, const double* sigma, const double* v, int64_t ldv, int k,
+                            const double* sigma_true, int r, double out[5]);
+
 /* ------------------------------------------------- row-sharded multi-GPU ---
  * One process (one rlra_ctx) per GPU; A (m_total x n) split by rows.  The
  * collectives are NCCL (loaded at run time from libnccl.so.2) on the context

@@ -273,4 +273,39 @@ int ref_two_sided_from_column(const double* a, int m, int n, const int* jc, cons
     });
 }
 
+// report.hpp verify(a, SvdFactors, sigma_true): out = rel_fro, rel_spec,
+// fro_floor, spec_floor, spec_bound
+int ref_verify_svd(const double* a, int m, int n, const double* u, const double* sigma, const double* v, int k,
+                   const double* sigma_true, int r, double* out) {
+    return guard([&] {
+        rlra::SvdFactors f;
+        f.u = wrap(u, m, k);
+        f.v = wrap(v, n, k);
+        f.sigma.assign(sigma, sigma + k);
+        f.k = k;
+        std::vector<double> st;
+        if (r > 0) st.assign(sigma_true, sigma_true + r);
+        rlra::ErrorReport rep = rlra::verify(wrap(a, m, n), f, st);
+        out[0] = rep.rel_frobenius_error;
+        out[1] = rep.rel_spectral_error;
+        out[2] = rep.fro_floor;
+        out[3] = rep.spec_floor;
+        out[4] = rep.spec_bound;
+    });
+}
+
+// io.hpp save_binary / load_binary (row-major file <-> column-major buffer)
+int ref_save_binary(const char* path, const double* a, int m, int n) {
+    return guard([&] { rlra::save_binary(path, wrap(a, m, n)); });
+}
+
+int ref_load_binary(const char* path, int* rows, int* cols, double* out) {
+    return guard([&] {
+        rlra::DenseMatrix A = rlra::load_binary(path);
+        *rows = A.rows();
+        *cols = A.cols();
+        if (out) put(A, out);
+    });
+}
+
 }  // extern "C"

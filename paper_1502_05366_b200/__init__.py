@@ -601,6 +601,57 @@ class Engine:
                                               C.byref(res), C.byref(qres)))
         return dict(jc=jc, jr=jr, v=v, w=w, c=c, u=u, r=r, k=k, residual=res.value, qr_residual=qres.value)
 
+    # -- binary I/O, generator, verifier (csrc/io.cu) ---------------------------
+    @staticmethod
+    def binary_header(path):
+        """(rows, cols) of a reference-format binary file (io.hpp:66-93 checks)."""
+        r, c = C.c_int(0), C.c_int(0)
+        _check(lib().rlra_binary_header(os.fsencode(path), C.byref(r), C.byref(c)))
+        return r.value, c.value
+
+    def load_binary(self, path, row0=0, rows=None):
+        """Rows [row0, row0 + rows) of the file as a column-major array."""
+        m, n = self.binary_header(path)
+        rows = m - row0 if rows is None else rows
+        out = np.zeros((rows, n), order="F")
+        _check(lib().rlra_load_binary(self._ctx, HOST, os.fsencode(path), _i64(row0), rows, _d(out),
+                                      _i64(max(1, rows))))
+        return out
+
+    def device_load_binary(self, path, row0, rows, out_ptr, ld):
+        _check(lib().rlra_load_binary(self._ctx, DEVICE, os.fsencode(path), _i64(row0), rows,
+                                      C.c_void_p(out_ptr), _i64(ld)))
+
+    def save_binary(self, path, a):
+        a = _F(a)
+        m, n = a.shape
+        _check(lib().rlra_save_binary(self._ctx, HOST, os.fsencode(path), _d(a), m, n, _i64(_ld(a))))
+
+    def gen_test_matrix(self, m, n, sigma, seed, noise=0.0):
+        sg = np.ascontiguousarray(sigma, dtype=np.float64)
+        out = np.zeros((m, n), order="F")
+        _check(lib().rlra_gen_test_matrix(self._ctx, HOST, m, n, _d(sg), len(sg), C.c_uint64(seed),
+                                          C.c_double(noise), _d(out), _i64(max(1, m))))
+        return out
+
+    def device_gen_test_matrix(self, m, n, sigma, seed, noise, out_ptr, ld):
+        sg = np.ascontiguousarray(sigma, dtype=np.float64)
+        _check(lib().rlra_gen_test_matrix(self._ctx, DEVICE, m, n, _d(sg), len(sg), C.c_uint64(seed),
+                                          C.c_double(noise), C.c_void_p(out_ptr), _i64(ld)))
+
+    def verify_svd(self, a, u, s, v, sigma_true=None):
+        """report.hpp verify(a, SvdFactors, sigma_true)."""
+        a, u, v = _F(a), _F(u), _F(v)
+        m, n = a.shape
+        k = u.shape[1]
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        st = np.ascontiguousarray(sigma_true if sigma_true is not None else np.zeros(0), dtype=np.float64)
+        out = np.zeros(5)
+        _check(lib().rlra_verify_svd(self._ctx, HOST, _d(a), m, n, _i64(_ld(a)), _d(u), _i64(max(1, m)), _d(s),
+                                     _d(v), _i64(max(1, n)), k, _d(st) if len(st) else None, len(st), _d(out)))
+        return dict(rel_frobenius_error=out[0], rel_spectral_error=out[1], fro_floor=out[2],
+                    spec_floor=out[3], spec_bound=out[4])
+
     def host_rsvd_ptr(self, variant, a_ptr, m, n, lda, k, p, q, s, omega, u_ptr, sigma_ptr, v_ptr):
         """rlra_rsvd with HOST pointers (pinned or pageable): the drop-in call
         a reference user makes, H2D/D2H inside the call."""

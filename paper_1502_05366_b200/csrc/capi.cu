@@ -16,6 +16,7 @@
 
 #include "dist.cuh"
 #include "engine.cuh"
+#include "io.cuh"
 #include "gemm.cuh"
 #include "jacobi.cuh"
 #include "qr.cuh"
@@ -551,6 +552,76 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
         V.finish(C);
         S.finish(C);
         sync(C);
+    });
+}
+
+rlra_status rlra_binary_header(const char* path, int* rows, int* cols) {
+    try {
+        if (!path || !rows || !cols) raise(RLRA_EINVAL, "null argument to rlra_binary_header");
+        const BinaryHeader h = read_binary_header(path);
+        *rows = h.rows;
+        *cols = h.cols;
+        return RLRA_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<rlra_status>(e.status);
+    }
+}
+
+rlra_status rlra_load_binary(rlra_ctx* ctx, int loc, const char* path, int64_t row0, int rows, double* a,
+                             int64_t lda) {
+    return guard(ctx, [&](Context& C) {
+        need(path, "path");
+        const BinaryHeader h = read_binary_header(path);
+        Out A(C, loc, a, rows, h.cols, lda, "a");
+        load_binary_rows(C, path, row0, A.m);
+        A.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_save_binary(rlra_ctx* ctx, int loc, const char* path, const double* a, int m, int n, int64_t lda) {
+    return guard(ctx, [&](Context& C) {
+        need(path, "path");
+        if (m <= 0 || n <= 0) raise(RLRA_EDIM, fmt("save_binary: %dx%d matrix", m, n));
+        In A(C, loc, a, m, n, lda, "a");
+        save_binary(C, path, A.m);
+    });
+}
+
+rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const double* sigma, int r, uint64_t seed,
+                                 double noise, double* a, int64_t lda) {
+    return guard(ctx, [&](Context& C) {
+        if (r < 0 || r > std::min(m, n)) raise(RLRA_EDIM, fmt("gen_test_matrix: %d singular values for %dx%d", r, m, n));
+        if (r > 0) need(sigma, "sigma");
+        Out A(C, loc, a, m, n, lda, "a");
+        gen_test_matrix(C, std::vector<double>(sigma, sigma + r), seed, noise, A.m);
+        A.finish(C);
+        sync(C);
+    });
+}
+
+rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* u,
+                            int64_t ldu, const double* sigma, const double* v, int64_t ldv, int k,
+                            const double* sigma_true, int r, double out[5]) {
+    return guard(ctx, [&](Context& C) {
+        need(out, "out");
+        if (k < 0 || k > std::min(m, n)) raise(RLRA_EDIM, "verify: SVD factor shapes do not match the matrix");
+        In A(C, loc, a, m, n, lda, "a"), U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
+        Buf sd(C, sizeof(double) * std::max(k, 1));
+        if (k > 0) {
+            need(sigma, "sigma");
+            RLRA_CUDA(cudaMemcpyAsync(sd.p, sigma, sizeof(double) * k,
+                                      loc == RLRA_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, C.stream));
+        }
+        std::vector<double> st;
+        if (r > 0) st.assign(sigma_true, sigma_true + r);
+        const VerifyReport rep = verify_svd(C, A.m, U.m, sd.d(), V.m, k, st);
+        out[0] = rep.rel_frobenius_error;
+        out[1] = rep.rel_spectral_error;
+        out[2] = rep.fro_floor;
+        out[3] = rep.spec_floor;
+        out[4] = rep.spec_bound;
     });
 }
 
