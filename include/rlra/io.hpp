@@ -1,0 +1,4 @@
+// Drop-in forwarding header: the reference include path rlra/io.hpp maps onto
+// the B200 engine API (include/rlra/rlra.hpp).
+#pragma once
+#include "rlra/rlra.hpp"

@@ -29,6 +29,7 @@
 #include <initializer_list>
 #include <numeric>
 #include <stdexcept>
+#include <limits>
 #include <string>
 #include <utility>
 #include <vector>
@@ -723,6 +724,103 @@ inline IdFactors id_from_qb(const QbFactors& qb, const DenseMatrix& a, int k) {
 inline CurFactors cur_rand(const DenseMatrix& a, int k, int p, int q_power, int s, RngState& rng) {
     IdFactors col = id_rand(a, k, p, q_power, s, rng);
     return detail::cur_from_two_sided(a, detail::two_sided_from_column(a, std::move(col)));
+}
+
+// ---------------------------------------------------------------- io.hpp ---
+// Binary matrix files (io.hpp:40-109): same format, validation and messages;
+// the engine streams the rows through the GPU (csrc/io.cu).
+inline void save_binary(const std::string& path, const DenseMatrix& a) {
+    detail::check(rlra_save_binary(detail::ctx(), RLRA_HOST, path.c_str(), a.data(), a.rows(), a.cols(), detail::ld(a)));
+}
+inline DenseMatrix load_binary(const std::string& path) {
+    int m = 0, n = 0;
+    detail::check(rlra_binary_header(path.c_str(), &m, &n));
+    DenseMatrix a(m, n);
+    detail::check(rlra_load_binary(detail::ctx(), RLRA_HOST, path.c_str(), 0, m, a.data(), detail::ld(a)));
+    return a;
+}
+
+// ----------------------------------------------------------- testmat.hpp ---
+struct SpectrumSpec {  // testmat.hpp:16-53
+    enum class Kind { kTypeI, kTypeII, kTypeIII, kCustom };
+    Kind kind = Kind::kTypeII;
+    std::vector<double> custom_exponents;
+    static SpectrumSpec type_i() { return {Kind::kTypeI, {}}; }
+    static SpectrumSpec type_ii() { return {Kind::kTypeII, {}}; }
+    static SpectrumSpec type_iii() { return {Kind::kTypeIII, {}}; }
+    static SpectrumSpec custom(std::vector<double> exponents) {
+        for (std::size_t i = 0; i + 1 < exponents.size(); ++i)
+            if (exponents[i] < exponents[i + 1])
+                throw DimensionError("SpectrumSpec: custom exponents must be nonincreasing");
+        return {Kind::kCustom, std::move(exponents)};
+    }
+    std::vector<double> sigma(int r) const {
+        if (r < 1) throw DimensionError("SpectrumSpec: rank must be positive");
+        std::vector<double> exps;
+        if (kind == Kind::kCustom) {
+            if (int(custom_exponents.size()) != r)
+                throw DimensionError(detail::msg("SpectrumSpec: %zu custom exponents for rank %d",
+                                                 custom_exponents.size(), r));
+            exps = custom_exponents;
+        } else {
+            const double end = kind == Kind::kTypeI ? -0.5 : kind == Kind::kTypeII ? -2.0 : -3.5;
+            exps.resize(std::size_t(r));
+            if (r == 1)
+                exps[0] = end;
+            else
+                for (int j = 0; j < r; ++j) exps[std::size_t(j)] = end * double(j) / (r - 1);
+        }
+        std::vector<double> sv(static_cast<std::size_t>(r));
+        for (int j = 0; j < r; ++j) sv[std::size_t(j)] = std::pow(10.0, exps[std::size_t(j)]);
+        return sv;
+    }
+};
+struct TestMatrix {
+    DenseMatrix a;
+    std::vector<double> sigma_true;
+};
+// testmat.hpp:65-74 semantics on the GPU: U, V are orthonormalised Philox
+// Gaussians keyed by one draw of `rng` (not the reference's RngState bits;
+// the spectrum is exact).
+inline TestMatrix gen_test_matrix(int m, int n, const SpectrumSpec& spec, RngState& rng) {
+    TestMatrix out;
+    out.sigma_true = spec.sigma(std::min(m, n));
+    out.a = DenseMatrix(m, n);
+    detail::check(rlra_gen_test_matrix(detail::ctx(), RLRA_HOST, m, n, out.sigma_true.data(),
+                                       int(out.sigma_true.size()), rng.next_u64(), 0.0, out.a.data(),
+                                       detail::ld(out.a)));
+    return out;
+}
+
+// ------------------------------------------------------------ report.hpp ---
+struct ErrorReport {  // report.hpp:73-93 (numeric fields)
+    std::string method;
+    int m = 0, n = 0, k = 0;
+    double rel_frobenius_error = 0.0;
+    double rel_spectral_error = 0.0;
+    double fro_floor = std::numeric_limits<double>::quiet_NaN();
+    double spec_floor = std::numeric_limits<double>::quiet_NaN();
+    double spec_bound = std::numeric_limits<double>::quiet_NaN();
+};
+inline ErrorReport verify(const DenseMatrix& a, const SvdFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.u.rows() != a.rows() || f.v.rows() != a.cols() || f.u.cols() != f.k || f.v.cols() != f.k ||
+        int(f.sigma.size()) != f.k)
+        throw DimensionError("verify: SVD factor shapes do not match the matrix");
+    double out[5];
+    detail::check(rlra_verify_svd(detail::ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), detail::ld(a), f.u.data(),
+                                  detail::ld(f.u), f.sigma.data(), f.v.data(), detail::ld(f.v), f.k,
+                                  sigma_true.empty() ? nullptr : sigma_true.data(), int(sigma_true.size()), out));
+    ErrorReport r;
+    r.method = "svd";
+    r.m = a.rows();
+    r.n = a.cols();
+    r.k = f.k;
+    r.rel_frobenius_error = out[0];
+    r.rel_spectral_error = out[1];
+    r.fro_floor = out[2];
+    r.spec_floor = out[3];
+    r.spec_bound = out[4];
+    return r;
 }
 
 }  // namespace rlra

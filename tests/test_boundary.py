@@ -98,8 +98,16 @@ def test_cpp_dropin_headers_compile(tmp_path):
     if not shutil.which("g++"):
         pytest.skip("no g++")
     src = tmp_path / "t.cpp"
-    src.write_text('#include "rlra/rlra.hpp"\nint main(){ rlra::DenseMatrix a(3,2); rlra::RngState r(1);'
-                   ' (void)a; (void)r; return 0; }\n')
+    src.write_text(
+        '#include "rlra/rlra.hpp"\n#include "rlra/io.hpp"\n#include "rlra/testmat.hpp"\n'
+        '#include "rlra/report.hpp"\n#include "rlra/rsvd.hpp"\n#include "rlra/interp.hpp"\n'
+        'int main(){ rlra::RngState r(1);\n'
+        '  rlra::TestMatrix t = rlra::gen_test_matrix(40, 30, rlra::SpectrumSpec::type_ii(), r);\n'
+        '  rlra::SvdFactors f = rlra::rsvd_v2(t.a, 5, 5, 1, 1, r);\n'
+        '  rlra::ErrorReport e = rlra::verify(t.a, f, t.sigma_true);\n'
+        '  rlra::save_binary("x.bin", t.a); rlra::DenseMatrix b = rlra::load_binary("x.bin");\n'
+        '  rlra::CurFactors c = rlra::cur_rand(b, 3, 2, 1, 1, r);\n'
+        '  (void)e; (void)c; return 0; }\n')
     res = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
                           str(src)], capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
