@@ -178,6 +178,16 @@ rlra_status rlra_cur_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, co
                                      const rlra_omega* omega, int* jc, int* jr, double* v, int64_t ldv, double* w,
                                      int64_t ldw, double* c, int64_t ldc, double* u, int64_t ldu, double* r,
                                      int64_t ldr, double* residual, double* qr_residual);
+/* qb_blocked (qb.hpp:98-152) with W row-sharded (this rank's m_local rows;
+ * destroyed when inplace on the device, else copied): q (m_local x cap) this
+ * rank's rows of Q, b (cap x n) replicated; ell, residual history, final
+ * residual and tolerance flag as rlra_qb_blocked.  rlra_svd_from_qb on
+ * (q, b) with m = m_local then yields this rank's rows of U. */
+rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, double* a, int m_local, int n,
+                                       int64_t lda, int64_t m_total, int inplace, int blk, int num_blocks,
+                                       double tol, int q_power, int reorth_period, const rlra_omega* omega,
+                                       double* q, int64_t ldq, double* b, int64_t ldb, int cap, int* ell,
+                                       double* hist, int* nhist, double* final_residual, int* reached);
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,

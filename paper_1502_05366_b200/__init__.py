@@ -581,6 +581,27 @@ class Engine:
                                              _i64(max(1, n)), C.byref(res), C.byref(cl)))
         return dict(jc=jc, v=v, k=k, qr_residual=res.value, clamped=bool(cl.value))
 
+    def qb_blocked_rowsharded(self, comm, a_local, m_total, b, num_blocks, tol, q_power, reorth_period,
+                              rng=None, omega=None):
+        """rlra_qb_blocked_rowsharded with host buffers: Q rows of this rank,
+        B replicated."""
+        a = _F(a_local)
+        mg, n = a.shape
+        om = _omega(omega, rng, substream=True).struct()
+        cap = int(min(b * num_blocks, min(m_total, n)))
+        q = np.zeros((mg, max(cap, 1)), order="F")
+        bb = np.zeros((max(cap, 1), n), order="F")
+        hist = np.zeros(max(num_blocks, 1))
+        ell, nh, reached = C.c_int(0), C.c_int(0), C.c_int(0)
+        fin = C.c_double(0)
+        _check(lib().rlra_qb_blocked_rowsharded(self._ctx, comm, HOST, _d(a), mg, n, _i64(_ld(a)), _i64(m_total), 0,
+                                                b, num_blocks, C.c_double(tol), q_power, reorth_period,
+                                                C.byref(om), _d(q), _i64(max(1, mg)), _d(bb), _i64(max(cap, 1)), cap,
+                                                C.byref(ell), _d(hist), C.byref(nh), C.byref(fin), C.byref(reached)))
+        e = ell.value
+        return dict(q=q[:, :e], b=bb[:e], ell=e, history=list(hist[: nh.value]), final_residual=fin.value,
+                    tolerance_reached=bool(reached.value))
+
     def cur_rand_rowsharded(self, comm, a_local, row0, m_total, k, p, q_power, s, rng=None, omega=None):
         """rlra_cur_rand_rowsharded with host buffers (this rank's rows)."""
         a = _F(a_local)

@@ -662,6 +662,55 @@ rlra_status rlra_comm_destroy(rlra_comm* comm) {
     return RLRA_OK;
 }
 
+rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, double* a, int m_local, int n,
+                                       int64_t lda, int64_t m_total, int inplace, int blk, int num_blocks,
+                                       double tol, int q_power, int reorth_period, const rlra_omega* omega,
+                                       double* q, int64_t ldq, double* b, int64_t ldb, int cap, int* ell,
+                                       double* hist, int* nhist, double* final_residual, int* reached) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        if (m_total < m_local || m_total > INT32_MAX)
+            raise(RLRA_EDIM, fmt("qb_blocked_rowsharded: m_total %lld, local rows %d", (long long)m_total, m_local));
+        if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
+        if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
+        if (tol < 0.0) raise(RLRA_EDIM, fmt("tol must be >= 0 (got %g)", tol));
+        if (q_power < 0) raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
+        if (reorth_period < 1) raise(RLRA_EDIM, fmt("reorth_period must be >= 1 (got %d)", reorth_period));
+        const int64_t need_cap = std::min<int64_t>(int64_t(blk) * num_blocks, std::min<int64_t>(m_total, n));
+        if (cap < need_cap)
+            raise(RLRA_EINVAL, fmt("qb_blocked: capacity %d < min(b*M, min(m,n)) = %lld", cap, (long long)need_cap));
+        OmegaSource om = omega_of(omega);
+        DMatBuf Wown;
+        DMat W;
+        if (loc == RLRA_DEVICE && inplace) {
+            need(a, "a");
+            W.p = a;
+            W.rows = m_local;
+            W.cols = n;
+            W.ld = lda;
+        } else {
+            In A(C, loc, a, m_local, n, lda, "a");
+            Wown = DMatBuf(C, m_local, n);
+            copy_mat(C, A.m, Wown);
+            W = Wown.m;
+            sync(C);
+        }
+        Out Q(C, loc, q, m_local, cap, ldq, "q"), B(C, loc, b, cap, n, ldb, "b");
+        QbOut r = qb_blocked_rowsharded(C, comm->c, W, m_total, blk, num_blocks, tol, q_power, reorth_period, om,
+                                        Q.m, B.m);
+        if (Q.host && r.ell > 0) d2h_mat(C, Q.m.block(0, 0, m_local, r.ell), Q.host, Q.ldh);
+        if (B.host && r.ell > 0) d2h_mat(C, B.m.block(0, 0, r.ell, n), B.host, B.ldh);
+        if (loc == RLRA_HOST && inplace) d2h_mat(C, W, a, lda);
+        sync(C);
+        if (ell) *ell = r.ell;
+        if (nhist) *nhist = int(r.hist.size());
+        if (hist)
+            for (size_t i = 0; i < r.hist.size(); ++i) hist[i] = r.hist[i];
+        if (final_residual) *final_residual = r.final_residual;
+        if (reached) *reached = r.reached ? 1 : 0;
+    });
+}
+
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,

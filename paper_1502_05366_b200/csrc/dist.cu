@@ -621,4 +621,75 @@ double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, 
     return std::sqrt(allreduce_scalar(ctx, cm, loc));
 }
 
+
+QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_total, int blk, int num_blocks,
+                            double tol, int q_power, int reorth_period, OmegaSource& om, const DMat& Q,
+                            const DMat& B) {
+    const int mg = int(W.rows), n = int(W.cols);
+    const int rmax = int(std::min<int64_t>(m_total, n));
+    QbOut out;
+    Buf sq(ctx, sizeof(double));
+    auto global_fro = [&](double local_sq) { return std::sqrt(allreduce_scalar(ctx, cm, local_sq)); };
+    sum_squares(ctx, W, sq.d());
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    double resid = global_fro(ctx.h_scalars[0]);
+    DMatBuf Z(ctx, n, blk), P(ctx, std::max(1, int(Q.cols)), blk);
+    for (int i = 1; i <= num_blocks; ++i) {  // qb.hpp:116-142
+        const int width = std::min(blk, rmax - out.ell);
+        if (width < 1) break;
+        const DMat Qi = Q.block(0, out.ell, mg, width);
+        const DMat Zi = Z.m.block(0, 0, n, width);
+        const bool reorth = (i % reorth_period == 0);
+        sketch(ctx, Op::N, W, width, om, Qi);  // W_g Omega_i (the same Omega on every rank)
+        orth_rowsharded(ctx, cm, Qi, m_total, q_power > 0 || reorth);
+        for (int j = 0; j < q_power; ++j) {
+            gemm(ctx, Op::T, Op::N, 1.0, W, Qi, 0.0, Zi);
+            allreduce(ctx, cm, Zi.p, size_t(n) * width);
+            orth_span_inplace(ctx, Zi);  // replicated
+            gemm(ctx, Op::N, Op::N, 1.0, W, Zi, 0.0, Qi);
+            orth_rowsharded(ctx, cm, Qi, m_total, j + 1 < q_power || reorth);
+        }
+        if (reorth) {  // qb.hpp:126-130
+            if (out.ell > 0) {
+                const DMat Qp = Q.block(0, 0, mg, out.ell);
+                const DMat Pi = P.m.block(0, 0, out.ell, width);
+                gemm(ctx, Op::T, Op::N, 1.0, Qp, Qi, 0.0, Pi);
+                allreduce(ctx, cm, Pi.p, size_t(out.ell) * width);  // Q^T Q_i, l x b
+                gemm(ctx, Op::N, Op::N, -1.0, Qp, Pi, 1.0, Qi);
+            }
+            orth_rowsharded(ctx, cm, Qi, m_total, false);
+        }
+        const DMat Bi = B.block(out.ell, 0, width, n);
+        gemm(ctx, Op::T, Op::N, 1.0, Qi, W, 0.0, Bi);  // B_i = sum_g Q_i,g^T W_g
+        {
+            // B_i lives inside B (ld = cap): reduce through a contiguous copy
+            DMatBuf Bc(ctx, width, n);
+            copy_mat(ctx, Bi, Bc.m);
+            allreduce(ctx, cm, Bc.m.p, size_t(width) * n);
+            copy_mat(ctx, Bc.m, Bi);
+        }
+        // W_g <- W_g - Q_i,g B_i and ||W_g||^2 in one pass, then the sum over ranks
+        GemmOpts o;
+        o.epi = EPI_RESID;
+        o.R = W.p;
+        o.ldr = W.ld;
+        o.resid_sq = sq.d();
+        gemm(ctx, Op::N, Op::N, mg, n, width, 1.0, Qi.p, Qi.ld, Bi.p, Bi.ld, 0.0, W.p, W.ld, o);
+        out.ell += width;
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        resid = global_fro(ctx.h_scalars[0]);
+        out.hist.push_back(resid);
+        if (tol > 0.0 && resid < tol) {
+            out.final_residual = resid;
+            out.reached = true;
+            return out;
+        }
+    }
+    out.final_residual = resid;
+    out.reached = !(tol > 0.0);
+    return out;
+}
+
 }  // namespace rlra_b200

@@ -37,4 +37,13 @@ double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, 
                            int q, int s, OmegaSource& om, int* jc, const DMat& V, int* jr, const DMat& Wg,
                            const DMat& Cg, const DMat& U, const DMat& R, IdOut* id_out);
 
+// qb_blocked (qb.hpp:98-142) on the row-sharded W (destroyed: left as the
+// residual rows): Q (m_g x cap) row-sharded, B (cap x n) replicated.  The
+// exchanges: the b x b CholQR Grams, n x b power partials, the l x b
+// re-orthogonalisation projection, the b x n block B_i, and ||W||^2.
+// svd_from_qb on (Q_g, B) then gives U_g, sigma, V (the lift is local).
+QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_total, int blk, int num_blocks,
+                            double tol, int q_power, int reorth_period, OmegaSource& om, const DMat& Q,
+                            const DMat& B);
+
 }  // namespace rlra_b200

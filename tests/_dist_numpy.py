@@ -183,3 +183,54 @@ def row_id_rowsharded(Cg, row0, k):
     for j in range(mg):
         W[j] = np.eye(k)[int(pos[j])] if pos[j] < k else T[:, j]
     return jr, W
+
+
+# numpy mirror of csrc/dist.cu qb_blocked_rowsharded (qb.hpp:98-142 on a
+# row-sharded W): the collectives are the b x b Gram (inside the distributed
+# QR), the n x b power partials, the l x b reorth projection, B_i and ||W||^2.
+def _allreduce(x):
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        t = torch.from_numpy(np.ascontiguousarray(x))
+        dist.all_reduce(t)
+        return t.numpy()
+    return x
+
+
+def _orth_rows(Y):
+    """CholQR2 of the row-sharded Y (Gram allreduce, replicated Cholesky)."""
+    for _ in range(2):
+        G = _allreduce(Y.T @ Y)
+        R = np.linalg.cholesky(G).T
+        Y = np.linalg.solve(R.T, Y.T).T
+    return Y
+
+
+def qb_rowsharded(Wg, m_total, b, M, tol, q, reorth, seed):
+    Wg = np.array(Wg, dtype=np.float64, order="F")
+    n = Wg.shape[1]
+    rmax = min(m_total, n)
+    Q = np.zeros((Wg.shape[0], 0))
+    B = np.zeros((0, n))
+    hist = []
+    for i in range(1, M + 1):
+        width = min(b, rmax - Q.shape[1])
+        if width < 1:
+            break
+        Om = omega_rows(seed, i, 0, n, width)  # the same n x b draw on every rank
+        Qi = _orth_rows(Wg @ Om)
+        for _ in range(q):
+            Z = np.linalg.qr(_allreduce(Wg.T @ Qi))[0]
+            Qi = _orth_rows(Wg @ Z)
+        if i % reorth == 0:
+            if Q.shape[1]:
+                Qi = Qi - Q @ _allreduce(Q.T @ Qi)
+            Qi = _orth_rows(Qi)
+        Bi = _allreduce(Qi.T @ Wg)
+        Wg = Wg - Qi @ Bi
+        Q = np.hstack([Q, Qi])
+        B = np.vstack([B, Bi])
+        r = float(np.sqrt(_allreduce(np.array([np.sum(Wg * Wg)]))[0]))
+        hist.append(r)
+        if tol > 0 and r < tol:
+            break
+    return Q, B, hist

@@ -131,3 +131,50 @@ def test_rowsharded_row_id_pivot_statistics_match_oracle(tmp_path, world):
     ref = orc.id_column(np.asfortranarray(c.T), k)  # id_row(c, k) = id_column(c^T, k)
     assert np.array_equal(jr, ref["jc"][:k])
     assert np.max(np.abs(W - ref["v"])) <= 1e-10
+
+
+def _qb_worker(rank, world, port, m, n, out_dir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from _dist_numpy import qb_rowsharded
+
+    rs = np.random.default_rng(8)
+    r = min(m, n)
+    U, _ = np.linalg.qr(rs.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rs.standard_normal((n, r)))
+    a = (U * (np.arange(r) + 1.0) ** -2) @ V.T
+    bounds = np.linspace(0, m, world + 1).astype(int)
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    Q, B, hist = qb_rowsharded(a[r0:r1], m, 8, 12, 1e-4, 1, 1, seed=5)
+    np.savez(os.path.join(out_dir, f"qb{rank}.npz"), Q=Q, B=B, hist=np.array(hist), a=a)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_rowsharded_qb_world2_matches_world1(tmp_path):
+    """The row-sharded QB collective logic (csrc/dist.cu qb_blocked_rowsharded,
+    mirrored in numpy over gloo): the same adaptive rank and residual history
+    at world 2 as at world 1, Q orthonormal across the shards, A = QB + W."""
+    m, n = 120, 90
+    res = {}
+    for world in (1, 2):
+        d = tmp_path / f"w{world}"
+        d.mkdir()
+        mp.spawn(_qb_worker, args=(world, _free_port(), m, n, str(d)), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"qb{r}.npz")) for r in range(world)]
+        res[world] = (np.vstack([x["Q"] for x in parts]), parts[0]["B"], parts[0]["hist"], parts[0]["a"])
+        for x in parts[1:]:
+            assert np.array_equal(x["B"], parts[0]["B"]) and np.array_equal(x["hist"], parts[0]["hist"])
+    Q1, B1, h1, a = res[1]
+    Q2, B2, h2, _ = res[2]
+    assert Q1.shape == Q2.shape and len(h1) == len(h2)
+    np.testing.assert_allclose(h2, h1, rtol=1e-8, atol=1e-14)
+    assert np.linalg.norm(Q2.T @ Q2 - np.eye(Q2.shape[1])) <= 1e-12
+    assert abs(np.linalg.norm(a - Q2 @ B2) - h2[-1]) <= 1e-10

@@ -140,3 +140,27 @@ def test_native_rowsharded_id_cur_world1_match_engine_and_oracle(orc, m, n, k, p
     assert rel_fro(cg["u"], co["u"]) <= 1e-6
     # W: skeleton rows are exactly the identity
     np.testing.assert_array_equal(cg["w"][cg["jr"], :], np.eye(k))
+
+
+def test_native_rowsharded_qb_world1_matches_engine_and_oracle(orc):
+    """Row-sharded qb_blocked (csrc/dist.cu) on a 1-rank NCCL communicator:
+    same adaptive rank, residual history and QB as the single-GPU engine and
+    the oracle with the reference's per-block Omega substreams."""
+    from helpers import make_test_matrix, rel_fro
+
+    eng = R.Engine(0)
+    m, n, b, M, tol = 700, 500, 16, 20, 1e-6
+    a = make_test_matrix(m, n, (np.arange(min(m, n)) + 1.0) ** -2, seed=4)
+    comm = _world1_comm(eng)
+    try:
+        got = eng.qb_blocked_rowsharded(comm.handle, a, m, b, M, tol, 1, 1, rng=R.Rng(12345))
+    finally:
+        comm.close()
+    single = eng.qb_blocked(a, b, M, tol, 1, 1, rng=R.Rng(12345))
+    want = orc.qb_blocked(a, b, M, tol, 1, 1, orc.rng(12345))
+    assert got["ell"] == single["ell"] == want["ell"]
+    assert got["tolerance_reached"] == want["reached"]
+    assert abs(got["final_residual"] - want["final"]) <= 1e-6 * want["final"] + 1e-13
+    np.testing.assert_allclose(got["history"], want["history"], rtol=1e-6, atol=1e-13)
+    assert rel_fro(got["q"] @ got["b"], a) <= 2.0 * rel_fro(want["q"] @ want["b"], a) + 1e-14
+    assert np.linalg.norm(got["q"].T @ got["q"] - np.eye(got["ell"])) <= 1e-12
