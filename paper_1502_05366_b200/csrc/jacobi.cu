@@ -12,6 +12,7 @@ namespace rlra_b200 {
 namespace {
 
 constexpr int kJacThreads = 256;
+constexpr int kJacReg = 16;  // register-resident column slice per lane (m <= 512)
 constexpr int kOneSidedSweepCap = 60;  // reference core/jacobi.hpp:29
 constexpr int kTwoSidedSweepCap = 30;  // reference core/jacobi.hpp:28
 
@@ -168,11 +169,30 @@ __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
                     double* wp = Ws + size_t(p) * m;
                     double* wq = Ws + size_t(q) * m;
                     double app = 0.0, aqq = 0.0, apq = 0.0;
-                    for (int i = lane; i < m; i += 32) {
-                        const double xp = wp[i], xq = wq[i];
-                        app += xp * xp;
-                        aqq += xq * xq;
-                        apq += xp * xq;
+                    // columns up to 32 * kJacReg long stay in registers between
+                    // the dot products and the rotation (loads issued together)
+                    const bool regs = m <= 32 * kJacReg;
+                    double rp[kJacReg], rq[kJacReg];
+                    if (regs) {
+#pragma unroll
+                        for (int u = 0; u < kJacReg; ++u) {
+                            const int i = lane + 32 * u;
+                            rp[u] = i < m ? wp[i] : 0.0;
+                            rq[u] = i < m ? wq[i] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kJacReg; ++u) {
+                            app += rp[u] * rp[u];
+                            aqq += rq[u] * rq[u];
+                            apq += rp[u] * rq[u];
+                        }
+                    } else {
+                        for (int i = lane; i < m; i += 32) {
+                            const double xp = wp[i], xq = wq[i];
+                            app += xp * xp;
+                            aqq += xq * xq;
+                            apq += xp * xq;
+                        }
                     }
                     app = warp_sum(app);
                     aqq = warp_sum(aqq);
@@ -180,12 +200,23 @@ __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
                     if (app != 0.0 && aqq != 0.0 && fabs(apq) > eps * sqrt(app * aqq)) {
                         const double zeta = (aqq - app) / (2.0 * apq);
                         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                        const double c = 1.0 / sqrt(1.0 + t * t);
+                        const double c = rsqrt(1.0 + t * t);
                         const double s = t * c;
-                        for (int i = lane; i < m; i += 32) {
-                            const double xp = wp[i], xq = wq[i];
-                            wp[i] = c * xp - s * xq;
-                            wq[i] = s * xp + c * xq;
+                        if (regs) {
+#pragma unroll
+                            for (int u = 0; u < kJacReg; ++u) {
+                                const int i = lane + 32 * u;
+                                if (i < m) {
+                                    wp[i] = c * rp[u] - s * rq[u];
+                                    wq[i] = s * rp[u] + c * rq[u];
+                                }
+                            }
+                        } else {
+                            for (int i = lane; i < m; i += 32) {
+                                const double xp = wp[i], xq = wq[i];
+                                wp[i] = c * xp - s * xq;
+                                wq[i] = s * xp + c * xq;
+                            }
                         }
                         if (lane < C2) {
                             const double xp = Jm[p * C2 + lane], xq = Jm[q * C2 + lane];
@@ -205,23 +236,20 @@ __global__ void __launch_bounds__(BW * 32) block_jacobi_kernel(BlockJacArgs a) {
                 }
                 // V(:, cols) <- V(:, cols) * Jm, one row per thread
                 for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                    double x[C2], y[C2];
+                    double x[C2];
 #pragma unroll
                     for (int c = 0; c < C2; ++c) {
                         const int gc = gcol(c);
                         x[c] = gc < n ? a.V[i + int64_t(gc) * a.ldv] : 0.0;
                     }
+                    // row i is read completely before any of it is written
 #pragma unroll
                     for (int c = 0; c < C2; ++c) {
                         double s = 0.0;
 #pragma unroll
                         for (int t = 0; t < C2; ++t) s += x[t] * Jm[c * C2 + t];
-                        y[c] = s;
-                    }
-#pragma unroll
-                    for (int c = 0; c < C2; ++c) {
                         const int gc = gcol(c);
-                        if (gc < n) a.V[i + int64_t(gc) * a.ldv] = y[c];
+                        if (gc < n) a.V[i + int64_t(gc) * a.ldv] = s;
                     }
                 }
                 if (threadIdx.x == 0) flags[sweep % 3] = 1;
