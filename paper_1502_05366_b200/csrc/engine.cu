@@ -166,11 +166,18 @@ void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource&
     const int n = int(A.cols);
     if (!sketched) sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
     if (q == 0) return;
-    DMatBuf Z(ctx, n, l);
+    DMatBuf Z(ctx, n, l), Y2;
+    if (span_only) Y2 = DMatBuf(ctx, Y.rows, l);  // span-only orth output: no copy back into Y
     GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
-        if ((2 * j - 2) % s == 0) orth_mid(ctx, Y, span_only);
-        gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z);  // Z = A^T Y
+        DMat Yc = Y;
+        if ((2 * j - 2) % s == 0) {
+            if (span_only && orth_span_into(ctx, Y, Y2.m))
+                Yc = Y2.m;
+            else
+                orth_mid(ctx, Y, span_only);
+        }
+        gemm(ctx, Op::T, Op::N, 1.0, A, Yc, 0.0, Z);  // Z = A^T Y
         if ((2 * j - 1) % s == 0) orth_mid(ctx, Z, span_only);
         gemm(ctx, Op::N, Op::N, 1.0, A, Z, 0.0, Y);  // Y = A Z
     }

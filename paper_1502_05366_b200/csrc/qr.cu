@@ -760,6 +760,22 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
     return res;
 }
 
+bool orth_span_into(Context& ctx, const DMat& Y, const DMat& out) {
+    const int m = int(Y.rows), n = int(Y.cols);
+    if (m < n || n == 0) return false;
+    ProfScope prof(ctx, "orth", m, n, 1, 0.0);
+    GemmTag tag(ctx, "gemm_orth");
+    DMatBuf G1(ctx, n, n), R1i(ctx, n, n);
+    GemmOpts sy;
+    sy.upper_tiles_only = true;
+    gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G1, sy);
+    if (!chol_upper_inv(ctx, G1, R1i, ctx.cholqr_pivot_floor)) return false;
+    GemmOpts tri;
+    tri.tri_b_upper = true;
+    gemm(ctx, Op::N, Op::N, 1.0, Y, R1i, 0.0, out, tri);
+    return true;
+}
+
 QrResult orth_span_inplace(Context& ctx, const DMat& Y) {
     const int m = int(Y.rows), n = int(Y.cols);
     ProfScope prof(ctx, "orth", m, n, 1, 0.0);

@@ -31,6 +31,11 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R);
 // the Q_i appended by QB) always comes from orth_inplace.
 QrResult orth_span_inplace(Context& ctx, const DMat& Y);
 
+// One CholQR pass of Y written into `out` (same shape, no aliasing) without
+// the copy back; false (out untouched) when the Gram is too ill-conditioned
+// for a single pass — the caller then orthonormalises Y in place.
+bool orth_span_into(Context& ctx, const DMat& Y, const DMat& out);
+
 // Always the Householder path (used for the fallback and for tests).
 QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R);
 
