@@ -582,6 +582,52 @@ inline QbFactors qb_blocked(const DenseMatrix& a, int b, int num_blocks, double 
     return detail::qb_call(w, false, b, num_blocks, tol, q_power, reorth_period, rng);
 }
 
+namespace detail {
+// the composite drivers: node streams drawn from rng in the reference's order
+template <class F>
+inline QbFactors qb_composite(const DenseMatrix& a, int rank, int count, bool substream_per_draw, RngState& rng,
+                              F&& call) {
+    std::vector<rlra_rng> nodes(static_cast<std::size_t>(count));
+    for (auto& nd : nodes) rlra_rng_substream(rng.raw(), &nd);
+    rlra_rng_nodes holder{nodes.data(), count, substream_per_draw ? 1 : 0};
+    rlra_omega om{};
+    om.mode = RLRA_OMEGA_CALLBACK;
+    om.fill = rlra_omega_fill_rng_nodes;
+    om.user = &holder;
+    QbFactors f;
+    f.q = DenseMatrix(a.rows(), rank);
+    f.b = DenseMatrix(rank, a.cols());
+    double fin = 0.0;
+    check(call(&om, f.q.data(), f.b.data(), &fin));
+    f.ell = rank;
+    f.residual_report.final_residual = fin;
+    f.residual_report.history.push_back(fin);
+    return f;
+}
+}  // namespace detail
+
+// qb.hpp:159-204: M independently sampled blocks, projected sequentially
+inline QbFactors qb_parallel(const DenseMatrix& a, int b, int num_blocks, int q_power, RngState& rng) {
+    const int rank = (b >= 1 && num_blocks >= 1) ? b * num_blocks : 1;
+    return detail::qb_composite(a, rank, std::max(num_blocks, 1), false, rng, [&](rlra_omega* om, double* q, double* bb,
+                                                                                   double* fin) {
+        return rlra_qb_parallel(detail::ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), detail::ld(a), b, num_blocks,
+                                q_power, om, q, std::max(1, a.rows()), bb, std::max(1, rank), fin);
+    });
+}
+
+// qb.hpp:211-271: leaf QBs of 2^j row slabs merged pairwise up a binary tree
+inline QbFactors qb_hierarchical(const DenseMatrix& a, int num_row_blocks, int b, int num_blocks, int q_power,
+                                 RngState& rng) {
+    const int rank = (b >= 1 && num_blocks >= 1) ? b * num_blocks : 1;
+    const int count = std::max(1, 2 * num_row_blocks - 1);
+    return detail::qb_composite(a, rank, count, true, rng, [&](rlra_omega* om, double* q, double* bb, double* fin) {
+        return rlra_qb_hierarchical(detail::ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), detail::ld(a),
+                                    num_row_blocks, b, num_blocks, q_power, om, q, std::max(1, a.rows()), bb,
+                                    std::max(1, rank), fin);
+    });
+}
+
 inline SvdFactors svd_from_qb(const QbFactors& qb, int k, Vnum vnum) {
     if (k < 0 || k > qb.ell) throw DimensionError(detail::msg("rank k = %d outside [0, rank(B) = %d]", k, qb.ell));
     const int kk = k == 0 ? qb.ell : k;

@@ -101,6 +101,17 @@ void rlra_rng_gaussian_fill(rlra_rng* r, int rows, int cols, double* out);
  * (rsvd/sample/id_rand) and substream-then-draw (qb_blocked, qb.hpp:119). */
 void rlra_omega_fill_rng(void* user, int draw, int rows, int cols, double* out);
 void rlra_omega_fill_rng_substream(void* user, int draw, int rows, int cols, double* out);
+/* Per-node streams for the composite QB drivers (qb_parallel, qb_hierarchical):
+ * draw ids are (node << 16) | block; nodes[node] is the node's RngState in the
+ * reference's order (qb_parallel: one substream per block, drawn directly;
+ * qb_hierarchical: the leaf substreams then the merge substreams, each
+ * node's qb_blocked taking one further substream per block). */
+typedef struct {
+    rlra_rng* nodes;
+    int count;
+    int substream_per_draw;
+} rlra_rng_nodes;
+void rlra_omega_fill_rng_nodes(void* user, int draw, int rows, int cols, double* out);
 
 /* ------------------------------------------------------------- context --- */
 rlra_status rlra_ctx_create(int device, rlra_ctx** out);
@@ -118,6 +129,19 @@ rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap,
 /* The cudaStream_t the context launches on (for event timing by callers). */
 void* rlra_ctx_stream(const rlra_ctx* ctx);
 const char* rlra_last_error(void);
+
+/* qb_parallel (qb.hpp:159-204): M independent block samples, per-block
+ * orthonormalisation, sequential cross-block projection, B = Q^T A, ell = b*M.
+ * qb_hierarchical (qb.hpp:211-271): fixed-rank QB of num_row_blocks (2^j)
+ * horizontal slabs, merged pairwise up a binary tree (QB of the stacked B's,
+ * Q lifted through the block-diagonal stages).  q: m x (b*M), b: (b*M) x n.
+ * Omega draw ids: (node << 16) | block (see rlra_rng_nodes). */
+rlra_status rlra_qb_parallel(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int blk,
+                             int num_blocks, int q_power, const rlra_omega* omega, double* q, int64_t ldq,
+                             double* b, int64_t ldb, double* final_residual);
+rlra_status rlra_qb_hierarchical(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                 int num_row_blocks, int blk, int num_blocks, int q_power, const rlra_omega* omega,
+                                 double* q, int64_t ldq, double* b, int64_t ldb, double* final_residual);
 
 /* ------------------------------------------- I/O, generator, verifier ---
  * Binary matrix files in the reference format (io.hpp:40-109): int32 rows,

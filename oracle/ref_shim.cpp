@@ -273,6 +273,31 @@ int ref_two_sided_from_column(const double* a, int m, int n, const int* jc, cons
     });
 }
 
+// qb.hpp qb_parallel / qb_hierarchical: q m x ell, b ell x n (ld ell)
+int ref_qb_parallel(const double* a, int m, int n, int blk, int num_blocks, int q_power, ref_rng* r, double* q,
+                    double* b, double* final_resid) {
+    return guard([&] {
+        rlra::RngState st = to_state(r);
+        rlra::QbFactors f = rlra::qb_parallel(wrap(a, m, n), blk, num_blocks, q_power, st);
+        put(f.q, q);
+        put(f.b, b);
+        *final_resid = f.residual_report.final_residual;
+        from_state(st, r);
+    });
+}
+
+int ref_qb_hierarchical(const double* a, int m, int n, int nrb, int blk, int num_blocks, int q_power, ref_rng* r,
+                        double* q, double* b, double* final_resid) {
+    return guard([&] {
+        rlra::RngState st = to_state(r);
+        rlra::QbFactors f = rlra::qb_hierarchical(wrap(a, m, n), nrb, blk, num_blocks, q_power, st);
+        put(f.q, q);
+        put(f.b, b);
+        *final_resid = f.residual_report.final_residual;
+        from_state(st, r);
+    });
+}
+
 // report.hpp verify(a, SvdFactors, sigma_true): out = rel_fro, rel_spec,
 // fro_floor, spec_floor, spec_bound
 int ref_verify_svd(const double* a, int m, int n, const double* u, const double* sigma, const double* v, int k,

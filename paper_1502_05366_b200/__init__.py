@@ -73,6 +73,10 @@ class _Omega(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class _RngNodes(C.Structure):  # rlra_rng_nodes
+    _fields_ = [("nodes", C.c_void_p), ("count", C.c_int), ("substream_per_draw", C.c_int)]
+
+
 _lib = None
 
 
@@ -404,6 +408,38 @@ class Engine:
         return dict(q=np.asfortranarray(Q[:, :e]), b=np.asfortranarray(B[:e]), ell=e,
                     history=hist[:nh.value].copy(), final_residual=fin.value,
                     tolerance_reached=bool(reached.value))
+
+    @staticmethod
+    def _node_streams(rng, count, substream_per_draw):
+        """rlra_rng_nodes of `count` substreams of rng, in the reference's order."""
+        nodes = (_RngStruct * count)()
+        for i in range(count):
+            lib().rlra_rng_substream(C.byref(rng._s), C.byref(nodes[i]))
+        holder = _RngNodes(C.cast(nodes, C.c_void_p), count, int(substream_per_draw))
+        return nodes, holder
+
+    def _composite_qb(self, fn, a, args, rank, rng, count, substream_per_draw):
+        A = _F(a)
+        m, n = A.shape
+        nodes, holder = self._node_streams(rng, count, substream_per_draw)
+        om = _Omega(OMEGA_CALLBACK, C.cast(lib().rlra_omega_fill_rng_nodes, C.c_void_p),
+                          C.cast(C.pointer(holder), C.c_void_p), 0)
+        Q = np.zeros((m, rank), order="F")
+        B = np.zeros((rank, n), order="F")
+        fin = C.c_double(0)
+        _check(fn(self._ctx, HOST, _d(A), m, n, _i64(_ld(A)), *args, C.byref(om), _d(Q), _i64(max(1, m)), _d(B),
+                  _i64(max(1, rank)), C.byref(fin)))
+        return dict(q=Q, b=B, ell=rank, final_residual=fin.value, history=[fin.value], tolerance_reached=True)
+
+    def qb_parallel(self, a, b, num_blocks, q_power, rng):
+        """qb.hpp:159 (reference Omega streams: one substream per block)."""
+        return self._composite_qb(lib().rlra_qb_parallel, a, (b, num_blocks, q_power), b * num_blocks, rng,
+                                  num_blocks, False)
+
+    def qb_hierarchical(self, a, num_row_blocks, b, num_blocks, q_power, rng):
+        """qb.hpp:211 (reference streams: leaf substreams, then merge substreams)."""
+        return self._composite_qb(lib().rlra_qb_hierarchical, a, (num_row_blocks, b, num_blocks, q_power),
+                                  b * num_blocks, rng, 2 * num_row_blocks - 1, True)
 
     def svd_from_qb(self, qb, k=0, vnum=VNUM_QR):
         """qb.hpp:276 — qb is the dict qb_blocked returns."""

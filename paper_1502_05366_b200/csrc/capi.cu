@@ -555,6 +555,54 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
     });
 }
 
+rlra_status rlra_qb_parallel(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int blk,
+                             int num_blocks, int q_power, const rlra_omega* omega, double* q, int64_t ldq,
+                             double* b, int64_t ldb, double* final_residual) {
+    return guard(ctx, [&](Context& C) {  // qb.hpp:161-170 checks and messages
+        if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
+        if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
+        if (q_power < 0) raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
+        const int rmax = std::min(m, n);
+        if (int64_t(blk) * num_blocks > rmax)
+            raise(RLRA_EDIM, fmt("b*M = %d exceeds min(m,n) = %d", blk * num_blocks, rmax));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        const int rank = blk * num_blocks;
+        Out Q(C, loc, q, m, rank, ldq, "q"), B(C, loc, b, rank, n, ldb, "b");
+        const double r = qb_parallel(C, A.m, blk, num_blocks, q_power, om, Q.m, B.m);
+        Q.finish(C);
+        B.finish(C);
+        sync(C);
+        if (final_residual) *final_residual = r;
+    });
+}
+
+rlra_status rlra_qb_hierarchical(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
+                                 int num_row_blocks, int blk, int num_blocks, int q_power, const rlra_omega* omega,
+                                 double* q, int64_t ldq, double* b, int64_t ldb, double* final_residual) {
+    return guard(ctx, [&](Context& C) {  // qb.hpp:213-226 checks and messages
+        const int blocks = num_row_blocks;
+        if (blocks < 2 || (blocks & (blocks - 1)) != 0)
+            raise(RLRA_EDIM, fmt("num_row_blocks must be one of {2,4,8,...} (got %d)", blocks));
+        const int base = m / blocks;
+        if (base < 1) raise(RLRA_EDIM, fmt("num_row_blocks %d exceeds row count %d", blocks, m));
+        if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
+        if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
+        if (q_power < 0) raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
+        const int rank = blk * num_blocks;
+        if (rank > std::min(base, n))
+            raise(RLRA_EDIM, fmt("leaf rank b*M = %d exceeds the smallest row block (%d x %d)", rank, base, n));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        Out Q(C, loc, q, m, rank, ldq, "q"), B(C, loc, b, rank, n, ldb, "b");
+        const double r = qb_hierarchical(C, A.m, blocks, blk, num_blocks, q_power, om, Q.m, B.m);
+        Q.finish(C);
+        B.finish(C);
+        sync(C);
+        if (final_residual) *final_residual = r;
+    });
+}
+
 rlra_status rlra_binary_header(const char* path, int* rows, int* cols) {
     try {
         if (!path || !rows || !cols) raise(RLRA_EINVAL, "null argument to rlra_binary_header");

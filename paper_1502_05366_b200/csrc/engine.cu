@@ -345,6 +345,96 @@ QbOut qb_blocked(Context& ctx, const DMat& W, int blk, int num_blocks, double to
     return out;
 }
 
+// ||A - Q B||_F through the fused residual GEMM (A copied: the epilogue is
+// read-only on R when C is null)
+static double qb_residual(Context& ctx, const DMat& A, const DMat& Q, const DMat& B) {
+    Buf sq(ctx, sizeof(double));
+    GemmOpts o;
+    o.epi = EPI_RESID;
+    o.R = A.p;
+    o.ldr = A.ld;
+    o.resid_sq = sq.d();
+    gemm(ctx, Op::N, Op::N, int(A.rows), int(A.cols), int(Q.cols), 1.0, Q.p, Q.ld, B.p, B.ld, 0.0, nullptr, 0, o);
+    return std::sqrt(read_scalar(ctx, sq.d()));
+}
+
+double qb_parallel(Context& ctx, const DMat& A, int blk, int num_blocks, int q_power, OmegaSource& om, const DMat& Q,
+                   const DMat& B) {
+    const int m = int(A.rows), n = int(A.cols);
+    DMatBuf Y(ctx, m, blk), Z(ctx, n, blk), P(ctx, blk * num_blocks, blk);
+    for (int i = 0; i < num_blocks; ++i) {  // qb.hpp:176-186, node i draws its block directly
+        const DMat Qi = Q.block(0, int64_t(i) * blk, m, blk);
+        OmegaSource oi{om.o, i << 16};
+        sketch(ctx, Op::N, A, blk, oi, Qi);  // y_i = A Omega_i
+        for (int j = 0; j < q_power; ++j) {
+            orth(ctx, Qi);
+            gemm(ctx, Op::T, Op::N, 1.0, A, Qi, 0.0, Z.m);
+            orth(ctx, Z.m);
+            gemm(ctx, Op::N, Op::N, 1.0, A, Z.m, 0.0, Qi);
+        }
+        orth(ctx, Qi);  // qb.hpp:188-189
+    }
+    for (int i = 1; i < num_blocks; ++i) {  // qb.hpp:191-198: sequential projection
+        const DMat Qp = Q.block(0, 0, m, int64_t(i) * blk), Qi = Q.block(0, int64_t(i) * blk, m, blk);
+        const DMat Pi = P.m.block(0, 0, int64_t(i) * blk, blk);
+        gemm(ctx, Op::T, Op::N, 1.0, Qp, Qi, 0.0, Pi);
+        gemm(ctx, Op::N, Op::N, -1.0, Qp, Pi, 1.0, Qi);
+        orth(ctx, Qi);
+    }
+    gemm(ctx, Op::T, Op::N, 1.0, Q, A, 0.0, B);  // B = Q^T A
+    return qb_residual(ctx, A, Q, B);
+}
+
+double qb_hierarchical(Context& ctx, const DMat& A, int num_row_blocks, int blk, int num_blocks, int q_power,
+                       OmegaSource& om, const DMat& Q, const DMat& B) {
+    const int m = int(A.rows), n = int(A.cols), blocks = num_row_blocks, rank = blk * num_blocks;
+    const int base = m / blocks;
+    struct Node {
+        DMatBuf q, b;
+        int row0 = 0, rows = 0;
+    };
+    std::vector<Node> nodes(static_cast<size_t>(blocks));
+    int row0 = 0;
+    for (int t = 0; t < blocks; ++t) {  // leaves (qb.hpp:235-244), node t's substreams
+        const int rows_t = (t == blocks - 1) ? m - row0 : base;
+        DMatBuf W(ctx, rows_t, n);
+        copy_mat(ctx, A.block(row0, 0, rows_t, n), W.m);
+        nodes[size_t(t)].q = DMatBuf(ctx, rows_t, rank);
+        nodes[size_t(t)].b = DMatBuf(ctx, rank, n);
+        nodes[size_t(t)].row0 = row0;
+        nodes[size_t(t)].rows = rows_t;
+        OmegaSource ot{om.o, t << 16};
+        qb_blocked(ctx, W.m, blk, num_blocks, 0.0, q_power, 1, ot, nodes[size_t(t)].q.m, nodes[size_t(t)].b.m);
+        row0 += rows_t;
+    }
+    int merge = blocks;  // merge nodes follow the leaves (qb.hpp:245-263)
+    while (nodes.size() > 1) {
+        std::vector<Node> next;
+        for (size_t t = 0; t + 1 < nodes.size(); t += 2) {
+            Node& L = nodes[t];
+            Node& Rn = nodes[t + 1];
+            DMatBuf S(ctx, 2 * rank, n), Qm(ctx, 2 * rank, rank);
+            copy_mat(ctx, L.b.m, S.m.block(0, 0, rank, n));
+            copy_mat(ctx, Rn.b.m, S.m.block(rank, 0, rank, n));
+            Node M;
+            M.b = DMatBuf(ctx, rank, n);
+            OmegaSource omg{om.o, (merge++) << 16};
+            qb_blocked(ctx, S.m, blk, num_blocks, 0.0, q_power, 1, omg, Qm.m, M.b.m);
+            M.row0 = L.row0;
+            M.rows = L.rows + Rn.rows;
+            M.q = DMatBuf(ctx, M.rows, rank);
+            gemm(ctx, Op::N, Op::N, 1.0, L.q.m, Qm.m.block(0, 0, rank, rank), 0.0, M.q.m.block(0, 0, L.rows, rank));
+            gemm(ctx, Op::N, Op::N, 1.0, Rn.q.m, Qm.m.block(rank, 0, rank, rank), 0.0,
+                 M.q.m.block(L.rows, 0, Rn.rows, rank));
+            next.push_back(std::move(M));
+        }
+        nodes = std::move(next);
+    }
+    copy_mat(ctx, nodes[0].q.m, Q);
+    copy_mat(ctx, nodes[0].b.m, B);
+    return qb_residual(ctx, A, Q, B);
+}
+
 void svd_from_qb(Context& ctx, const DMat& Q, const DMat& B, int k, int vnum, const DMat& U,
                  double* sigma, const DMat& V) {
     const int ell = int(B.rows), n = int(B.cols);

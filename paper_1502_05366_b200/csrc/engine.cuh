@@ -55,6 +55,13 @@ struct QbOut {
 QbOut qb_blocked(Context& ctx, const DMat& W, int blk, int num_blocks, double tol, int q_power,
                  int reorth_period, OmegaSource& om, const DMat& Q, const DMat& B);
 
+// qb.hpp:159-204 / 211-271 (the composite drivers); Q m x (b*M), B (b*M) x n;
+// Omega draw ids (node << 16) | block.  Return ||A - QB||_F.
+double qb_parallel(Context& ctx, const DMat& A, int blk, int num_blocks, int q_power, OmegaSource& om, const DMat& Q,
+                   const DMat& B);
+double qb_hierarchical(Context& ctx, const DMat& A, int num_row_blocks, int blk, int num_blocks, int q_power,
+                       OmegaSource& om, const DMat& Q, const DMat& B);
+
 // qb.hpp:276-288 (k already resolved to [1, ell]); U m x k, sigma k, V n x k
 void svd_from_qb(Context& ctx, const DMat& Q, const DMat& B, int k, int vnum, const DMat& U,
                  double* sigma, const DMat& V);

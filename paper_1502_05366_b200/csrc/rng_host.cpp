@@ -75,4 +75,17 @@ void rlra_omega_fill_rng_substream(void* user, int, int rows, int cols, double* 
     rlra_rng_gaussian_fill(&child, rows, cols, out);
 }
 
+void rlra_omega_fill_rng_nodes(void* user, int draw, int rows, int cols, double* out) {
+    rlra_rng_nodes* nd = static_cast<rlra_rng_nodes*>(user);
+    const int node = draw >> 16;
+    rlra_rng* st = &nd->nodes[node < nd->count ? node : nd->count - 1];
+    if (nd->substream_per_draw) {
+        rlra_rng child;
+        rlra_rng_substream(st, &child);
+        rlra_rng_gaussian_fill(&child, rows, cols, out);
+    } else {
+        rlra_rng_gaussian_fill(st, rows, cols, out);
+    }
+}
+
 }  // extern "C"

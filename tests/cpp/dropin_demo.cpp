@@ -29,6 +29,9 @@ int main(int argc, char** argv) {
     if (worst > 1e-8 || e.rel_frobenius_error > 10.0 * e.fro_floor + 1e-12) return 3;
     rlra::CurFactors c = rlra::cur_rand(a, 30, 10, 2, 1, rng);
     rlra::QbFactors qb = rlra::qb_blocked(a, 20, 10, 1e-3, 1, 1, rng);
+    rlra::QbFactors qh = rlra::qb_hierarchical(a, 4, 10, 3, 1, rng);
+    rlra::QbFactors qp = rlra::qb_parallel(a, 10, 3, 1, rng);
+    if (qh.ell != 30 || qp.ell != 30 || !(qh.residual_report.final_residual > 0.0)) return 5;
     try {
         rlra::matmul(rlra::DenseMatrix(3, 4), rlra::DenseMatrix(5, 2));
         return 4;

@@ -259,3 +259,66 @@ def test_cur_linkage_rank_deficient_message(eng):
     with pytest.raises(R.NumericalError) as e:
         eng.cur_from_two_sided(a, ts)
     assert "9" in str(e.value)
+
+
+def _ref_lib():
+    import ctypes as C
+    import os
+
+    import _oracle
+
+    if not os.path.exists(_oracle.REF_PATH):
+        pytest.skip("oracle/_ref not built")
+    lib = C.CDLL(_oracle.REF_PATH)
+    lib.ref_last_error.restype = C.c_char_p
+    return lib
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_qb_parallel_vs_reference(eng, q):
+    """qb_parallel (qb.hpp:159-204) with the reference's per-block streams:
+    Q, B and the residual match the unmodified reference."""
+    import ctypes as C
+
+    import _oracle
+
+    lib = _ref_lib()
+    m, n, b, M = 300, 200, 10, 4
+    a = make_test_matrix(m, n, np.exp(-np.arange(200) / 15.0), seed=21)
+    got = eng.qb_parallel(a, b, M, q, R.Rng(777))
+    Q = np.zeros((m, b * M), order="F")
+    B = np.zeros((b * M, n), order="F")
+    fin = C.c_double(0)
+    r = _oracle.Rng()
+    lib.ref_rng_seed(C.byref(r), C.c_uint64(777))
+    af = np.asfortranarray(a)
+    assert lib.ref_qb_parallel(_oracle.d(af), m, n, b, M, q, C.byref(r), _oracle.d(Q), _oracle.d(B), C.byref(fin)) == 0
+    assert rel_fro(got["q"], Q) <= 1e-10 and rel_fro(got["b"], B) <= 1e-10
+    assert abs(got["final_residual"] - fin.value) <= 1e-8 * fin.value + 1e-14
+
+
+@pytest.mark.parametrize("nrb", [2, 4])
+def test_qb_hierarchical_vs_reference(eng, nrb):
+    """qb_hierarchical (qb.hpp:211-271): leaf QBs of the row slabs, pairwise
+    merges up the tree, the reference's leaf-then-merge substreams."""
+    import ctypes as C
+
+    import _oracle
+
+    lib = _ref_lib()
+    m, n, b, M = 400, 150, 8, 3
+    a = make_test_matrix(m, n, np.exp(-np.arange(150) / 8.0), seed=22)
+    got = eng.qb_hierarchical(a, nrb, b, M, 1, R.Rng(31))
+    Q = np.zeros((m, b * M), order="F")
+    B = np.zeros((b * M, n), order="F")
+    fin = C.c_double(0)
+    r = _oracle.Rng()
+    lib.ref_rng_seed(C.byref(r), C.c_uint64(31))
+    af = np.asfortranarray(a)
+    assert lib.ref_qb_hierarchical(_oracle.d(af), m, n, nrb, b, M, 1, C.byref(r), _oracle.d(Q), _oracle.d(B),
+                                   C.byref(fin)) == 0
+    assert rel_fro(got["q"], Q) <= 1e-9 and rel_fro(got["b"], B) <= 1e-9
+    assert abs(got["final_residual"] - fin.value) <= 1e-8 * fin.value + 1e-14
+    with pytest.raises(R.DimensionError) as e:
+        eng.qb_hierarchical(a, 3, b, M, 1, R.Rng(1))
+    assert "num_row_blocks must be one of {2,4,8,...} (got 3)" in str(e.value)
