@@ -212,6 +212,16 @@ rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, 
                                        double tol, int q_power, int reorth_period, const rlra_omega* omega,
                                        double* q, int64_t ldq, double* b, int64_t ldb, int cap, int* ell,
                                        double* hist, int* nhist, double* final_residual, int* reached);
+/* qb_hierarchical (qb.hpp:211-271) over the ranks: num_row_blocks = world * L
+ * (a power of two), rank g holding slabs [g L, (g+1) L) of the reference's
+ * partition (floor(m_total / num_row_blocks) rows each, the last slab the
+ * remainder).  Leaves and the rank's own subtree merge locally; the subtree
+ * roots' B are allgathered over NVLink and the upper merges run replicated.
+ * q: this rank's m_local x (b*M) rows of Q, b: (b*M) x n replicated. */
+rlra_status rlra_qb_hierarchical_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local,
+                                            int n, int64_t lda, int64_t m_total, int num_row_blocks, int blk,
+                                            int num_blocks, int q_power, const rlra_omega* omega, double* q,
+                                            int64_t ldq, double* b, int64_t ldb, double* final_residual);
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,

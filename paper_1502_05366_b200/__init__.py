@@ -441,6 +441,22 @@ class Engine:
         return self._composite_qb(lib().rlra_qb_hierarchical, a, (num_row_blocks, b, num_blocks, q_power),
                                   b * num_blocks, rng, 2 * num_row_blocks - 1, True)
 
+    def qb_hierarchical_rowsharded(self, comm, a_local, m_total, num_row_blocks, b, num_blocks, q_power, rng):
+        """rlra_qb_hierarchical_rowsharded with host buffers (this rank's slabs)."""
+        fn = lib().rlra_qb_hierarchical_rowsharded
+        A = _F(a_local)
+        mg, n = A.shape
+        rank = b * num_blocks
+        nodes, holder = self._node_streams(rng, 2 * num_row_blocks - 1, True)
+        om = _Omega(OMEGA_CALLBACK, C.cast(lib().rlra_omega_fill_rng_nodes, C.c_void_p),
+                    C.cast(C.pointer(holder), C.c_void_p), 0)
+        Q = np.zeros((mg, rank), order="F")
+        B = np.zeros((rank, n), order="F")
+        fin = C.c_double(0)
+        _check(fn(self._ctx, comm, HOST, _d(A), mg, n, _i64(_ld(A)), _i64(m_total), num_row_blocks, b, num_blocks,
+                  q_power, C.byref(om), _d(Q), _i64(max(1, mg)), _d(B), _i64(max(1, rank)), C.byref(fin)))
+        return dict(q=Q, b=B, ell=rank, final_residual=fin.value)
+
     def svd_from_qb(self, qb, k=0, vnum=VNUM_QR):
         """qb.hpp:276 — qb is the dict qb_blocked returns."""
         q, b = _F(qb["q"]), _F(qb["b"])

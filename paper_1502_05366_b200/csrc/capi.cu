@@ -759,6 +759,44 @@ rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, 
     });
 }
 
+rlra_status rlra_qb_hierarchical_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local,
+                                            int n, int64_t lda, int64_t m_total, int num_row_blocks, int blk,
+                                            int num_blocks, int q_power, const rlra_omega* omega, double* q,
+                                            int64_t ldq, double* b, int64_t ldb, double* final_residual) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        const int nrb = num_row_blocks, W = comm->c.nranks;
+        if (nrb < 2 || (nrb & (nrb - 1)) != 0)
+            raise(RLRA_EDIM, fmt("num_row_blocks must be one of {2,4,8,...} (got %d)", nrb));
+        if (nrb % W != 0)
+            raise(RLRA_EDIM, fmt("num_row_blocks %d is not a multiple of the %d ranks", nrb, W));
+        if (m_total > INT32_MAX) raise(RLRA_EDIM, "qb_hierarchical_rowsharded: m_total too large");
+        const int64_t base = m_total / nrb;
+        if (base < 1) raise(RLRA_EDIM, fmt("num_row_blocks %d exceeds row count %lld", nrb, (long long)m_total));
+        if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
+        if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
+        if (q_power < 0) raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
+        const int rank = blk * num_blocks;
+        if (rank > std::min<int64_t>(base, n))
+            raise(RLRA_EDIM, fmt("leaf rank b*M = %d exceeds the smallest row block (%lld x %d)", rank,
+                                 (long long)base, n));
+        const int L = nrb / W, g = comm->c.rank;
+        const int64_t want = (g == W - 1) ? m_total - base * L * (W - 1) : base * L;
+        if (m_local != want)
+            raise(RLRA_EDIM, fmt("qb_hierarchical_rowsharded: rank %d holds %d rows, its %d slabs need %lld", g,
+                                 m_local, L, (long long)want));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m_local, n, lda, "a");
+        Out Q(C, loc, q, m_local, rank, ldq, "q"), B(C, loc, b, rank, n, ldb, "b");
+        const double r = qb_hierarchical_rowsharded(C, comm->c, A.m, m_total, nrb, blk, num_blocks, q_power, om, Q.m,
+                                                    B.m);
+        Q.finish(C);
+        B.finish(C);
+        sync(C);
+        if (final_residual) *final_residual = r;
+    });
+}
+
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,

@@ -692,4 +692,119 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
     return out;
 }
 
+
+// qb_hierarchical (qb.hpp:211-271) with the row slabs on the ranks: rank g
+// holds slabs [g L, (g+1) L) of the num_row_blocks = world * L slabs, factors
+// them and merges its own subtree locally (no communication), allgathers the
+// subtree roots' B (rank x n each), and runs the upper merges replicated; its
+// rows of Q are its local Q lifted through the upper merges' blocks on its
+// path.  Omega node ids follow the reference: leaves 0..nrb-1, then the merges
+// level by level, pair by pair.
+double qb_hierarchical_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int num_row_blocks, int blk,
+                                  int num_blocks, int q_power, OmegaSource& om, const DMat& Q, const DMat& B) {
+    const int mg = int(A.rows), n = int(A.cols), W = cm.nranks, g = cm.rank;
+    const int nrb = num_row_blocks, L = nrb / W, rank = blk * num_blocks;
+    const int64_t base = m_total / nrb;
+    struct Node {
+        DMatBuf q, b;
+        int rows = 0;
+    };
+    // global index of the merge (level lv, pair pi) among the merge nodes
+    auto merge_id = [&](int lv, int pi) {
+        int id = nrb, cnt = nrb;
+        for (int l = 0; l < lv; ++l) {
+            cnt /= 2;
+            id += cnt;
+        }
+        return id + pi;
+    };
+    std::vector<Node> nodes;
+    int64_t r0 = 0;
+    for (int t = 0; t < L; ++t) {  // this rank's leaves
+        const int leaf = g * L + t;
+        const int rows_t = int((leaf == nrb - 1) ? mg - r0 : base);
+        Node nd;
+        DMatBuf Wt(ctx, rows_t, n);
+        copy_mat(ctx, A.block(r0, 0, rows_t, n), Wt.m);
+        nd.q = DMatBuf(ctx, rows_t, rank);
+        nd.b = DMatBuf(ctx, rank, n);
+        nd.rows = rows_t;
+        OmegaSource ot{om.o, leaf << 16};
+        qb_blocked(ctx, Wt.m, blk, num_blocks, 0.0, q_power, 1, ot, nd.q.m, nd.b.m);
+        nodes.push_back(std::move(nd));
+        r0 += rows_t;
+    }
+    auto merge_pair = [&](Node& Lf, Node& Rt, int id, DMatBuf* Qm_out) {
+        DMatBuf S(ctx, 2 * rank, n), Qm(ctx, 2 * rank, rank);
+        copy_mat(ctx, Lf.b.m, S.m.block(0, 0, rank, n));
+        copy_mat(ctx, Rt.b.m, S.m.block(rank, 0, rank, n));
+        Node M;
+        M.b = DMatBuf(ctx, rank, n);
+        OmegaSource omg{om.o, id << 16};
+        qb_blocked(ctx, S.m, blk, num_blocks, 0.0, q_power, 1, omg, Qm.m, M.b.m);
+        if (Qm_out) *Qm_out = std::move(Qm);
+        return std::make_pair(std::move(M), std::move(Qm));
+    };
+    int lv = 0;
+    for (; (int(nodes.size()) > 1); ++lv) {  // local subtree
+        std::vector<Node> next;
+        for (size_t t = 0; t + 1 < nodes.size(); t += 2) {
+            const int pi = g * (int(nodes.size()) / 2) + int(t / 2);
+            auto mq = merge_pair(nodes[t], nodes[t + 1], merge_id(lv, pi), nullptr);
+            Node M = std::move(mq.first);
+            const DMatBuf& Qm = mq.second;
+            M.rows = nodes[t].rows + nodes[t + 1].rows;
+            M.q = DMatBuf(ctx, M.rows, rank);
+            gemm(ctx, Op::N, Op::N, 1.0, nodes[t].q.m, Qm.m.block(0, 0, rank, rank), 0.0,
+                 M.q.m.block(0, 0, nodes[t].rows, rank));
+            gemm(ctx, Op::N, Op::N, 1.0, nodes[t + 1].q.m, Qm.m.block(rank, 0, rank, rank), 0.0,
+                 M.q.m.block(nodes[t].rows, 0, nodes[t + 1].rows, rank));
+            next.push_back(std::move(M));
+        }
+        nodes = std::move(next);
+    }
+    // upper levels: every rank's subtree root B, merged replicated
+    DMatBuf allB(ctx, rank, int64_t(n) * W);  // rank x n blocks side by side
+    {
+        DMatBuf mine(ctx, rank, n);
+        copy_mat(ctx, nodes[0].b.m, mine.m);
+        allgather(ctx, cm, mine.m.p, allB.m.p, size_t(rank) * n);
+    }
+    std::vector<Node> up(static_cast<size_t>(W));
+    for (int r = 0; r < W; ++r) {
+        up[size_t(r)].b = DMatBuf(ctx, rank, n);
+        copy_mat(ctx, allB.m.block(0, int64_t(r) * n, rank, n), up[size_t(r)].b.m);
+    }
+    DMatBuf T(ctx, rank, rank), Tn(ctx, rank, rank);
+    eye_mat(ctx, T.m);
+    int pos = g;  // this rank's index at the current upper level
+    for (; up.size() > 1; ++lv) {
+        std::vector<Node> next;
+        for (size_t t = 0; t + 1 < up.size(); t += 2) {
+            auto mq = merge_pair(up[t], up[t + 1], merge_id(lv, int(t / 2)), nullptr);
+            if (int(t) == (pos & ~1)) {  // this rank's path: T <- T * (top or bottom block)
+                const int64_t off = (pos & 1) ? rank : 0;
+                gemm(ctx, Op::N, Op::N, 1.0, T.m, mq.second.m.block(off, 0, rank, rank), 0.0, Tn.m);
+                copy_mat(ctx, Tn.m, T.m);
+            }
+            next.push_back(std::move(mq.first));
+        }
+        up = std::move(next);
+        pos >>= 1;
+    }
+    gemm(ctx, Op::N, Op::N, 1.0, nodes[0].q.m, T.m, 0.0, Q);  // this rank's rows of Q
+    copy_mat(ctx, up[0].b.m, B);
+    // ||A - Q B||_F over all ranks
+    Buf sq(ctx, sizeof(double));
+    GemmOpts o;
+    o.epi = EPI_RESID;
+    o.R = A.p;
+    o.ldr = A.ld;
+    o.resid_sq = sq.d();
+    gemm(ctx, Op::N, Op::N, mg, n, rank, 1.0, Q.p, Q.ld, B.p, B.ld, 0.0, nullptr, 0, o);
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    return std::sqrt(allreduce_scalar(ctx, cm, ctx.h_scalars[0]));
+}
+
 }  // namespace rlra_b200

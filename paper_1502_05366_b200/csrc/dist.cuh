@@ -46,4 +46,11 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
                             double tol, int q_power, int reorth_period, OmegaSource& om, const DMat& Q,
                             const DMat& B);
 
+// qb_hierarchical (qb.hpp:211-271) with num_row_blocks = world * L slabs,
+// rank g holding slabs [g L, (g+1) L) (the reference's slab partition:
+// floor(m_total / nrb) rows each, the last slab taking the remainder).
+// Q (m_g x b*M) this rank's rows, B replicated; returns ||A - QB||_F.
+double qb_hierarchical_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int num_row_blocks, int blk,
+                                  int num_blocks, int q_power, OmegaSource& om, const DMat& Q, const DMat& B);
+
 }  // namespace rlra_b200

@@ -234,3 +234,81 @@ def qb_rowsharded(Wg, m_total, b, M, tol, q, reorth, seed):
         if tol > 0 and r < tol:
             break
     return Q, B, hist
+
+
+# numpy mirror of csrc/dist.cu qb_hierarchical_rowsharded: leaves and the
+# rank's subtree locally, allgather of the subtree-root B's, replicated upper
+# merges, Q lifted through this rank's path.  Fixed-rank QB with counter-based
+# Omega per (node, block) so the single-process and sharded runs draw alike.
+def _qb_fixed(W, b, M, q, node, seed):
+    n = W.shape[1]
+    Q = np.zeros((W.shape[0], 0))
+    B = np.zeros((0, n))
+    for i in range(M):
+        Om = omega_rows(seed, (node << 16) | i, 0, n, b)
+        Qi = np.linalg.qr(W @ Om)[0]
+        for _ in range(q):
+            Qi = np.linalg.qr(W @ np.linalg.qr(W.T @ Qi)[0])[0]
+        if Q.shape[1]:
+            Qi = np.linalg.qr(Qi - Q @ (Q.T @ Qi))[0]
+        Bi = Qi.T @ W
+        W = W - Qi @ Bi
+        Q, B = np.hstack([Q, Qi]), np.vstack([B, Bi])
+    return Q, B
+
+
+def qb_hierarchical_np(slabs, b, M, q, seed):
+    """Single-process reference: slabs is the list of row slabs."""
+    nrb = len(slabs)
+    nodes = [_qb_fixed(s, b, M, q, t, seed) for t, s in enumerate(slabs)]
+    mid = nrb
+    while len(nodes) > 1:
+        nxt = []
+        for t in range(0, len(nodes), 2):
+            (ql, bl), (qr, br) = nodes[t], nodes[t + 1]
+            qm, bm = _qb_fixed(np.vstack([bl, br]), b, M, q, mid, seed)
+            mid += 1
+            r = bl.shape[0]
+            nxt.append((np.vstack([ql @ qm[:r], qr @ qm[r:]]), bm))
+        nodes = nxt
+    return nodes[0]
+
+
+def qb_hierarchical_rowsharded_np(my_slabs, nrb, b, M, q, seed):
+    world, g = dist.get_world_size(), dist.get_rank()
+    L = len(my_slabs)
+    rank = b * M
+
+    def merge_id(lv, pi):
+        idx, cnt = nrb, nrb
+        for _ in range(lv):
+            cnt //= 2
+            idx += cnt
+        return idx + pi
+
+    nodes = [_qb_fixed(s, b, M, q, g * L + t, seed) for t, s in enumerate(my_slabs)]
+    lv = 0
+    while len(nodes) > 1:
+        nxt = []
+        for t in range(0, len(nodes), 2):
+            (ql, bl), (qr, br) = nodes[t], nodes[t + 1]
+            qm, bm = _qb_fixed(np.vstack([bl, br]), b, M, q, merge_id(lv, g * (len(nodes) // 2) + t // 2), seed)
+            nxt.append((np.vstack([ql @ qm[:rank], qr @ qm[rank:]]), bm))
+        nodes = nxt
+        lv += 1
+    Bs = [torch.zeros(rank, nodes[0][1].shape[1], dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(Bs, torch.from_numpy(np.ascontiguousarray(nodes[0][1])))
+    up = [x.numpy() for x in Bs]
+    T = np.eye(rank)
+    pos = g
+    while len(up) > 1:
+        nxt = []
+        for t in range(0, len(up), 2):
+            qm, bm = _qb_fixed(np.vstack([up[t], up[t + 1]]), b, M, q, merge_id(lv, t // 2), seed)
+            if t == (pos & ~1):
+                T = T @ (qm[rank:] if pos & 1 else qm[:rank])
+            nxt.append(bm)
+        up = nxt
+        pos >>= 1
+        lv += 1
+    return nodes[0][0] @ T, up[0]

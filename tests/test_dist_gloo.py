@@ -178,3 +178,44 @@ def test_rowsharded_qb_world2_matches_world1(tmp_path):
     np.testing.assert_allclose(h2, h1, rtol=1e-8, atol=1e-14)
     assert np.linalg.norm(Q2.T @ Q2 - np.eye(Q2.shape[1])) <= 1e-12
     assert abs(np.linalg.norm(a - Q2 @ B2) - h2[-1]) <= 1e-10
+
+
+def _qbh_worker(rank, world, port, nrb, out_dir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from _dist_numpy import qb_hierarchical_rowsharded_np
+
+    a = _matrix(128, 48)
+    base = 128 // nrb
+    slabs = [a[t * base:(t + 1) * base] if t < nrb - 1 else a[t * base:] for t in range(nrb)]
+    L = nrb // world
+    Q, B = qb_hierarchical_rowsharded_np(slabs[rank * L:(rank + 1) * L], nrb, 4, 2, 1, seed=3)
+    np.savez(os.path.join(out_dir, f"qh{rank}.npz"), Q=Q, B=B)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,nrb", [(2, 2), (2, 4), (4, 4)])
+def test_rowsharded_hierarchical_qb_matches_single_process(tmp_path, world, nrb):
+    """qb_hierarchical over ranks (csrc/dist.cu, mirrored in numpy over gloo):
+    local subtree merges, the allgather of subtree-root B's and the replicated
+    upper merges reproduce the single-process tree exactly."""
+    from _dist_numpy import qb_hierarchical_np
+
+    mp.spawn(_qbh_worker, args=(world, _free_port(), nrb, str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(os.path.join(tmp_path, f"qh{r}.npz")) for r in range(world)]
+    Q = np.vstack([x["Q"] for x in parts])
+    for x in parts[1:]:
+        assert np.array_equal(x["B"], parts[0]["B"])
+    a = _matrix(128, 48)
+    base = 128 // nrb
+    slabs = [a[t * base:(t + 1) * base] if t < nrb - 1 else a[t * base:] for t in range(nrb)]
+    Qs, Bs = qb_hierarchical_np(slabs, 4, 2, 1, seed=3)
+    assert np.max(np.abs(Q - Qs)) <= 1e-12 and np.max(np.abs(parts[0]["B"] - Bs)) <= 1e-12

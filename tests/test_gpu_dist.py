@@ -164,3 +164,24 @@ def test_native_rowsharded_qb_world1_matches_engine_and_oracle(orc):
     np.testing.assert_allclose(got["history"], want["history"], rtol=1e-6, atol=1e-13)
     assert rel_fro(got["q"] @ got["b"], a) <= 2.0 * rel_fro(want["q"] @ want["b"], a) + 1e-14
     assert np.linalg.norm(got["q"].T @ got["q"] - np.eye(got["ell"])) <= 1e-12
+
+
+@pytest.mark.parametrize("nrb", [2, 4])
+def test_native_hierarchical_qb_world1_matches_single_gpu(nrb):
+    """qb_hierarchical over the ranks (csrc/dist.cu) on a 1-rank NCCL
+    communicator: the rank holds every slab, merges its subtree locally and
+    goes through the allgather path; Q, B equal the single-GPU driver (same
+    reference substreams)."""
+    from helpers import make_test_matrix, rel_fro
+
+    eng = R.Engine(0)
+    m, n, b, M = 400, 150, 8, 3
+    a = make_test_matrix(m, n, np.exp(-np.arange(150) / 8.0), seed=22)
+    comm = _world1_comm(eng)
+    try:
+        got = eng.qb_hierarchical_rowsharded(comm.handle, a, m, nrb, b, M, 1, R.Rng(31))
+    finally:
+        comm.close()
+    want = eng.qb_hierarchical(a, nrb, b, M, 1, R.Rng(31))
+    assert rel_fro(got["q"], want["q"]) <= 1e-12 and rel_fro(got["b"], want["b"]) <= 1e-12
+    assert abs(got["final_residual"] - want["final_residual"]) <= 1e-10 * want["final_residual"]
