@@ -839,34 +839,187 @@ inline TestMatrix gen_test_matrix(int m, int n, const SpectrumSpec& spec, RngSta
 }
 
 // ------------------------------------------------------------ report.hpp ---
-struct ErrorReport {  // report.hpp:73-93 (numeric fields)
+enum class FactorizationKind { kSvd, kId, kCur };
+struct NnzCounts {
+    std::vector<std::pair<std::string, double>> parts;
+    double total = 0.0;
+};
+// report.hpp:30-58 storage accounting (plain arithmetic)
+inline NnzCounts nnz_report(FactorizationKind kind, int m, int n, int k, double density = 1.0) {
+    if (m < 1 || n < 1 || k < 1 || k > std::min(m, n))
+        throw DimensionError(detail::msg("nnz_report: invalid shape m=%d n=%d k=%d", m, n, k));
+    if (!(density > 0.0) || density > 1.0)
+        throw DimensionError(detail::msg("nnz_report: density %g outside (0, 1]", density));
+    const double dm = m, dn = n, dk = k;
+    NnzCounts out;
+    switch (kind) {
+        case FactorizationKind::kSvd: out.parts = {{"U", dk * dm}, {"sigma", dk}, {"V", dk * dn}}; break;
+        case FactorizationKind::kId:
+            out.parts = {{"C", density * dk * dm}, {"V_interp", dk * (dn - dk)}, {"indices", dk}};
+            break;
+        case FactorizationKind::kCur:
+            out.parts = {{"C", density * dk * dm}, {"U", dk * dk}, {"R", density * dk * dn}};
+            break;
+    }
+    for (const auto& p : out.parts) out.total += p.second;
+    return out;
+}
+struct ErrorReport {  // report.hpp:73-93
     std::string method;
     int m = 0, n = 0, k = 0;
+    std::string params;
     double rel_frobenius_error = 0.0;
     double rel_spectral_error = 0.0;
     double fro_floor = std::numeric_limits<double>::quiet_NaN();
     double spec_floor = std::numeric_limits<double>::quiet_NaN();
     double spec_bound = std::numeric_limits<double>::quiet_NaN();
+    NnzCounts nnz;
+    double wall_seconds = 0.0;
 };
-inline ErrorReport verify(const DenseMatrix& a, const SvdFactors& f, const std::vector<double>& sigma_true = {}) {
-    if (f.u.rows() != a.rows() || f.v.rows() != a.cols() || f.u.cols() != f.k || f.v.cols() != f.k ||
-        int(f.sigma.size()) != f.k)
-        throw DimensionError("verify: SVD factor shapes do not match the matrix");
+namespace detail {
+// verify_reconstruction (report.hpp:97-138) for recon = X Y^T on the GPU
+inline ErrorReport verify_xyt(const DenseMatrix& a, const DenseMatrix& x, const DenseMatrix& y, int k,
+                              const char* method, const std::vector<double>& sigma_true) {
     double out[5];
-    detail::check(rlra_verify_svd(detail::ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), detail::ld(a), f.u.data(),
-                                  detail::ld(f.u), f.sigma.data(), f.v.data(), detail::ld(f.v), f.k,
-                                  sigma_true.empty() ? nullptr : sigma_true.data(), int(sigma_true.size()), out));
+    check(rlra_verify_lowrank(ctx(), RLRA_HOST, a.data(), a.rows(), a.cols(), ld(a), x.data(), ld(x), y.data(), ld(y),
+                              k, sigma_true.empty() ? nullptr : sigma_true.data(), int(sigma_true.size()), out));
     ErrorReport r;
-    r.method = "svd";
+    r.method = method;
     r.m = a.rows();
     r.n = a.cols();
-    r.k = f.k;
+    r.k = k;
     r.rel_frobenius_error = out[0];
     r.rel_spectral_error = out[1];
     r.fro_floor = out[2];
     r.spec_floor = out[3];
     r.spec_bound = out[4];
     return r;
+}
+}  // namespace detail
+inline ErrorReport verify(const DenseMatrix& a, const SvdFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.u.rows() != a.rows() || f.v.rows() != a.cols() || f.u.cols() != f.k || f.v.cols() != f.k ||
+        int(f.sigma.size()) != f.k)
+        throw DimensionError("verify: SVD factor shapes do not match the matrix");
+    DenseMatrix us = f.u;
+    scale_columns_inplace(us, f.sigma);
+    ErrorReport r = detail::verify_xyt(a, us, f.v, f.k, "svd", sigma_true);
+    if (f.k > 0) r.nnz = nnz_report(FactorizationKind::kSvd, a.rows(), a.cols(), f.k);
+    return r;
+}
+inline ErrorReport verify(const DenseMatrix& a, const IdFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.v.rows() != a.cols() || f.v.cols() != f.k || f.jc.size() != a.cols())
+        throw DimensionError("verify: column-ID factor shapes do not match the matrix");
+    ErrorReport r = detail::verify_xyt(a, select_columns(a, f.jc, f.k), f.v, f.k, "id", sigma_true);
+    if (f.k > 0) r.nnz = nnz_report(FactorizationKind::kId, a.rows(), a.cols(), f.k);
+    return r;
+}
+inline ErrorReport verify(const DenseMatrix& a, const RowIdFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.w.rows() != a.rows() || f.w.cols() != f.k || f.jr.size() != a.rows())
+        throw DimensionError("verify: row-ID factor shapes do not match the matrix");
+    ErrorReport r = detail::verify_xyt(a, f.w, transpose(select_rows(a, f.jr, f.k)), f.k, "id-row", sigma_true);
+    if (f.k > 0) r.nnz = nnz_report(FactorizationKind::kId, a.cols(), a.rows(), f.k);
+    return r;
+}
+inline ErrorReport verify(const DenseMatrix& a, const CurFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.c.rows() != a.rows() || f.r.cols() != a.cols() || f.c.cols() != f.k || f.r.rows() != f.k ||
+        f.u.rows() != f.k || f.u.cols() != f.k)
+        throw DimensionError("verify: CUR factor shapes do not match the matrix");
+    ErrorReport r = detail::verify_xyt(a, f.c, transpose(matmul(f.u, f.r)), f.k, "cur", sigma_true);
+    if (f.k > 0) r.nnz = nnz_report(FactorizationKind::kCur, a.rows(), a.cols(), f.k);
+    return r;
+}
+inline ErrorReport verify(const DenseMatrix& a, const QbFactors& f, const std::vector<double>& sigma_true = {}) {
+    if (f.q.rows() != a.rows() || f.b.cols() != a.cols() || f.q.cols() != f.ell || f.b.rows() != f.ell)
+        throw DimensionError("verify: QB factor shapes do not match the matrix");
+    ErrorReport r = detail::verify_xyt(a, f.q, transpose(f.b), f.ell, "qb", sigma_true);
+    if (f.ell > 0) {
+        const double dm = a.rows(), dn = a.cols(), dl = f.ell;
+        r.nnz.parts = {{"Q", dl * dm}, {"B", dl * dn}};
+        r.nnz.total = dl * (dm + dn);
+    }
+    return r;
+}
+// report.hpp:210-244 CSV emission
+inline std::string csv_header() {
+    return "method,m,n,k,params,rel_fro_error,rel_spec_error,fro_floor,spec_floor,spec_bound,nnz_total,seconds";
+}
+namespace detail {
+inline std::string csv_num(double v) { return std::isnan(v) ? std::string() : msg("%.17g", v); }
+}  // namespace detail
+inline std::string csv_row(const ErrorReport& r) {
+    std::string row = r.method;
+    row += detail::msg(",%d,%d,%d,", r.m, r.n, r.k);
+    row += r.params;
+    for (double v : {r.rel_frobenius_error, r.rel_spectral_error, r.fro_floor, r.spec_floor, r.spec_bound,
+                     r.nnz.total}) {
+        row += ',';
+        row += detail::csv_num(v);
+    }
+    row += detail::msg(",%.6f", r.wall_seconds);
+    return row;
+}
+
+// ---------------------------------------------------- io.hpp: spectrum ---
+inline void save_spectrum(const std::string& path, const std::vector<double>& sigma) {  // io.hpp:114-121
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw IoError(detail::msg("save_spectrum: cannot open '%s' for writing", path.c_str()));
+    bool ok = true;
+    for (double v : sigma) ok = ok && std::fprintf(f, "%.17g\n", v) > 0;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw IoError(detail::msg("save_spectrum: write to '%s' failed", path.c_str()));
+}
+inline std::vector<double> load_spectrum(const std::string& path) {  // io.hpp:123-147
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw IoError(detail::msg("load_spectrum: cannot open '%s'", path.c_str()));
+    std::vector<double> sigma;
+    std::string line;
+    int lineno = 0, c = 0;
+    bool more = true;
+    while (more) {
+        line.clear();
+        while ((c = std::fgetc(f)) != EOF && c != '\n') line.push_back(char(c));
+        more = c != EOF;
+        if (!more && line.empty()) break;
+        ++lineno;
+        if (line.empty()) continue;
+        const char* begin = line.c_str();
+        char* end = nullptr;
+        const double v = std::strtod(begin, &end);
+        if (end == begin) {
+            std::fclose(f);
+            throw IoError(detail::msg("load_spectrum: '%s' line %d is not a number", path.c_str(), lineno));
+        }
+        std::size_t pos = std::size_t(end - begin);
+        while (pos < line.size() && (line[pos] == ' ' || line[pos] == '\r')) ++pos;
+        if (pos != line.size() || !std::isfinite(v)) {
+            std::fclose(f);
+            throw IoError(detail::msg("load_spectrum: '%s' line %d is not a finite number", path.c_str(), lineno));
+        }
+        sigma.push_back(v);
+    }
+    std::fclose(f);
+    return sigma;
+}
+
+// ---------------------------------------------------- qb.hpp: qb_single ---
+inline QbFactors qb_single(const DenseMatrix& a, double tol, int max_rank, RngState& rng) {  // qb.hpp:43-95
+    const int m = a.rows(), n = a.cols();
+    const int cap = std::max(1, max_rank);
+    DenseMatrix Q(m, cap), B(cap, n);
+    int ell = 0, reached = 0, nh = 0;
+    double fin = 0.0;
+    std::vector<double> hist(static_cast<std::size_t>(cap));
+    rlra_omega om = detail::omega_from(rng, false);
+    detail::check(rlra_qb_single(detail::ctx(), RLRA_HOST, a.data(), m, n, detail::ld(a), tol, max_rank, &om, Q.data(),
+                                 std::max(1, m), B.data(), cap, &ell, hist.data(), &nh, &fin, &reached));
+    QbFactors f;
+    f.q = submatrix(Q, 0, m, 0, ell);
+    f.b = submatrix(B, 0, ell, 0, n);
+    f.ell = ell;
+    f.residual_report.final_residual = fin;
+    f.residual_report.tolerance_reached = reached != 0;
+    f.residual_report.history.assign(hist.begin(), hist.begin() + nh);
+    return f;
 }
 
 }  // namespace rlra

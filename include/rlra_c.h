@@ -143,6 +143,13 @@ rlra_status rlra_qb_hierarchical(rlra_ctx* ctx, int loc, const double* a, int m,
                                  int num_row_blocks, int blk, int num_blocks, int q_power, const rlra_omega* omega,
                                  double* q, int64_t ldq, double* b, int64_t ldb, double* final_residual);
 
+/* qb_single (qb.hpp:43-95): one direction at a time until ||A - QB||_F < tol
+ * or max_rank columns; q m x max_rank, b max_rank x n (ld >= max_rank); Omega
+ * draws are n x 1 columns in the reference's order (redraws included). */
+rlra_status rlra_qb_single(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, double tol,
+                           int max_rank, const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,
+                           int* ell, double* hist, int* nhist, double* final_residual, int* reached);
+
 /* ------------------------------------------- I/O, generator, verifier ---
  * Binary matrix files in the reference format (io.hpp:40-109): int32 rows,
  * int32 cols (little-endian), then rows*cols doubles row by row; exactly
@@ -163,6 +170,12 @@ rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const dou
  * start vectors from RngState 0x5bd1e995 as the reference), out[2..4] the
  * Frobenius floor, spectral floor and sketch bound (NaN without sigma_true,
  * r = 0). */
+/* verify_reconstruction (report.hpp:97-138) for recon = X Y^T (X m x k,
+ * Y n x k): the ID (X = C, Y = V), CUR (X = C, Y = (U R)^T) and QB (X = Q,
+ * Y = B^T) reports.  out as rlra_verify_svd. */
+rlra_status rlra_verify_lowrank(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* x,
+                                int64_t ldx, const double* y, int64_t ldy, int k, const double* sigma_true, int r,
+                                double out[5]);
 rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* u,
                             int64_t ldu, const double* sigma, const double* v, int64_t ldv, int k,
                             const double* sigma_true, int r, double out[5]);

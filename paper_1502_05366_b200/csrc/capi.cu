@@ -649,6 +649,48 @@ rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const dou
     });
 }
 
+rlra_status rlra_verify_lowrank(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* x,
+                                int64_t ldx, const double* y, int64_t ldy, int k, const double* sigma_true, int r,
+                                double out[5]) {
+    return guard(ctx, [&](Context& C) {
+        need(out, "out");
+        if (k < 0 || k > std::min(m, n)) raise(RLRA_EDIM, "verify: factor shapes do not match the matrix");
+        In A(C, loc, a, m, n, lda, "a"), X(C, loc, x, m, k, ldx, "x"), Y(C, loc, y, n, k, ldy, "y");
+        std::vector<double> st;
+        if (r > 0) st.assign(sigma_true, sigma_true + r);
+        const VerifyReport rep = verify_lowrank(C, A.m, X.m, Y.m, k, st);
+        out[0] = rep.rel_frobenius_error;
+        out[1] = rep.rel_spectral_error;
+        out[2] = rep.fro_floor;
+        out[3] = rep.spec_floor;
+        out[4] = rep.spec_bound;
+    });
+}
+
+rlra_status rlra_qb_single(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, double tol,
+                           int max_rank, const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,
+                           int* ell, double* hist, int* nhist, double* final_residual, int* reached) {
+    return guard(ctx, [&](Context& C) {  // qb.hpp:44-50 checks and messages
+        if (tol <= 0.0) raise(RLRA_EDIM, fmt("qb_single needs tol > 0 (got %g)", tol));
+        const int rmax = std::min(m, n);
+        if (max_rank < 1 || max_rank > rmax)
+            raise(RLRA_EDIM, fmt("max_rank %d outside [1, min(m,n) = %d]", max_rank, rmax));
+        OmegaSource om = omega_of(omega);
+        In A(C, loc, a, m, n, lda, "a");
+        Out Q(C, loc, q, m, max_rank, ldq, "q"), B(C, loc, b, max_rank, n, ldb, "b");
+        const QbOut r = qb_single(C, A.m, tol, max_rank, om, Q.m, B.m);
+        Q.finish(C);
+        B.finish(C);
+        sync(C);
+        if (ell) *ell = r.ell;
+        if (nhist) *nhist = int(r.hist.size());
+        if (hist)
+            for (size_t i = 0; i < r.hist.size(); ++i) hist[i] = r.hist[i];
+        if (final_residual) *final_residual = r.final_residual;
+        if (reached) *reached = r.reached ? 1 : 0;
+    });
+}
+
 rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* u,
                             int64_t ldu, const double* sigma, const double* v, int64_t ldv, int k,
                             const double* sigma_true, int r, double out[5]) {

@@ -306,47 +306,38 @@ void gen_test_matrix(Context& ctx, const std::vector<double>& sigma, uint64_t se
     }
 }
 
-VerifyReport verify_svd(Context& ctx, const DMat& A, const DMat& U, const double* sigma, const DMat& V, int k,
-                        const std::vector<double>& sigma_true) {
+VerifyReport verify_lowrank(Context& ctx, const DMat& A, const DMat& X, const DMat& Y, int k,
+                            const std::vector<double>& sigma_true) {
     const int m = int(A.rows), n = int(A.cols);
     VerifyReport r;
-    DMatBuf US(ctx, m, std::max(k, 1));
-    if (k > 0) {
-        copy_mat(ctx, U.block(0, 0, m, k), US.m.block(0, 0, m, k));
-        scale_cols_by_kernel<<<grid_for(ctx, int64_t(m) * k), 256, 0, ctx.stream>>>(US.m.p, US.m.ld, m, k, sigma);
-        RLRA_LAUNCH_CHECK();
-        ++ctx.launches;
-    }
     Buf sq(ctx, sizeof(double) * 2);
     sum_squares(ctx, A, sq.d());
-    double diff2;
-    if (k > 0) {
+    if (k > 0) {  // ||A - X Y^T||^2 through the fused residual GEMM
         GemmOpts o;
         o.epi = EPI_RESID;
         o.R = A.p;
         o.ldr = A.ld;
         o.resid_sq = sq.d() + 1;
-        gemm(ctx, Op::N, Op::T, m, n, k, 1.0, US.m.p, US.m.ld, V.p, V.ld, 0.0, nullptr, 0, o);
+        gemm(ctx, Op::N, Op::T, m, n, k, 1.0, X.p, X.ld, Y.p, Y.ld, 0.0, nullptr, 0, o);
     } else {
         sum_squares(ctx, A, sq.d() + 1);
     }
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx.stream));
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
     const double fro_a = std::sqrt(ctx.h_scalars[0]);
-    diff2 = ctx.h_scalars[1];
-    const double fro_diff = std::sqrt(diff2);
+    const double fro_diff = std::sqrt(ctx.h_scalars[1]);
     r.rel_frobenius_error = fro_diff / (fro_a > 0.0 ? fro_a : 1.0);
     if (fro_diff == 0.0) {
         r.rel_spectral_error = 0.0;
     } else {
         rlra_rng est;
         rlra_rng_seed(&est, 0x5bd1e995u);  // report.hpp:116: fixed, reproducible
-        const DMat USk = US.m.block(0, 0, m, k), Vk = V.block(0, 0, n, k);
+        const DMat Xk = X.block(0, 0, m, k), Yk = Y.block(0, 0, n, k);
         const double spec_a = spectral_est(ctx, A, nullptr, nullptr, 60, &est);
-        const double spec_d = spectral_est(ctx, A, k > 0 ? &USk : nullptr, k > 0 ? &Vk : nullptr, 60, &est);
+        const double spec_d = spectral_est(ctx, A, k > 0 ? &Xk : nullptr, k > 0 ? &Yk : nullptr, 60, &est);
         r.rel_spectral_error = spec_d / (spec_a > 0.0 ? spec_a : 1.0);
     }
-    if (!sigma_true.empty()) {
+    if (!sigma_true.empty()) {  // report.hpp:123-136
         const int rr = int(sigma_true.size());
         double tail2 = 0.0, all2 = 0.0;
         for (int j = 0; j < rr; ++j) {
@@ -360,6 +351,100 @@ VerifyReport verify_svd(Context& ctx, const DMat& A, const DMat& U, const double
         r.spec_bound = std::sqrt(double(k) * n) * sig_next / sig1;
     }
     return r;
+}
+
+VerifyReport verify_svd(Context& ctx, const DMat& A, const DMat& U, const double* sigma, const DMat& V, int k,
+                        const std::vector<double>& sigma_true) {
+    const int m = int(A.rows);
+    DMatBuf US(ctx, m, std::max(k, 1));
+    if (k > 0) {
+        copy_mat(ctx, U.block(0, 0, m, k), US.m.block(0, 0, m, k));
+        scale_cols_by_kernel<<<grid_for(ctx, int64_t(m) * k), 256, 0, ctx.stream>>>(US.m.p, US.m.ld, m, k, sigma);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+    }
+    return verify_lowrank(ctx, A, US.m, V, k, sigma_true);
+}
+
+// qb_single (qb.hpp:43-95): one Gaussian direction per step, projected
+// against the captured basis, normalised, B row = y^T R, R -= y b^T; GEMV
+// and rank-1 kernels over the residual copy (a BLAS-2 method by design)
+__global__ void rank1_sub_kernel(double* R, int64_t ldr, int m, int n, const double* y, const double* b) {
+    const int64_t tot = int64_t(m) * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % m), j = int(e / m);
+        R[i + int64_t(j) * ldr] -= y[i] * b[j];
+    }
+}
+
+QbOut qb_single(Context& ctx, const DMat& A, double tol, int max_rank, OmegaSource& om, const DMat& Q, const DMat& B) {
+    const int m = int(A.rows), n = int(A.cols);
+    DMatBuf R(ctx, m, n);
+    copy_mat(ctx, A, R.m);
+    Buf om_d(ctx, sizeof(double) * n), t(ctx, sizeof(double) * std::max(max_rank, 1)), tmp(ctx, sizeof(double) * m),
+        sc(ctx, sizeof(double) * 2);
+    std::vector<double> h(n);
+    QbOut out;
+    double resid = 0.0;
+    {
+        Buf s2(ctx, sizeof(double));
+        sum_squares(ctx, R.m, s2.d());
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, s2.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        resid = std::sqrt(ctx.h_scalars[0]);
+    }
+    for (;;) {
+        if (resid < tol) {
+            out.reached = true;
+            break;
+        }
+        if (out.ell >= max_rank) break;
+        const int l = out.ell;
+        double* y = Q.p + int64_t(l) * Q.ld;
+        double ynorm = 0.0;
+        for (int tries = 0;; ++tries) {
+            const int draw = om.next_draw++;
+            if (om.o->mode == RLRA_OMEGA_PHILOX) {
+                DMat od{om_d.d(), n, 1, std::max(n, 1)};
+                philox_fill(ctx, od, om.o->seed, draw, 0);
+            } else {
+                if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
+                om.o->fill(om.o->user, draw, n, 1, h.data());
+                RLRA_CUDA(cudaMemcpyAsync(om_d.p, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+            }
+            gemv(ctx, false, R.m, om_d.d(), y);  // y = R omega
+            if (l > 0) {                          // y -= Q (Q^T y)
+                const DMat Ql = Q.block(0, 0, m, l);
+                gemv(ctx, true, Ql, y, t.d());
+                gemv(ctx, false, Ql, t.d(), tmp.d());
+                axpy_mat_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(y, m, tmp.d(), m, m, 1, -1.0);
+                RLRA_LAUNCH_CHECK();
+            }
+            ynorm = std::sqrt(sq_norm(ctx, y, m, sc.d()));
+            if (ynorm >= 1e-14 * resid) break;
+            if (tries + 1 >= 64)
+                raise(RLRA_ENUM, fmt("qb_single: no new direction found in 64 draws (residual %g)", resid));
+        }
+        scale_vec_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(y, m, sc.d());  // sc holds ||y||^2
+        RLRA_LAUNCH_CHECK();
+        // b = y^T R -> row l of B (stride B.ld), then R -= y b^T
+        Buf bj(ctx, sizeof(double) * n);
+        gemv(ctx, true, R.m, y, bj.d());
+        RLRA_CUDA(cudaMemcpy2DAsync(B.p + l, sizeof(double) * B.ld, bj.p, sizeof(double), sizeof(double), n,
+                                    cudaMemcpyDeviceToDevice, ctx.stream));
+        rank1_sub_kernel<<<grid_for(ctx, int64_t(m) * n), 256, 0, ctx.stream>>>(R.m.p, R.m.ld, m, n, y, bj.d());
+        RLRA_LAUNCH_CHECK();
+        ctx.launches += 3;
+        ++out.ell;
+        Buf s2(ctx, sizeof(double));
+        sum_squares(ctx, R.m, s2.d());
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, s2.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        resid = std::sqrt(ctx.h_scalars[0]);
+        out.hist.push_back(resid);
+    }
+    out.final_residual = resid;
+    return out;
 }
 
 }  // namespace rlra_b200

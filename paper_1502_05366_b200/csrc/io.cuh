@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "engine.cuh"
 
 namespace rlra_b200 {
 
@@ -30,8 +31,15 @@ struct VerifyReport {
     double rel_spectral_error = 0.0;
     double fro_floor = NAN, spec_floor = NAN, spec_bound = NAN;
 };
-// report.hpp:97-138 verify(a, SvdFactors, sigma_true); sigma on the device
+// report.hpp:97-138 verify_reconstruction for recon = X Y^T (X m x k, Y n x k)
+VerifyReport verify_lowrank(Context& ctx, const DMat& A, const DMat& X, const DMat& Y, int k,
+                            const std::vector<double>& sigma_true);
+// report.hpp:142-154 verify(a, SvdFactors, sigma_true); sigma on the device
 VerifyReport verify_svd(Context& ctx, const DMat& A, const DMat& U, const double* sigma, const DMat& V, int k,
                         const std::vector<double>& sigma_true);
+
+// qb.hpp:43-95 qb_single: Q (m x max_rank), B (max_rank x n, ld >= max_rank)
+QbOut qb_single(Context& ctx, const DMat& A, double tol, int max_rank, OmegaSource& om, const DMat& Q,
+                const DMat& B);
 
 }  // namespace rlra_b200

@@ -111,3 +111,15 @@ def test_cpp_dropin_headers_compile(tmp_path):
     res = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
                           str(src)], capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
+
+
+def test_reference_cli_compiles_against_dropin_headers(tmp_path):
+    """The reference's UNMODIFIED command-line driver compiles against the
+    drop-in headers (include/rlra) with the self-written CLI11 subset
+    (tools/cli11) — the source-level drop-in check."""
+    src = "/root/reference/proj/tools/rlra_cli.cpp"
+    if not os.path.exists(src) or not shutil.which("g++"):
+        pytest.skip("reference source or g++ absent")
+    res = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-I",
+                          os.path.join(ROOT, "tools", "cli11"), src], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr[-3000:]
