@@ -1,6 +1,8 @@
 // jacobi.cu — one-sided Jacobi SVD and two-sided Jacobi eigensolver.
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "jacobi.cuh"
 #include "reduce.cuh"
@@ -435,6 +437,7 @@ struct GramJacArgs {
     int nb;      // column blocks (even)
     int* flags;  // [0..2] rotated-in-sweep, [3] status, [4] sweeps used
     int inner_cap;
+    long long* phase_clk;  // optional: CTA 0's clock64 per phase (RLRA_JACOBI_PHASES)
 };
 
 __global__ void __launch_bounds__(256) gram_jacobi_kernel(GramJacArgs a) {
@@ -640,6 +643,354 @@ __global__ void __launch_bounds__(256) gram_jacobi_kernel(GramJacArgs a) {
     if (blockIdx.x == 0 && t == 0) flags[4] = sweep;
 }
 
+// ------------------------ Gram block Jacobi, shared-memory-resident pairs ---
+// For l x l inputs with l up to ~1400 (the R-hat of rsvd_v2 at C1/C4/C5).
+// Columns in blocks of BW; a sweep is nb-1 "cross" rounds (block pairs from a
+// round-robin tournament; inside a visit BW steps rotate every (I_k, J_k+s)
+// column pair) plus one "intra" round (blocks 2g, 2g+1; BW-1 tournament
+// steps over the pairs inside each block), so every column pair is rotated
+// exactly once per sweep — a cyclic ordering, as the reference's
+// (core/jacobi.hpp:164-199), with its rotation formula, skip rule and
+// "sweep without rotations" stop.  Per visit one CTA
+//   1. stages the 2*BW columns in shared memory once and forms
+//      G = W_p^T W_p on DMMA (each warp a row slice, upper 8x8 tiles; a
+//      tile's two operand fragments are the same column-block loads);
+//   2. runs the visit's steps on G: thread (k, l) owns the 2x2 block of
+//      pairs (k, l), computes both pairs' rotations itself from the diagonal
+//      entries (no serial parameter phase), updates its G block into the
+//      other buffer and its J block in place — one barrier per step;
+//   3. W_p J on DMMA straight from shared memory to W, and V_p <- V_p J.
+// The one-sided variant (block_jacobi_kernel) re-reads all staged columns
+// in every inner round and is shared-memory-bandwidth bound.
+template <int BW>
+struct BGram {
+    static constexpr int C2 = 2 * BW;       // columns per pair
+    static constexpr int NB8 = C2 / 8;      // 8-column blocks
+    static constexpr int NT = NB8 * (NB8 + 1) / 2;  // upper 8x8 Gram tiles
+    static constexpr int GP = C2 + 1;       // G / J pitch
+    static constexpr int JP = C2 + 4;       // J pitch for the DMMA B fragments
+    static constexpr int KF = C2 / 4;       // k-fragments of the apply
+};
+
+__host__ __device__ inline int bgram_rows(int m) { return (m + 31) & ~31; }    // 8 warps x k-steps of 4
+__host__ __device__ inline int bgram_pitch(int m) { return bgram_rows(m) + 4; }  // == 4 mod 16: conflict-free
+
+template <int BW>
+size_t bgram_smem(int m) {
+    using B = BGram<BW>;
+    return sizeof(double) * (size_t(B::C2) * bgram_pitch(m) + 3 * B::C2 * B::GP + B::C2 * B::JP + 8 * B::NT * 64);
+}
+
+// 1/x and 1/sqrt(x) from the MUFU approximations (MUFU.RCP64H / RSQ64H, no
+// special-case subroutine) plus three Newton steps: ~1 ulp on normal inputs
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    double e = fma(-hx * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-hx * y, y, 0.5);
+    y = fma(y, e, y);
+    const double r = fma(-x, y * y, 1.0);  // last step on the full residual
+    return fma(0.5 * y, r, y);
+}
+
+// The reference rotation (core/jacobi.hpp:170-180) for the pair with Gram
+// entries (app, aqq, apq): skip unless |apq| > eps sqrt(app aqq); then
+// t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (aqq - app) / (2 apq),
+// c = 1 / sqrt(1 + t^2), s = t c.
+// Fast form, branch-free (the inner step is one dependent chain, so two of
+// them interleave): t = |e| / (|d| + hypot(d, e)) with d = aqq - app,
+// e = 2 apq — the same t — and the skip test on squares.  Returns false when
+// a product is near over/underflow; the caller then takes jac_rotation_ref.
+__device__ __forceinline__ bool jac_rotation_fast(double app, double aqq, double apq, double& c, double& s,
+                                                  int& act) {
+    const double pr = app * aqq, d = aqq - app, e = 2.0 * apq;
+    const double h2 = fma(d, d, e * e);
+    const bool ok = pr > 1e-290 && pr < 1e290 && h2 > 1e-290 && h2 < 1e290;
+    act = apq * apq > 1e-30 * pr;
+    const double h = h2 * rsqrt_nr(h2);
+    const double tm = fabs(e) * rcp_nr(fabs(d) + h);
+    const double t = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? tm : -tm;
+    const double cc = rsqrt_nr(fma(t, t, 1.0));
+    c = act ? cc : 1.0;
+    s = act ? t * cc : 0.0;
+    return ok;
+}
+__device__ __noinline__ int jac_rotation_ref(double app, double aqq, double apq, double& c, double& s) {
+    c = 1.0;
+    s = 0.0;
+    if (!(app != 0.0 && aqq != 0.0 && fabs(apq) > 1e-15 * sqrt(app * aqq))) return 0;
+    const double zeta = (aqq - app) / (2.0 * apq);
+    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    c = 1.0 / sqrt(1.0 + t * t);
+    s = t * c;
+    return 1;
+}
+
+// pair k of step st in a cross (I_k, J_{k+st}) or intra (tournament inside
+// each block) visit; returns p | q << 8, p < q
+template <int BW>
+__device__ __forceinline__ int bgram_pair(bool intra, int k, int st) {
+    if (!intra) return k | ((BW + (k + st) % BW) << 8);
+    const int half = k / (BW / 2), kk = k % (BW / 2), base = half * BW;
+    const int c1 = base + rr_col(kk, st, BW), c2 = base + rr_col(BW - 1 - kk, st, BW);
+    return min(c1, c2) | (max(c1, c2) << 8);
+}
+
+template <int BW>
+__global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
+    using B = BGram<BW>;
+    constexpr int C2 = B::C2, NB8 = B::NB8, NT = B::NT, GP = B::GP, JP = B::JP, KF = B::KF;
+    static_assert(BW * BW <= 256, "one thread per 2x2 pair block");
+    extern __shared__ double bsm[];
+    const int m = a.m, n = a.n, nb = a.nb;
+    const int Mp = bgram_rows(m), P = bgram_pitch(m);
+    double* Ws = bsm;                               // C2 columns, pitch P
+    double* G0 = Ws + size_t(C2) * P;               // C2 x GP, two buffers
+    double* J = G0 + 2 * C2 * GP;                   // C2 x GP
+    double* Jb = J + C2 * GP;                       // C2 x JP
+    double* Pb = Jb + C2 * JP;                      // 8 warps x NT tiles x 64 partial Grams
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+    volatile int* flags = a.flags;
+    const bool clk = a.phase_clk != nullptr && blockIdx.x == 0 && t == 0;
+    long long ph[6] = {0, 0, 0, 0, 0, 0}, c0 = clock64();
+    auto mark = [&](int i) {
+        if (clk) {
+            const long long c1 = clock64();
+            ph[i] += c1 - c0;
+            c0 = c1;
+        }
+    };
+    int sweep = 0;
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            if (blockIdx.x == 0 && t == 0) flags[3] = RLRA_ECONV;
+            break;
+        }
+        if (blockIdx.x == 0 && t == 0) flags[(sweep + 1) % 3] = 0;
+        for (int r = 0; r < nb; ++r) {
+            const bool intra = r == nb - 1;
+            for (int g = blockIdx.x; g < nb / 2; g += gridDim.x) {
+                int bI = 2 * g, bJ = 2 * g + 1;
+                if (!intra) {
+                    const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
+                    bI = min(b1, b2);
+                    bJ = max(b1, b2);
+                }
+                auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
+                // ---- stage the pair's columns (rows >= m zero) ----------------
+                for (int c = warp; c < C2; c += 8) {
+                    const int gc = gcol(c);
+                    double* dst = Ws + size_t(c) * P;
+                    if (gc < n) {
+                        const double* src = a.W + int64_t(gc) * a.ldw;
+                        for (int i = lane; i < m; i += 32) {
+                            const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src + i));
+                        }
+                        for (int i = m + lane; i < Mp; i += 32) dst[i] = 0.0;
+                    } else {
+                        for (int i = lane; i < Mp; i += 32) dst[i] = 0.0;
+                    }
+                }
+                asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+                __syncthreads();
+                mark(0);
+                // ---- 1. Gram: warp w sums rows [w*Mp/8, (w+1)*Mp/8) ------------
+                {
+                    // two accumulator sets (even / odd k-steps) halve the DMMA chain
+                    double acc[2][NT][2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int u = 0; u < NT; ++u) acc[h][u][0] = acc[h][u][1] = 0.0;
+                    const int k1 = (warp + 1) * (Mp / 8);
+                    for (int k = warp * (Mp / 8); k < k1; k += 8) {  // Mp / 8 is a multiple of 4
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (h == 1 && k + 4 >= k1) break;
+                            double f[NB8];
+#pragma unroll
+                            for (int bb = 0; bb < NB8; ++bb) f[bb] = Ws[(bb * 8 + lr) * P + k + 4 * h + lc];
+                            int u = 0;
+#pragma unroll
+                            for (int bi = 0; bi < NB8; ++bi)
+#pragma unroll
+                                for (int bj = bi; bj < NB8; ++bj, ++u)
+                                    jac_dmma(acc[h][u][0], acc[h][u][1], f[bi], f[bj]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < NT; ++u) {
+                        Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc] = acc[0][u][0] + acc[1][u][0];
+                        Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc + 1] = acc[0][u][1] + acc[1][u][1];
+                    }
+                }
+                __syncthreads();
+                for (int e = t; e < NT * 64; e += 256) {
+                    const int u = e >> 6, w = e & 63;
+                    int bi = 0, rem = u;
+                    while (rem >= NB8 - bi) rem -= NB8 - bi++;
+                    const int bj = bi + rem;
+                    double s = 0.0;
+#pragma unroll
+                    for (int ww = 0; ww < 8; ++ww) s += Pb[(ww * NT + u) * 64 + w];
+                    const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
+                    G0[row * GP + col] = s;
+                    G0[col * GP + row] = s;
+                }
+                for (int e = t; e < C2 * C2; e += 256) J[(e / C2) * GP + e % C2] = (e / C2 == e % C2) ? 1.0 : 0.0;
+                __syncthreads();
+                mark(1);
+                // ---- 2. the visit's steps on G: thread (k, l) owns pair block (k, l)
+                int rot = 0;
+                {
+                    const int k = t / BW, l = t % BW;
+                    const bool own = t < BW * BW;
+                    const int nsteps = intra ? BW - 1 : BW;
+                    for (int st = 0; st < nsteps; ++st) {
+                        const double* Gc = G0 + (st & 1) * C2 * GP;
+                        double* Gn = G0 + ((st & 1) ^ 1) * C2 * GP;
+                        int act = 0;
+                        if (own) {
+                            const int pqk = bgram_pair<BW>(intra, k, st), pql = bgram_pair<BW>(intra, l, st);
+                            const int pk = pqk & 255, qk = pqk >> 8, pl = pql & 255, ql = pql >> 8;
+                            // (a padded column's Gram entries are 0: never rotated)
+                            const double kpp = Gc[pk * GP + pk], kqq = Gc[qk * GP + qk], kpq = Gc[pk * GP + qk];
+                            const double lpp = Gc[pl * GP + pl], lqq = Gc[ql * GP + ql], lpq = Gc[pl * GP + ql];
+                            double ck, sk, cl, sl;
+                            int ak, al;
+                            const bool okk = jac_rotation_fast(kpp, kqq, kpq, ck, sk, ak);
+                            const bool okl = jac_rotation_fast(lpp, lqq, lpq, cl, sl, al);
+                            if (!okk) ak = jac_rotation_ref(kpp, kqq, kpq, ck, sk);
+                            if (!okl) al = jac_rotation_ref(lpp, lqq, lpq, cl, sl);
+                            act = (k == l) ? ak : 0;
+                            if (al) {  // J <- J R_l on rows {pk, qk}
+                                const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
+                                const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
+                                J[pk * GP + pl] = cl * j0 - sl * j1;
+                                J[pk * GP + ql] = sl * j0 + cl * j1;
+                                J[qk * GP + pl] = cl * j2 - sl * j3;
+                                J[qk * GP + ql] = sl * j2 + cl * j3;
+                            }
+                            if (k <= l) {  // G block (k, l) <- R_k^T B R_l, mirrored
+                                double b00 = Gc[pk * GP + pl], b01 = Gc[pk * GP + ql];
+                                double b10 = Gc[qk * GP + pl], b11 = Gc[qk * GP + ql];
+                                if (al) {
+                                    const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
+                                    const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
+                                    b00 = x0, b01 = x1, b10 = x2, b11 = x3;
+                                }
+                                if (ak) {
+                                    const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
+                                    const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
+                                    b00 = y0, b01 = y1, b10 = y2, b11 = y3;
+                                }
+                                Gn[pk * GP + pl] = b00;
+                                Gn[pk * GP + ql] = b01;
+                                Gn[qk * GP + pl] = b10;
+                                Gn[qk * GP + ql] = b11;
+                                Gn[pl * GP + pk] = b00;
+                                Gn[ql * GP + pk] = b01;
+                                Gn[pl * GP + qk] = b10;
+                                Gn[ql * GP + qk] = b11;
+                            }
+                        }
+                        rot |= __syncthreads_or(act);
+                    }
+                }
+                mark(2);
+                if (!rot) continue;  // uniform across the CTA
+                if (t == 0) flags[sweep % 3] = 1;
+                for (int e = t; e < C2 * C2; e += 256) Jb[(e / C2) * JP + e % C2] = J[(e / C2) * GP + e % C2];
+                __syncthreads();
+                // ---- 3. W_p <- W_p J (shared -> global) and V_p <- V_p J ------
+                double bf[KF][NB8];
+#pragma unroll
+                for (int kf = 0; kf < KF; ++kf)
+#pragma unroll
+                    for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
+                int ocol[NB8][2];
+#pragma unroll
+                for (int ct = 0; ct < NB8; ++ct)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(ct * 8 + 2 * lc + h);
+                for (int sl0 = 2 * warp; sl0 < Mp / 8; sl0 += 16) {  // Mp / 8 is a multiple of 4
+                    double af[2][KF];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+#pragma unroll
+                        for (int kf = 0; kf < KF; ++kf) af[u][kf] = Ws[(4 * kf + lc) * P + (sl0 + u) * 8 + lr];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+                        for (int ct = 0; ct < NB8; ++ct) {
+                            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                            for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                            if (row < m) {
+                                if (ocol[ct][0] < n) a.W[row + int64_t(ocol[ct][0]) * a.ldw] = o0;
+                                if (ocol[ct][1] < n) a.W[row + int64_t(ocol[ct][1]) * a.ldw] = o1;
+                            }
+                        }
+                    }
+                }
+                mark(3);
+                int icol[KF];
+#pragma unroll
+                for (int kf = 0; kf < KF; ++kf) icol[kf] = gcol(4 * kf + lc);
+                constexpr int U = 32 / KF;  // V slabs (8 rows) in flight per warp
+                for (int sl0 = warp * U; sl0 < (n + 7) / 8; sl0 += 8 * U) {
+                    double af[U][KF];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+                        for (int kf = 0; kf < KF; ++kf)
+                            af[u][kf] = (row < n && icol[kf] < n) ? a.V[row + int64_t(icol[kf]) * a.ldv] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+                        for (int ct = 0; ct < NB8; ++ct) {
+                            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                            for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                            if (row < n) {
+                                if (ocol[ct][0] < n) a.V[row + int64_t(ocol[ct][0]) * a.ldv] = o0;
+                                if (ocol[ct][1] < n) a.V[row + int64_t(ocol[ct][1]) * a.ldv] = o1;
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                mark(4);
+            }
+            grid_sync(a.bar);
+            mark(5);
+        }
+        const int rotated = flags[sweep % 3];
+        ++sweep;
+        if (!rotated || n < 2) break;
+    }
+    if (blockIdx.x == 0 && t == 0) flags[4] = sweep;
+    if (clk)
+        for (int i = 0; i < 6; ++i) a.phase_clk[i] = ph[i];
+}
+
 int coop_grid(Context& ctx, const void* kern, int want_blocks) {
     int per_sm = 0;
     RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kJacThreads, 0));
@@ -803,6 +1154,48 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     a.V = V.m.p;
     a.ldv = V.m.ld;
     a.flags = flags.i();
+    // kernel choice: the shared-memory-resident Gram block Jacobi when a
+    // block pair fits (l up to ~1400), else the streaming Gram variant;
+    // RLRA_SVD_KERNEL=bgram|block|gram|onesided forces one (A/B timing)
+    static const int forced = [] {
+        const char* e = std::getenv("RLRA_SVD_KERNEL");
+        if (!e) return 0;
+        const std::string v(e);
+        return v == "bgram" ? 1 : v == "block" ? 2 : v == "gram" ? 3 : v == "onesided" ? 4 : 0;
+    }();
+    constexpr size_t kSmemCap = 220 * 1024;
+    const int bgw = (n > 32 && bgram_smem<16>(m) <= kSmemCap) ? 16 : (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
+    if ((forced == 0 || forced == 1) && bgw > 0) {
+        GramJacArgs g;
+        g.bar = ctx.gbar;
+        g.W = W.m.p;
+        g.ldw = W.m.ld;
+        g.m = m;
+        g.n = n;
+        g.V = V.m.p;
+        g.ldv = V.m.ld;
+        g.nb = ceil_div(n, bgw) + (ceil_div(n, bgw) & 1);
+        g.flags = flags.i();
+        g.inner_cap = 1;
+        static const bool want_clk = std::getenv("RLRA_JACOBI_PHASES") != nullptr;
+        Buf clkb(ctx, want_clk ? sizeof(long long) * 8 : 8);
+        g.phase_clk = want_clk ? reinterpret_cast<long long*>(clkb.p) : nullptr;
+        void* args[] = {&g};
+        const void* kern = bgw == 16 ? (const void*)bgram_jacobi_kernel<16> : (const void*)bgram_jacobi_kernel<8>;
+        const size_t smem = bgw == 16 ? bgram_smem<16>(m) : bgram_smem<8>(m);
+        RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const int grid = std::min(g.nb / 2, ctx.num_sms);
+        RLRA_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), args, smem, ctx.stream));
+        if (want_clk) {
+            long long h[6];
+            RLRA_CUDA(cudaMemcpyAsync(h, clkb.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+            RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+            std::fprintf(stderr, "bgram<%d> m=%d n=%d clocks: stage %lld gram %lld steps %lld applyW %lld applyV %lld sync %lld\n",
+                         bgw, m, n, h[0], h[1], h[2], h[3], h[4], h[5]);
+        }
+        goto launched;
+    }
+    {
     constexpr int BW = 8;
     const size_t bj_smem = sizeof(double) * (size_t(2 * BW) * m + 4 * BW * BW);
     const int nblk = ceil_div(n, BW) + (ceil_div(n, BW) & 1);
@@ -813,7 +1206,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_jacobi_kernel<BW>, BW * 32,
                                                                 bj_smem));
     }
-    if (per_sm > 0 && nblk / 2 <= per_sm * ctx.num_sms) {
+    if (forced != 3 && forced != 4 && per_sm > 0 && nblk / 2 <= per_sm * ctx.num_sms) {
         BlockJacArgs b;
         b.W = W.m.p;
         b.ldw = W.m.ld;
@@ -827,7 +1220,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         void* args[] = {&b};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
                                               args, bj_smem, ctx.stream));
-    } else if (n > 2 * kGB) {
+    } else if (forced != 4 && n > 2 * kGB) {
         // columns too long for shared memory: Gram block Jacobi
         static int gram_cap = 0;
         if (!gram_cap) {
@@ -848,6 +1241,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.nb = ceil_div(n, kGB) + (ceil_div(n, kGB) & 1);
         g.flags = flags.i();
         g.inner_cap = kGInnerCap;
+        g.phase_clk = nullptr;
         void* args[] = {&g};
         const int grid = std::min(g.nb / 2, gram_cap);
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)gram_jacobi_kernel, dim3(grid), dim3(256), args, kGramJacSmem,
@@ -860,6 +1254,8 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)onesided_jacobi_kernel, dim3(G), dim3(kJacThreads),
                                               args, 0, ctx.stream));
     }
+    }
+launched:
     ++ctx.launches;
     colnorm_kernel<<<ceil_div(n, 8), 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, sg.d());
     rank_desc_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(sg.d(), n, rank.i());

@@ -32,6 +32,18 @@ def timed(fn, reps=1):
     return e0.elapsed_time(e1) / reps / 1e3
 
 
+def phases(fn):
+    """Per-phase device ms of one call (engine profile records; nested)."""
+    eng.profile(True)
+    fn()
+    eng.synchronize()
+    out = {}
+    for r in eng.profile_records():
+        out[r["name"]] = round(out.get(r["name"], 0.0) + r["ms"], 3)
+    eng.profile(False)
+    return out
+
+
 def rsvd_cfg(name, m, n, k, p, q, sigma, noise=0.0, seed=1, reps=3):
     A, st = gen_test_matrix_device(eng, m, n, sigma, seed=seed, noise=noise)
     U = torch.empty(m * k, dtype=torch.float64, device="cuda")
@@ -43,6 +55,7 @@ def rsvd_cfg(name, m, n, k, p, q, sigma, noise=0.0, seed=1, reps=3):
                         U.data_ptr(), S.data_ptr(), V.data_ptr())
 
     t = timed(run, reps)
+    ph = phases(run)
     l = k + p
     F = 4.0 * m * n * l * (q + 1)
     rel = eng.device_rel_error(A.data_ptr(), m, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
@@ -50,7 +63,7 @@ def rsvd_cfg(name, m, n, k, p, q, sigma, noise=0.0, seed=1, reps=3):
     top = min(20, k)
     stt = st.cpu().numpy()[:top]
     return dict(config=name, entry="rsvd_v2", m=m, n=n, k=k, p=p, q=q, time_s=t, tflops=F / t / 1e12,
-                rel_fro_error=rel, sigma_top20_rel_vs_true=float(np.max(np.abs(s[:top] - stt) / stt)))
+                rel_fro_error=rel, sigma_top20_rel_vs_true=float(np.max(np.abs(s[:top] - stt) / stt)), phases_ms=ph)
 
 
 def c2():
@@ -71,13 +84,17 @@ def c2():
     U = torch.empty(m * ell, dtype=torch.float64, device="cuda")
     V = torch.empty(n * ell, dtype=torch.float64, device="cuda")
     S = torch.empty(ell, dtype=torch.float64, device="cuda")
-    ts = timed(lambda: eng.device_svd_from_qb(Q.data_ptr(), m, m, B.data_ptr(), n, cap, ell, 0, 0, U.data_ptr(), m,
-                                              S.data_ptr(), V.data_ptr(), n), 1)
+    def svd():
+        eng.device_svd_from_qb(Q.data_ptr(), m, m, B.data_ptr(), n, cap, ell, 0, 0, U.data_ptr(), m, S.data_ptr(),
+                               V.data_ptr(), n)
+
+    ts = timed(svd, 1)
+    ph = phases(svd)
     s = S.cpu().numpy()
     stt = st.cpu().numpy()
     return dict(config="C2", entry="qb_blocked(b=100,M=80,tol=1e-6,q=1) + svd_from_qb(k=0)", m=m, n=n,
                 ell=ell, blocks=len(out["f"]["history"]), final_residual=out["f"]["final_residual"],
-                tolerance_reached=out["f"]["tolerance_reached"], qb_time_s=tq, svd_time_s=ts, time_s=tq + ts,
+                tolerance_reached=out["f"]["tolerance_reached"], qb_time_s=tq, svd_time_s=ts, time_s=tq + ts, svd_phases_ms=ph,
                 sigma_top100_rel_vs_true=float(np.max(np.abs(s[:100] - stt[:100]) / stt[:100])))
 
 
