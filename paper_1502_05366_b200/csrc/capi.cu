@@ -408,13 +408,8 @@ rlra_status rlra_sketch(rlra_ctx* ctx, int loc, int trans, const double* a, int 
         Out Y(C, loc, y, yrows, l, ldy, "y");
         GemmTag tag(C, "gemm_sketch");
         if (o->mode == RLRA_OMEGA_PHILOX) {
-            GemmOpts g;
-            g.philox_b = true;
-            g.seed = o->seed;
-            g.draw = draw;
-            g.krow0 = row0;
-            gemm(C, trans ? Op::T : Op::N, Op::N, yrows, l, orows, 1.0, A.m.p, A.m.ld, nullptr, orows, 0.0,
-                 Y.m.p, Y.m.ld, g);
+            sketch_philox(C, trans ? Op::T : Op::N, yrows, l, orows, A.m.p, A.m.ld, o->seed, draw, row0, Y.m.p,
+                          Y.m.ld);
         } else {
             if (!o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
             std::vector<double> h(size_t(orows) * l);

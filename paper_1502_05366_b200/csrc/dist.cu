@@ -530,12 +530,7 @@ void sketch_left_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0,
     const int draw = om.next_draw++;
     GemmTag tag(ctx, "gemm_sketch");
     if (om.o->mode == RLRA_OMEGA_PHILOX) {
-        GemmOpts o;
-        o.philox_b = true;
-        o.seed = om.o->seed;
-        o.draw = draw;
-        o.krow0 = row0;
-        gemm(ctx, Op::T, Op::N, n, l, mg, 1.0, A.p, A.ld, nullptr, mg, 0.0, Yt.p, Yt.ld, o);
+        sketch_philox(ctx, Op::T, n, l, mg, A.p, A.ld, om.o->seed, draw, row0, Yt.p, Yt.ld);
     } else {
         if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
         std::vector<double> h(size_t(m_total) * l);

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "cpqr.cuh"
 #include "engine.cuh"
@@ -60,22 +61,48 @@ double read_scalar(Context& ctx, const double* d) {
     return ctx.h_scalars[0];
 }
 
+// Philox Omega: materialised by philox_fill (n x l doubles — 82 MB at C5,
+// 0.25% of A's bytes, 13 us of HBM writes) and multiplied by the plain GEMM,
+// which streams A at the power-iteration GEMMs' rate; generating Omega inside
+// the GEMM (GemmOpts::philox_b, the same bits) costs every M-tile the Philox
+// work again and measured 7% slower at C5 (122.7 vs 114.8 ms).
+// RLRA_SKETCH_FUSED=1 selects the in-GEMM generation.
+bool sketch_fused() {
+    static const bool v = [] {
+        const char* e = std::getenv("RLRA_SKETCH_FUSED");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // Y = A * Omega_draw (op_a = N, Omega n x l) or Y = A^T * Omega_draw (op_a =
-// T, Omega m x l).  Philox Omega is generated inside the GEMM; callback Omega
-// is drawn on the host in the reference's order and uploaded.
+// T, Omega m x l).  Callback Omega is drawn on the host in the reference's
+// order and uploaded.
 }  // namespace
+
+void sketch_philox(Context& ctx, Op op_a, int M, int l, int K, const double* A, int64_t lda, uint64_t seed, int draw,
+                   int64_t krow0, double* Y, int64_t ldy) {
+    if (sketch_fused()) {
+        GemmOpts o;
+        o.philox_b = true;
+        o.seed = seed;
+        o.draw = draw;
+        o.krow0 = krow0;
+        gemm(ctx, op_a, Op::N, M, l, K, 1.0, A, lda, nullptr, K, 0.0, Y, ldy, o);
+        return;
+    }
+    DMatBuf Om(ctx, K, l);
+    philox_fill(ctx, Om.m, seed, draw, krow0);
+    gemm(ctx, op_a, Op::N, M, l, K, 1.0, A, lda, Om.m.p, Om.m.ld, 0.0, Y, ldy, GemmOpts{});
+}
 
 void sketch(Context& ctx, Op op_a, const DMat& A, int l, OmegaSource& om, const DMat& Y) {
     const int rows = int(op_a == Op::N ? A.cols : A.rows);
     const int draw = om.next_draw++;
     GemmTag tag(ctx, "gemm_sketch");
     if (om.o->mode == RLRA_OMEGA_PHILOX) {
-        GemmOpts o;
-        o.philox_b = true;
-        o.seed = om.o->seed;
-        o.draw = draw;
         const int M = int(op_a == Op::N ? A.rows : A.cols);
-        gemm(ctx, op_a, Op::N, M, l, rows, 1.0, A.p, A.ld, nullptr, rows, 0.0, Y.p, Y.ld, o);
+        sketch_philox(ctx, op_a, M, l, rows, A.p, A.ld, om.o->seed, draw, 0, Y.p, Y.ld);
         return;
     }
     if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
@@ -203,11 +230,15 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
     const int64_t m = dA.rows, n = dA.cols;
     if (m <= 0 || n <= 0) return;
     if (!ctx.copy_stream) RLRA_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
-    // Omega once (callback mode: the reference's draw, uploaded; Philox: in-register)
+    // Omega once (callback mode: the reference's draw, uploaded; Philox: philox_fill)
     const int draw = om.next_draw++;
     DMatBuf Om;
     std::vector<double> h;
-    if (om.o->mode != RLRA_OMEGA_PHILOX) {
+    const bool fused = om.o->mode == RLRA_OMEGA_PHILOX && sketch_fused();
+    if (om.o->mode == RLRA_OMEGA_PHILOX && !fused) {
+        Om = DMatBuf(ctx, n, l);
+        philox_fill(ctx, Om.m, om.o->seed, draw, 0);
+    } else if (om.o->mode != RLRA_OMEGA_PHILOX) {
         if (!om.o->fill) raise(RLRA_EINVAL, "rlra_omega: callback mode without a fill function");
         h.resize(size_t(n) * l);
         om.o->fill(om.o->user, draw, int(n), l, h.data());
@@ -235,7 +266,7 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
         ev.push_back(e);
         RLRA_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
         const DMat Ar = dA.block(r0, 0, nr, n), Yr = Y.block(r0, 0, nr, l);
-        if (om.o->mode == RLRA_OMEGA_PHILOX) {
+        if (fused) {
             GemmOpts o;
             o.philox_b = true;
             o.seed = om.o->seed;

@@ -36,6 +36,10 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
 // Y = A Omega (op(A) = A or A^T), one Omega draw from om
 enum class Op;
 void sketch(Context& ctx, Op op_a, const DMat& A, int l, OmegaSource& om, const DMat& Y);
+// Y (M x l) = op(A) * Omega, Omega the K x l Philox draw starting at row
+// krow0 of the stream (materialised, or in-GEMM with RLRA_SKETCH_FUSED=1)
+void sketch_philox(Context& ctx, Op op_a, int M, int l, int K, const double* A, int64_t lda, uint64_t seed, int draw,
+                   int64_t krow0, double* Y, int64_t ldy);
 
 // rsvd.hpp:144-156 finish_qb_qr_bt: Q m x l, Bt n x l (overwritten by Qhat)
 void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat& U, double* sigma,
