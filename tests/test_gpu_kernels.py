@@ -191,6 +191,39 @@ def test_small_svd_gram_block_jacobi_vs_oracle(eng, orc, m, n, decay):
     assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
 
 
+@pytest.mark.parametrize("m,n,kind", [(1300, 1000, "graded"), (700, 37, "gauss"), (520, 17, "gauss"),
+                                      (300, 100, "deficient"), (400, 96, "scaled"), (64, 64, "gauss")])
+def test_small_svd_shared_gram_jacobi_vs_oracle(eng, orc, m, n, kind):
+    """The shared-memory-resident Gram block Jacobi (l <= ~1400; blocks of 16
+    columns when the pair fits, else 8): ragged last blocks, zero and repeated
+    columns (completion), columns scaled over 60 decades, graded spectra —
+    the reference's sigma, orthonormal factors, reconstruction."""
+    rs = np.random.default_rng(m * 7 + n)
+    a = rs.standard_normal((m, n))
+    if kind == "graded":
+        q1, _ = np.linalg.qr(rs.standard_normal((m, n)))
+        q2, _ = np.linalg.qr(rs.standard_normal((n, n)))
+        a = (q1 * np.exp(-np.arange(n) / 100.0)) @ q2.T
+    elif kind == "deficient":
+        a[:, 10:20] = 0.0
+        a[:, 30:40] = a[:, 50:60]
+    elif kind == "scaled":
+        a = a * 10.0 ** (-np.arange(n) * 60.0 / n)
+    u, s, v = eng.small_svd(a)
+    uo, so, vo = orc.small_svd(a)
+    r = min(m, n)
+    assert u.shape == (m, r) and v.shape == (n, r)
+    assert np.all(np.diff(s) <= 0)
+    if kind == "deficient":
+        nz = so > 1e-10 * so[0]
+        assert np.max(np.abs(s[nz] - so[nz]) / so[nz]) <= 1e-11
+        assert np.all(s[~nz] <= 1e-12 * so[0])
+    else:
+        assert np.max(np.abs(s - so) / so) <= 1e-10
+    assert rel_fro((u * s) @ v.T, a) <= 1e-12
+    assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
+
+
 def test_small_svd_kats(eng):
     _, s, _ = eng.small_svd(np.diag([2.0, -3.0]))
     assert np.allclose(s, [3.0, 2.0], rtol=1e-15)  # test_jacobi.cpp:95-101
