@@ -438,7 +438,36 @@ struct GramJacArgs {
     int* flags;  // [0..2] rotated-in-sweep, [3] status, [4] sweeps used
     int inner_cap;
     long long* phase_clk;  // optional: CTA 0's clock64 per phase (RLRA_JACOBI_PHASES)
+    unsigned* ver;         // bgram: per column block, rounds completed (zeroed)
 };
+
+// ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
+__device__ __forceinline__ unsigned jb_smem(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void jb_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(jb_smem(dst)),
+        "l"(src), "r"(bytes), "r"(jb_smem(bar))
+        : "memory");
+}
+__device__ __forceinline__ void jb_mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(jb_smem(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void jb_wait_at_least(const unsigned* p, unsigned v) {
+    unsigned cur, ns = 32;
+    for (;;) {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(p) : "memory");
+        if (cur >= v) break;
+        __nanosleep(ns);
+        ns = ns < 128 ? ns * 2 : 128;
+    }
+}
 
 __global__ void __launch_bounds__(256) gram_jacobi_kernel(GramJacArgs a) {
     extern __shared__ double gsm[];
@@ -762,6 +791,14 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
     double* Jb = J + C2 * GP;                       // C2 x JP
     double* Pb = Jb + C2 * JP;                      // 8 warps x NT tiles x 64 partial Grams
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+    const int m2 = (m + 1) & ~1;  // rows per bulk copy (W's ld is even, its pad row zero)
+    __shared__ __align__(8) uint64_t stage_bar;
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(jb_smem(&stage_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    unsigned stage_phase = 0, R = 0;  // R: global round (the version every block reaches)
     volatile int* flags = a.flags;
     const bool clk = a.phase_clk != nullptr && blockIdx.x == 0 && t == 0;
     long long ph[6] = {0, 0, 0, 0, 0, 0}, c0 = clock64();
@@ -789,22 +826,33 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                     bJ = max(b1, b2);
                 }
                 auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
-                // ---- stage the pair's columns (rows >= m zero) ----------------
-                for (int c = warp; c < C2; c += 8) {
-                    const int gc = gcol(c);
-                    double* dst = Ws + size_t(c) * P;
-                    if (gc < n) {
-                        const double* src = a.W + int64_t(gc) * a.ldw;
-                        for (int i = lane; i < m; i += 32) {
-                            const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
-                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src + i));
-                        }
-                        for (int i = m + lane; i < Mp; i += 32) dst[i] = 0.0;
-                    } else {
-                        for (int i = lane; i < Mp; i += 32) dst[i] = 0.0;
+                // ---- stage the pair's columns: wait for the two blocks' last
+                // writers (point-to-point, no grid barrier per round), then one
+                // bulk copy per column; rows >= m2 and padded columns zero ------
+                if (t == 0) {
+                    jb_wait_at_least(a.ver + bI, R);
+                    jb_wait_at_least(a.ver + bJ, R);
+                    // acquire (invalidates this SM's L1 for the later V loads); the
+                    // other CTAs' generic stores, then this CTA's generic smem reads
+                    // of the last visit, ordered before the async-proxy copies
+                    asm volatile("fence.acq_rel.gpu;\nfence.proxy.async.global;\nfence.proxy.async.shared::cta;\n" :::
+                                     "memory");
+                    const int nv = min(C2, max(0, min(BW, n - bI * BW)) + max(0, min(BW, n - bJ * BW)));
+                    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                                     jb_smem(&stage_bar)),
+                                 "r"(unsigned(nv) * unsigned(m2) * 8u)
+                                 : "memory");
+                    for (int c = 0; c < C2; ++c) {
+                        const int gc = gcol(c);
+                        if (gc < n) jb_bulk_load(Ws + size_t(c) * P, a.W + int64_t(gc) * a.ldw, unsigned(m2) * 8u, &stage_bar);
                     }
                 }
-                asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+                for (int c = warp; c < C2; c += 8) {
+                    double* dst = Ws + size_t(c) * P;
+                    for (int i = (gcol(c) < n ? m2 : 0) + lane; i < Mp; i += 32) dst[i] = 0.0;
+                }
+                jb_mbar_wait(&stage_bar, stage_phase);
+                stage_phase ^= 1u;
                 __syncthreads();
                 mark(0);
                 // ---- 1. Gram: warp w sums rows [w*Mp/8, (w+1)*Mp/8) ------------
@@ -911,7 +959,7 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                     }
                 }
                 mark(2);
-                if (!rot) continue;  // uniform across the CTA
+                if (rot) {  // uniform across the CTA
                 if (t == 0) flags[sweep % 3] = 1;
                 for (int e = t; e < C2 * C2; e += 256) Jb[(e / C2) * JP + e % C2] = J[(e / C2) * GP + e % C2];
                 __syncthreads();
@@ -976,12 +1024,20 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                         }
                     }
                 }
+                }
+                // publish: both blocks reached round R + 1
                 __syncthreads();
+                if (t == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ver + bI), "r"(R + 1) : "memory");
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ver + bJ), "r"(R + 1) : "memory");
+                }
                 mark(4);
             }
-            grid_sync(a.bar);
-            mark(5);
+            ++R;
         }
+        grid_sync(a.bar);  // once per sweep: every CTA sees the sweep's rotation flag
+        mark(5);
         const int rotated = flags[sweep % 3];
         ++sweep;
         if (!rotated || n < 2) break;
@@ -1140,7 +1196,13 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     const int m = int(A.rows), n = int(A.cols);
     if (n == 0) return;
     ProfScope prof(ctx, "small_svd", m, n, 0, 0.0);
-    DMatBuf W(ctx, m, n), V(ctx, n, n);
+    // W's leading dimension even and its pad row zero: bgram stages columns
+    // with 16-byte bulk copies
+    const int ldw = (m + 1) & ~1;
+    DMatBuf Wb(ctx, ldw, n), V(ctx, n, n);
+    RLRA_CUDA(cudaMemsetAsync(Wb.m.p, 0, sizeof(double) * size_t(ldw) * n, ctx.stream));
+    DMatBuf& W = Wb;
+    W.m.rows = m;
     copy_mat(ctx, A, W);
     eye_mat(ctx, V);
     Buf flags(ctx, sizeof(int) * 8), sg(ctx, sizeof(double) * n), rank(ctx, sizeof(int) * n),
@@ -1164,7 +1226,9 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         return v == "bgram" ? 1 : v == "block" ? 2 : v == "gram" ? 3 : v == "onesided" ? 4 : 0;
     }();
     constexpr size_t kSmemCap = 220 * 1024;
-    const int bgw = (n > 32 && bgram_smem<16>(m) <= kSmemCap) ? 16 : (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
+    static const int bw_env = std::getenv("RLRA_BGRAM_BW") ? std::atoi(std::getenv("RLRA_BGRAM_BW")) : 0;
+    int bgw = (n > 32 && bgram_smem<16>(m) <= kSmemCap) ? 16 : (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
+    if (bgw && bw_env == 8 && n > 16) bgw = 8;
     if ((forced == 0 || forced == 1) && bgw > 0) {
         GramJacArgs g;
         g.bar = ctx.gbar;
@@ -1177,6 +1241,9 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.nb = ceil_div(n, bgw) + (ceil_div(n, bgw) & 1);
         g.flags = flags.i();
         g.inner_cap = 1;
+        Buf verb(ctx, sizeof(unsigned) * g.nb);
+        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
+        g.ver = static_cast<unsigned*>(verb.p);
         static const bool want_clk = std::getenv("RLRA_JACOBI_PHASES") != nullptr;
         Buf clkb(ctx, want_clk ? sizeof(long long) * 8 : 8);
         g.phase_clk = want_clk ? reinterpret_cast<long long*>(clkb.p) : nullptr;
@@ -1242,6 +1309,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.flags = flags.i();
         g.inner_cap = kGInnerCap;
         g.phase_clk = nullptr;
+        g.ver = nullptr;
         void* args[] = {&g};
         const int grid = std::min(g.nb / 2, gram_cap);
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)gram_jacobi_kernel, dim3(grid), dim3(256), args, kGramJacSmem,
