@@ -438,7 +438,9 @@ struct GramJacArgs {
     int* flags;  // [0..2] rotated-in-sweep, [3] status, [4] sweeps used
     int inner_cap;
     long long* phase_clk;  // optional: CTA 0's clock64 per phase (RLRA_JACOBI_PHASES)
-    unsigned* ver;         // bgram: per column block, rounds completed (zeroed)
+    unsigned* ver;         // bgram: block versions + J hand-off flags (zeroed; see the kernel)
+    double* jbuf;          // bgram with helpers: 2 J slots per pair
+    int helpers;           // bgram: V helper CTAs (grid = nb)
 };
 
 // ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
@@ -777,22 +779,119 @@ __device__ __forceinline__ int bgram_pair(bool intra, int k, int st) {
     return min(c1, c2) | (max(c1, c2) << 8);
 }
 
+// Stage the 2*BW columns (global pitch ld, even; rows2 = rows rounded to 2)
+// of blocks bI, bJ into Xs (pitch P, Mp rows): thread 0 waits until both
+// blocks reached version `need` (their last writers published), then issues
+// one bulk copy per column; rows >= rows2 and padded columns are zeroed.
+template <int BW>
+__device__ __forceinline__ void bgram_stage(double* Xs, int P, int Mp, const double* X, int64_t ld, int rows2,
+                                            int n, int bI, int bJ, const unsigned* ver, unsigned need,
+                                            uint64_t* bar, unsigned& phase) {
+    constexpr int C2 = 2 * BW;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
+    if (t == 0) {
+        jb_wait_at_least(ver + bI, need);
+        jb_wait_at_least(ver + bJ, need);
+        // acquire (this SM's L1 invalidated); the writers' generic stores and
+        // this CTA's generic smem reads of the last visit ordered before the
+        // async-proxy copies
+        asm volatile("fence.acq_rel.gpu;\nfence.proxy.async.global;\nfence.proxy.async.shared::cta;\n" ::: "memory");
+        const int nv = max(0, min(BW, n - bI * BW)) + max(0, min(BW, n - bJ * BW));
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(jb_smem(bar)),
+                     "r"(unsigned(nv) * unsigned(rows2) * 8u)
+                     : "memory");
+        for (int c = 0; c < C2; ++c) {
+            const int gc = gcol(c);
+            if (gc < n) jb_bulk_load(Xs + size_t(c) * P, X + int64_t(gc) * ld, unsigned(rows2) * 8u, bar);
+        }
+    }
+    for (int c = warp; c < C2; c += 8) {
+        double* dst = Xs + size_t(c) * P;
+        for (int i = (gcol(c) < n ? rows2 : 0) + lane; i < Mp; i += 32) dst[i] = 0.0;
+    }
+    jb_mbar_wait(bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+}
+
+// X(rows, cols of the pair) <- Xs * J on DMMA (Xs staged, Jb pitch JP),
+// written straight to global; warps take pairs of 8-row slabs
+template <int BW>
+__device__ __forceinline__ void bgram_apply(const double* Xs, int P, int Mp, const double* Jb, double* X, int64_t ld,
+                                            int rows, int n, int bI, int bJ) {
+    using B = BGram<BW>;
+    constexpr int NB8 = B::NB8, JP = B::JP, KF = B::KF;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
+    double bf[KF][NB8];
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf)
+#pragma unroll
+        for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
+    int ocol[NB8][2];
+#pragma unroll
+    for (int ct = 0; ct < NB8; ++ct)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(ct * 8 + 2 * lc + h);
+    for (int sl0 = 2 * warp; sl0 < Mp / 8; sl0 += 16) {  // Mp / 8 is a multiple of 4
+        double af[2][KF];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int kf = 0; kf < KF; ++kf) af[u][kf] = Xs[(4 * kf + lc) * P + (sl0 + u) * 8 + lr];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+            for (int ct = 0; ct < NB8; ++ct) {
+                double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                if (row < rows) {
+                    if (ocol[ct][0] < n) X[row + int64_t(ocol[ct][0]) * ld] = o0;
+                    if (ocol[ct][1] < n) X[row + int64_t(ocol[ct][1]) * ld] = o1;
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void jb_publish(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// a.helpers == 0: CTA g runs pair slots g, g + grid, ... and applies J to
+// both W and V.  a.helpers == 1 (grid = nb): CTAs [0, nb/2) are the pair
+// owners (W: stage, Gram, steps, publish J, W J) and CTAs [nb/2, nb) their
+// V helpers (prefetch the pair's V columns while the owner works, then V J):
+// V's L2 traffic leaves the owners' critical path and runs on another SM.
+// Versions: ver[b] = rounds of block b's W columns done, ver[nb + b] = of
+// its V columns (helpers; == ver[b] without helpers); jrdy[g] = 2 (R + 1) +
+// rotated, jcon[g] = R + 1 once the helper copied round R's J (the owner
+// reuses J slot R & 1 two rounds later).
 template <int BW>
 __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
     using B = BGram<BW>;
-    constexpr int C2 = B::C2, NB8 = B::NB8, NT = B::NT, GP = B::GP, JP = B::JP, KF = B::KF;
+    constexpr int C2 = B::C2, NB8 = B::NB8, NT = B::NT, GP = B::GP, JP = B::JP;
     static_assert(BW * BW <= 256, "one thread per 2x2 pair block");
     extern __shared__ double bsm[];
-    const int m = a.m, n = a.n, nb = a.nb;
+    const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
     const int Mp = bgram_rows(m), P = bgram_pitch(m);
-    double* Ws = bsm;                               // C2 columns, pitch P
+    double* Ws = bsm;                               // C2 columns, pitch P (helpers: V columns)
     double* G0 = Ws + size_t(C2) * P;               // C2 x GP, two buffers
     double* J = G0 + 2 * C2 * GP;                   // C2 x GP
     double* Jb = J + C2 * GP;                       // C2 x JP
     double* Pb = Jb + C2 * JP;                      // 8 warps x NT tiles x 64 partial Grams
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
-    const int m2 = (m + 1) & ~1;  // rows per bulk copy (W's ld is even, its pad row zero)
+    const bool helpers = a.helpers != 0, helper = helpers && int(blockIdx.x) >= np;
+    const int g0 = helper ? int(blockIdx.x) - np : int(blockIdx.x), gstep = helpers ? np : int(gridDim.x);
+    unsigned* wver = a.ver;
+    unsigned* vver = helpers ? a.ver + nb : a.ver;
+    unsigned* jrdy = a.ver + 2 * nb;
+    unsigned* jcon = jrdy + np;
     __shared__ __align__(8) uint64_t stage_bar;
+    __shared__ int s_rot;
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(jb_smem(&stage_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -818,7 +917,7 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
         if (blockIdx.x == 0 && t == 0) flags[(sweep + 1) % 3] = 0;
         for (int r = 0; r < nb; ++r) {
             const bool intra = r == nb - 1;
-            for (int g = blockIdx.x; g < nb / 2; g += gridDim.x) {
+            for (int g = g0; g < np; g += gstep) {
                 int bI = 2 * g, bJ = 2 * g + 1;
                 if (!intra) {
                     const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
@@ -826,34 +925,40 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                     bJ = max(b1, b2);
                 }
                 auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
-                // ---- stage the pair's columns: wait for the two blocks' last
-                // writers (point-to-point, no grid barrier per round), then one
-                // bulk copy per column; rows >= m2 and padded columns zero ------
-                if (t == 0) {
-                    jb_wait_at_least(a.ver + bI, R);
-                    jb_wait_at_least(a.ver + bJ, R);
-                    // acquire (invalidates this SM's L1 for the later V loads); the
-                    // other CTAs' generic stores, then this CTA's generic smem reads
-                    // of the last visit, ordered before the async-proxy copies
-                    asm volatile("fence.acq_rel.gpu;\nfence.proxy.async.global;\nfence.proxy.async.shared::cta;\n" :::
-                                     "memory");
-                    const int nv = min(C2, max(0, min(BW, n - bI * BW)) + max(0, min(BW, n - bJ * BW)));
-                    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                                     jb_smem(&stage_bar)),
-                                 "r"(unsigned(nv) * unsigned(m2) * 8u)
-                                 : "memory");
-                    for (int c = 0; c < C2; ++c) {
-                        const int gc = gcol(c);
-                        if (gc < n) jb_bulk_load(Ws + size_t(c) * P, a.W + int64_t(gc) * a.ldw, unsigned(m2) * 8u, &stage_bar);
+                if (helper) {
+                    // ---- V helper: prefetch V_p, take the owner's J, V_p J ------
+                    bgram_stage<BW>(Ws, P, bgram_rows(n), a.V, a.ldv, (n + 1) & ~1, n, bI, bJ, vver, R, &stage_bar,
+                                    stage_phase);
+                    if (t == 0) {
+                        unsigned cur, ns = 32;
+                        for (;;) {
+                            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(jrdy + g) : "memory");
+                            if (cur >= 2 * (R + 1)) break;
+                            __nanosleep(ns);
+                            ns = ns < 128 ? ns * 2 : 128;
+                        }
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        s_rot = int(cur & 1u);
                     }
+                    __syncthreads();
+                    const int rot = s_rot;
+                    if (rot) {
+                        const double* js = a.jbuf + (size_t(g) * 2 + (R & 1)) * C2 * C2;
+                        for (int e = t; e < C2 * C2; e += 256) Jb[(e / C2) * JP + e % C2] = __ldcg(js + e);
+                    }
+                    __syncthreads();
+                    if (t == 0) jb_publish(jcon + g, R + 1);
+                    if (rot) bgram_apply<BW>(Ws, P, bgram_rows(n), Jb, a.V, a.ldv, n, n, bI, bJ);
+                    __syncthreads();
+                    if (t == 0) {
+                        __threadfence();
+                        jb_publish(vver + bI, R + 1);
+                        jb_publish(vver + bJ, R + 1);
+                    }
+                    continue;
                 }
-                for (int c = warp; c < C2; c += 8) {
-                    double* dst = Ws + size_t(c) * P;
-                    for (int i = (gcol(c) < n ? m2 : 0) + lane; i < Mp; i += 32) dst[i] = 0.0;
-                }
-                jb_mbar_wait(&stage_bar, stage_phase);
-                stage_phase ^= 1u;
-                __syncthreads();
+                // ---- owner: stage W_p -------------------------------------------
+                bgram_stage<BW>(Ws, P, Mp, a.W, a.ldw, (m + 1) & ~1, n, bI, bJ, wver, R, &stage_bar, stage_phase);
                 mark(0);
                 // ---- 1. Gram: warp w sums rows [w*Mp/8, (w+1)*Mp/8) ------------
                 {
@@ -891,12 +996,12 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                     int bi = 0, rem = u;
                     while (rem >= NB8 - bi) rem -= NB8 - bi++;
                     const int bj = bi + rem;
-                    double s = 0.0;
+                    double sum = 0.0;
 #pragma unroll
-                    for (int ww = 0; ww < 8; ++ww) s += Pb[(ww * NT + u) * 64 + w];
+                    for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * NT + u) * 64 + w];
                     const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
-                    G0[row * GP + col] = s;
-                    G0[col * GP + row] = s;
+                    G0[row * GP + col] = sum;
+                    G0[col * GP + row] = sum;
                 }
                 for (int e = t; e < C2 * C2; e += 256) J[(e / C2) * GP + e % C2] = (e / C2 == e % C2) ? 1.0 : 0.0;
                 __syncthreads();
@@ -959,78 +1064,75 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                     }
                 }
                 mark(2);
-                if (rot) {  // uniform across the CTA
-                if (t == 0) flags[sweep % 3] = 1;
-                for (int e = t; e < C2 * C2; e += 256) Jb[(e / C2) * JP + e % C2] = J[(e / C2) * GP + e % C2];
-                __syncthreads();
-                // ---- 3. W_p <- W_p J (shared -> global) and V_p <- V_p J ------
-                double bf[KF][NB8];
-#pragma unroll
-                for (int kf = 0; kf < KF; ++kf)
-#pragma unroll
-                    for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
-                int ocol[NB8][2];
-#pragma unroll
-                for (int ct = 0; ct < NB8; ++ct)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(ct * 8 + 2 * lc + h);
-                for (int sl0 = 2 * warp; sl0 < Mp / 8; sl0 += 16) {  // Mp / 8 is a multiple of 4
-                    double af[2][KF];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u)
-#pragma unroll
-                        for (int kf = 0; kf < KF; ++kf) af[u][kf] = Ws[(4 * kf + lc) * P + (sl0 + u) * 8 + lr];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int row = (sl0 + u) * 8 + lr;
-#pragma unroll
-                        for (int ct = 0; ct < NB8; ++ct) {
-                            double o0 = 0.0, o1 = 0.0;
-#pragma unroll
-                            for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
-                            if (row < m) {
-                                if (ocol[ct][0] < n) a.W[row + int64_t(ocol[ct][0]) * a.ldw] = o0;
-                                if (ocol[ct][1] < n) a.W[row + int64_t(ocol[ct][1]) * a.ldw] = o1;
-                            }
-                        }
+                if (rot && t == 0) flags[sweep % 3] = 1;
+                if (helpers) {
+                    // hand J to the V helper (slot R & 1, free once round R - 2's J was taken)
+                    double* js = a.jbuf + (size_t(g) * 2 + (R & 1)) * C2 * C2;
+                    if (rot) {
+                        if (t == 0) jb_wait_at_least(jcon + g, R >= 1 ? R - 1 : 0);
+                        __syncthreads();
+                        for (int e = t; e < C2 * C2; e += 256) __stcg(js + e, J[(e / C2) * GP + e % C2]);
+                    }
+                    __syncthreads();
+                    if (t == 0) {
+                        __threadfence();
+                        jb_publish(jrdy + g, 2 * (R + 1) + (rot ? 1u : 0u));
                     }
                 }
-                mark(3);
-                int icol[KF];
-#pragma unroll
-                for (int kf = 0; kf < KF; ++kf) icol[kf] = gcol(4 * kf + lc);
-                constexpr int U = 32 / KF;  // V slabs (8 rows) in flight per warp
-                for (int sl0 = warp * U; sl0 < (n + 7) / 8; sl0 += 8 * U) {
-                    double af[U][KF];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int row = (sl0 + u) * 8 + lr;
+                if (rot) {  // uniform across the CTA
+                    for (int e = t; e < C2 * C2; e += 256) Jb[(e / C2) * JP + e % C2] = J[(e / C2) * GP + e % C2];
+                    __syncthreads();
+                    // ---- 3. W_p <- W_p J (shared -> global); V_p <- V_p J here
+                    // without helpers (V from L2, 8-row slabs in flight) ------------
+                    bgram_apply<BW>(Ws, P, Mp, Jb, a.W, a.ldw, m, n, bI, bJ);
+                    mark(3);
+                    if (!helpers) {
+                        constexpr int KF = B::KF;
+                        double bf[KF][NB8];
 #pragma unroll
                         for (int kf = 0; kf < KF; ++kf)
-                            af[u][kf] = (row < n && icol[kf] < n) ? a.V[row + int64_t(icol[kf]) * a.ldv] : 0.0;
-                    }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int row = (sl0 + u) * 8 + lr;
+                            for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
+                        int icol[KF], ocol[NB8][2];
 #pragma unroll
-                        for (int ct = 0; ct < NB8; ++ct) {
-                            double o0 = 0.0, o1 = 0.0;
+                        for (int kf = 0; kf < KF; ++kf) icol[kf] = gcol(4 * kf + lc);
 #pragma unroll
-                            for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
-                            if (row < n) {
-                                if (ocol[ct][0] < n) a.V[row + int64_t(ocol[ct][0]) * a.ldv] = o0;
-                                if (ocol[ct][1] < n) a.V[row + int64_t(ocol[ct][1]) * a.ldv] = o1;
+                        for (int ct = 0; ct < NB8; ++ct)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(ct * 8 + 2 * lc + h);
+                        constexpr int U = 32 / KF;  // V slabs (8 rows) in flight per warp
+                        for (int sl0 = warp * U; sl0 < (n + 7) / 8; sl0 += 8 * U) {
+                            double af[U][KF];
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+                                for (int kf = 0; kf < KF; ++kf)
+                                    af[u][kf] = (row < n && icol[kf] < n) ? a.V[row + int64_t(icol[kf]) * a.ldv] : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+                                for (int ct = 0; ct < NB8; ++ct) {
+                                    double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                                    for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                                    if (row < n) {
+                                        if (ocol[ct][0] < n) a.V[row + int64_t(ocol[ct][0]) * a.ldv] = o0;
+                                        if (ocol[ct][1] < n) a.V[row + int64_t(ocol[ct][1]) * a.ldv] = o1;
+                                    }
+                                }
                             }
                         }
                     }
                 }
-                }
-                // publish: both blocks reached round R + 1
+                // publish: both blocks' W (and V without helpers) reached round R + 1
                 __syncthreads();
                 if (t == 0) {
                     __threadfence();
-                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ver + bI), "r"(R + 1) : "memory");
-                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ver + bJ), "r"(R + 1) : "memory");
+                    jb_publish(wver + bI, R + 1);
+                    jb_publish(wver + bJ, R + 1);
                 }
                 mark(4);
             }
@@ -1199,10 +1301,13 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     // W's leading dimension even and its pad row zero: bgram stages columns
     // with 16-byte bulk copies
     const int ldw = (m + 1) & ~1;
-    DMatBuf Wb(ctx, ldw, n), V(ctx, n, n);
+    const int ldv = (n + 1) & ~1;
+    DMatBuf Wb(ctx, ldw, n), V(ctx, ldv, n);
     RLRA_CUDA(cudaMemsetAsync(Wb.m.p, 0, sizeof(double) * size_t(ldw) * n, ctx.stream));
+    RLRA_CUDA(cudaMemsetAsync(V.m.p, 0, sizeof(double) * size_t(ldv) * n, ctx.stream));
     DMatBuf& W = Wb;
     W.m.rows = m;
+    V.m.rows = n;
     copy_mat(ctx, A, W);
     eye_mat(ctx, V);
     Buf flags(ctx, sizeof(int) * 8), sg(ctx, sizeof(double) * n), rank(ctx, sizeof(int) * n),
@@ -1226,9 +1331,12 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         return v == "bgram" ? 1 : v == "block" ? 2 : v == "gram" ? 3 : v == "onesided" ? 4 : 0;
     }();
     constexpr size_t kSmemCap = 220 * 1024;
+    // blocks of 8 columns: twice the CTAs of 16-column blocks, and the
+    // per-visit L2 traffic is what bounds a round (l = 510: 12.5 vs 15.0 ms;
+    // 4-column blocks: 15.1 ms).  RLRA_BGRAM_BW=16 selects 16.
     static const int bw_env = std::getenv("RLRA_BGRAM_BW") ? std::atoi(std::getenv("RLRA_BGRAM_BW")) : 0;
-    int bgw = (n > 32 && bgram_smem<16>(m) <= kSmemCap) ? 16 : (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
-    if (bgw && bw_env == 8 && n > 16) bgw = 8;
+    int bgw = (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
+    if (bw_env == 16 && n > 32 && bgram_smem<16>(m) <= kSmemCap) bgw = 16;
     if ((forced == 0 || forced == 1) && bgw > 0) {
         GramJacArgs g;
         g.bar = ctx.gbar;
@@ -1241,9 +1349,14 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.nb = ceil_div(n, bgw) + (ceil_div(n, bgw) & 1);
         g.flags = flags.i();
         g.inner_cap = 1;
-        Buf verb(ctx, sizeof(unsigned) * g.nb);
-        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
+        // V helpers when every pair owner and its helper fit one wave
+        static const bool no_help = std::getenv("RLRA_BGRAM_NOHELP") != nullptr;
+        g.helpers = (!no_help && g.nb <= ctx.num_sms) ? 1 : 0;
+        const size_t nver = size_t(3) * g.nb;
+        Buf verb(ctx, sizeof(unsigned) * nver), jb(ctx, g.helpers ? sizeof(double) * g.nb * (2 * bgw) * (2 * bgw) : 8);
+        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * nver, ctx.stream));
         g.ver = static_cast<unsigned*>(verb.p);
+        g.jbuf = jb.d();
         static const bool want_clk = std::getenv("RLRA_JACOBI_PHASES") != nullptr;
         Buf clkb(ctx, want_clk ? sizeof(long long) * 8 : 8);
         g.phase_clk = want_clk ? reinterpret_cast<long long*>(clkb.p) : nullptr;
@@ -1251,7 +1364,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         const void* kern = bgw == 16 ? (const void*)bgram_jacobi_kernel<16> : (const void*)bgram_jacobi_kernel<8>;
         const size_t smem = bgw == 16 ? bgram_smem<16>(m) : bgram_smem<8>(m);
         RLRA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        const int grid = std::min(g.nb / 2, ctx.num_sms);
+        const int grid = g.helpers ? g.nb : std::min(g.nb / 2, ctx.num_sms);
         RLRA_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), args, smem, ctx.stream));
         if (want_clk) {
             long long h[6];
@@ -1310,6 +1423,8 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.inner_cap = kGInnerCap;
         g.phase_clk = nullptr;
         g.ver = nullptr;
+        g.jbuf = nullptr;
+        g.helpers = 0;
         void* args[] = {&g};
         const int grid = std::min(g.nb / 2, gram_cap);
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)gram_jacobi_kernel, dim3(grid), dim3(256), args, kGramJacSmem,
