@@ -4,6 +4,8 @@
 
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+#include <utility>
 
 #include "cpqr.cuh"
 #include "gemm.cuh"
@@ -17,6 +19,7 @@ namespace rlra_b200 {
 namespace {
 
 constexpr int kCpqrThreads = 256;
+constexpr int kCpqrRegs = 24;  // register-resident rows per lane in cpqr_step_kernel (m - f <= 768)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -242,6 +245,317 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
     }
 }
 
+// ------------------------------------------------ one barrier per pivot ---
+// The same Businger–Golub steps as cpqr_coop_kernel (identical arithmetic,
+// so identical pivots), reorganised so a step needs ONE grid barrier and no
+// single-CTA phase: columns stay where they are (storage s = original column
+// index; the norms travel with them) and every CTA keeps the position <->
+// storage maps in shared memory and applies each swap itself.  Per step every
+// CTA (1) reduces the G slots to the pivot, (2) reads the pivot column (rows
+// f..m) and forms H_f in shared memory — the same reduction order in every
+// CTA, so every CTA holds the same v, beta — and (3) applies H_f to its own
+// trailing storage columns and downdates their norms (core/qr.hpp:190-200).
+// The pivot column's own rows f..m become (alpha, 0, ...) at the start of the
+// next step (nobody reads them before).  W is left in storage order; the host
+// gathers it into position order afterwards.
+__global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
+    extern __shared__ double csm[];
+    const int m = a.m, n = a.n;
+    double* vsh = csm;                                         // m: H_f's vector
+    int* p2s = reinterpret_cast<int*>(csm + m);                // position -> storage
+    int* s2p = p2s + n;                                        // storage -> position
+    __shared__ double sv[32], st[32], shb[32];
+    __shared__ int sp[32];
+    __shared__ int s_piv;
+    const int G = gridDim.x, g = blockIdx.x, t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    double* W = a.W;
+    const int64_t ldw = a.ldw;
+    const int cpb = (n + G - 1) / G;
+    const int j0 = g * cpb, j1 = min(n, j0 + cpb);
+    for (int i = t; i < n; i += blockDim.x) p2s[i] = s2p[i] = i;
+
+    // slots are double-buffered by step parity: step f reads buffer f & 1
+    // (published during step f - 1) while fast CTAs already publish step f's
+    // candidates into the other buffer — with one barrier per step a single
+    // buffer would let a fast CTA overwrite a slot a slow CTA has not read yet
+    int par = 0;
+    auto publish = [&](double bv, int bp, double tr) {
+        if (lane == 0) {
+            sv[warp] = bv;
+            sp[warp] = bp;
+            st[warp] = tr;
+        }
+        __syncthreads();
+        if (t == 0) {
+            double v = -DBL_MAX, tt = 0.0;
+            int p = INT_MAX;
+            for (int w = 0; w < nw; ++w) {
+                if (better(sv[w], sp[w], v, p)) {
+                    v = sv[w];
+                    p = sp[w];
+                }
+                tt += st[w];
+            }
+            a.slot_v[par * G + g] = v;
+            a.slot_p[par * G + g] = p;
+            a.slot_t[par * G + g] = tt;
+        }
+        __syncthreads();
+    };
+
+    {  // squared norms (core/qr.hpp:157-161)
+        double bv = -DBL_MAX, tr = 0.0;
+        int bp = INT_MAX;
+        for (int j = j0 + warp; j < j1; j += nw) {
+            double sum = 0.0;
+            for (int i = lane; i < m; i += 32) {
+                const double x = W[i + int64_t(j) * ldw];
+                sum += x * x;
+            }
+            sum = warp_sum(sum);
+            if (lane == 0) {
+                a.cn[j] = sum;
+                a.rn[j] = sum;
+            }
+            if (better(sum, j, bv, bp)) {
+                bv = sum;
+                bp = j;
+            }
+            tr += sum;
+        }
+        publish(bv, bp, tr);
+    }
+    grid_sync(a.bar);
+
+    int frank = 0;
+    bool reached = false;
+    if (a.tol_mode) {
+        double tt = 0.0;
+        for (int c = 0; c < G; ++c) tt += a.slot_t[c];
+        const double r = sqrt(tt);
+        reached = r <= a.tol;
+        if (g == 0 && t == 0) *a.res = r;
+    }
+    int pend_s = -1, pend_f = 0;  // the pivot column whose rows pend_f.. become (alpha, 0, ...)
+    double pend_alpha = 0.0;
+    auto finish_pending = [&]() {
+        if (pend_s >= 0) {
+            double* col = W + int64_t(pend_s) * ldw;
+            for (int i = pend_f + t; i < m; i += blockDim.x) col[i] = (i == pend_f) ? pend_alpha : 0.0;
+            pend_s = -1;
+        }
+    };
+    while (!reached && frank < a.kmax) {
+        const int f = frank;
+        finish_pending();
+        // 1. pivot (value desc, position asc) over the CTA slots
+        if (warp == 0) {
+            double v = -DBL_MAX;
+            int p = INT_MAX;
+            for (int c = lane; c < G; c += 32)
+                if (better(a.slot_v[par * G + c], a.slot_p[par * G + c], v, p)) {
+                    v = a.slot_v[par * G + c];
+                    p = a.slot_p[par * G + c];
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                if (better(ov, op, v, p)) {
+                    v = ov;
+                    p = op;
+                }
+            }
+            if (lane == 0) s_piv = p;
+        }
+        __syncthreads();
+        const int piv = s_piv;
+        const int sf = p2s[f], spv = p2s[piv];
+        // 2. householder_step on the pivot column (core/qr.hpp:44-66), in every CTA
+        const double* pc = W + int64_t(spv) * ldw;
+        double sum = 0.0;
+        for (int i = f + t; i < m; i += blockDim.x) {
+            const double x = pc[i];
+            vsh[i] = x;
+            sum += x * x;
+        }
+        sum = warp_sum(sum);
+        if (lane == 0) shb[warp] = sum;
+        __syncthreads();
+        double norm2 = 0.0;
+        for (int w = 0; w < nw; ++w) norm2 += shb[w];
+        const double x1 = vsh[f];
+        const double norm = sqrt(norm2);
+        const bool zero = norm < 1e-300;
+        const double alpha = x1 >= 0.0 ? -norm : norm;
+        const double beta = zero ? 0.0 : 2.0 / (2.0 * (norm2 - alpha * x1));
+        __syncthreads();
+        if (zero) {
+            for (int i = f + t; i < m; i += blockDim.x) vsh[i] = 0.0;
+        } else if (t == 0) {
+            vsh[f] = x1 - alpha;
+        }
+        // the swap (core/qr.hpp:182-187), on the maps
+        if (t == 0 && piv != f) {
+            p2s[f] = spv;
+            p2s[piv] = sf;
+            s2p[spv] = f;
+            s2p[sf] = piv;
+        }
+        __syncthreads();
+        if (g == 0) {
+            for (int i = t; i < m; i += blockDim.x) a.Vst[i + int64_t(f) * m] = i < f ? 0.0 : vsh[i];
+            if (t == 0) {
+                a.beta[f] = beta;
+                if (zero) a.out[2] = 1;
+            }
+        }
+        par ^= 1;  // this step's candidates go to the other buffer
+        // 3. apply H_f to own trailing columns, downdate (core/qr.hpp:190-200).
+        // Columns up to 32 * kCpqrRegs rows below f are held in registers, two
+        // per warp at a time, so the L2 round trips overlap (the same
+        // arithmetic in the same order as the loop form below).
+        double bv = -DBL_MAX, tr = 0.0;
+        int bp = INT_MAX;
+        auto downdate = [&](int j, int pos, double d, double s2, bool have_s2) {
+            double c = a.cn[j] - d * d;
+            const double ref = a.rn[j];
+            double rr = ref;
+            if (c < 1e-6 * ref || a.tol_mode) {
+                if (c < 1e-6 * ref) {
+                    c = s2;
+                    rr = s2;
+                }
+                tr += s2;
+            }
+            (void)have_s2;
+            if (lane == 0) {
+                a.cn[j] = c;
+                a.rn[j] = rr;
+            }
+            if (better(c, pos, bv, bp)) {
+                bv = c;
+                bp = pos;
+            }
+        };
+        if (m - f <= 32 * kCpqrRegs) {
+            for (int j = j0 + warp; j < j1; j += 2 * nw) {
+                const int jj[2] = {j, j + nw};
+                bool on[2];
+                double x[2][kCpqrRegs];
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    on[b] = jj[b] < j1 && s2p[jj[b]] > f;
+                    const double* wj = W + int64_t(on[b] ? jj[b] : 0) * ldw;
+#pragma unroll
+                    for (int u = 0; u < kCpqrRegs; ++u) {
+                        const int i = f + lane + 32 * u;
+                        x[b][u] = (on[b] && i < m) ? wj[i] : 0.0;
+                    }
+                }
+                if (beta != 0.0) {
+                    double sd[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int u = 0; u < kCpqrRegs; ++u) {
+                        const int i = f + lane + 32 * u;
+                        const double vi = i < m ? vsh[i] : 0.0;
+#pragma unroll
+                        for (int b = 0; b < 2; ++b) sd[b] += vi * x[b][u];
+                    }
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) {
+                        const double fct = beta * warp_sum(sd[b]);
+#pragma unroll
+                        for (int u = 0; u < kCpqrRegs; ++u) {
+                            const int i = f + lane + 32 * u;
+                            if (i < m) x[b][u] -= fct * vsh[i];
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) {
+                        if (!on[b]) continue;
+                        double* wj = W + int64_t(jj[b]) * ldw;
+#pragma unroll
+                        for (int u = 0; u < kCpqrRegs; ++u) {
+                            const int i = f + lane + 32 * u;
+                            if (i < m) wj[i] = x[b][u];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const double d = __shfl_sync(0xffffffffu, x[b][0], 0);  // row f
+                    double s2 = 0.0;
+                    const double c0 = a.cn[on[b] ? jj[b] : 0] - d * d, r0 = a.rn[on[b] ? jj[b] : 0];
+                    if (c0 < 1e-6 * r0 || a.tol_mode) {  // uniform across the warp
+#pragma unroll
+                        for (int u = 0; u < kCpqrRegs; ++u) {
+                            const int i = f + lane + 32 * u;
+                            if (i > f && i < m) s2 += x[b][u] * x[b][u];
+                        }
+                        s2 = warp_sum(s2);
+                    }
+                    if (on[b]) downdate(jj[b], s2p[jj[b]], d, s2, true);
+                }
+            }
+        } else {
+            for (int j = j0 + warp; j < j1; j += nw) {
+                const int pos = s2p[j];
+                if (pos <= f) continue;
+                double* wj = W + int64_t(j) * ldw;
+                if (beta != 0.0) {
+                    double sdot = 0.0;
+                    for (int i = f + lane; i < m; i += 32) sdot += vsh[i] * wj[i];
+                    const double fct = beta * warp_sum(sdot);
+                    for (int i = f + lane; i < m; i += 32) wj[i] -= fct * vsh[i];
+                    __syncwarp();
+                }
+                const double d = wj[f];
+                double s2 = 0.0;
+                if (a.cn[j] - d * d < 1e-6 * a.rn[j] || a.tol_mode) {
+                    for (int i = f + 1 + lane; i < m; i += 32) s2 += wj[i] * wj[i];
+                    s2 = warp_sum(s2);
+                }
+                downdate(j, pos, d, s2, true);
+            }
+        }
+        publish(bv, bp, tr);
+        if (spv >= j0 && spv < j1) {
+            pend_s = spv;
+            pend_f = f;
+            pend_alpha = zero ? 0.0 : alpha;
+        }
+        ++frank;
+        grid_sync(a.bar);
+        if (a.tol_mode && frank < a.rmax) {
+            double tt = 0.0;
+            for (int c = 0; c < G; ++c) tt += a.slot_t[par * G + c];
+            const double r = sqrt(tt);
+            if (g == 0 && t == 0) *a.res = r;
+            if (r <= a.tol) reached = true;
+        }
+    }
+    finish_pending();
+    if (g == 0) {
+        for (int i = t; i < n; i += blockDim.x) a.perm[i] = p2s[i];
+        if (t == 0) {
+            a.out[0] = frank;
+            a.out[1] = reached ? 1 : 0;
+        }
+    }
+}
+
+// Wp(:, p) = W(:, perm[p]): storage order -> position order
+__global__ void gather_cols_kernel(const double* W, int64_t ldw, int m, int n, const int* perm, double* Wp,
+                                   int64_t ldp) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(m) * n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int j = int(e / m), i = int(e % m);
+        Wp[i + int64_t(j) * ldp] = W[i + int64_t(perm[j]) * ldw];
+    }
+}
+
 // S1 = W(0:f, :) with diag sign fix; Q1 columns flipped alongside.
 __global__ void cpqr_finish_kernel(const double* W, int64_t ldw, int f, int n, double* S1,
                                    int64_t lds) {
@@ -343,11 +657,19 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     Buf Vst(ctx, sizeof(double) * size_t(m) * std::max(kmax, 1)), beta(ctx, sizeof(double) * (kmax + 1)),
         cn(ctx, sizeof(double) * n), rn(ctx, sizeof(double) * n), out(ctx, sizeof(int) * 4),
         res(ctx, sizeof(double));
+    // one-barrier-per-step kernel when its shared maps fit (m + n <= 27k);
+    // RLRA_CPQR_TWO_BARRIER=1 forces the two-barrier kernel
+    static const bool two_bar = std::getenv("RLRA_CPQR_TWO_BARRIER") != nullptr;
+    const size_t step_smem = sizeof(double) * size_t(m) + 2 * sizeof(int) * size_t(n);
+    const bool one_bar = !two_bar && step_smem <= 220 * 1024;
+    if (one_bar)
+        RLRA_CUDA(cudaFuncSetAttribute(cpqr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(step_smem)));
     int per_sm = 0;
-    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCpqrThreads, 0));
+    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, one_bar ? cpqr_step_kernel : cpqr_coop_kernel,
+                                                            kCpqrThreads, one_bar ? step_smem : 0));
     int G = std::max(1, std::min(ctx.num_sms * std::max(1, per_sm), ceil_div(n, 4 * (kCpqrThreads / 32))));
     G = std::min(G, ctx.num_sms);
-    Buf sv(ctx, sizeof(double) * G), sp(ctx, sizeof(int) * G), stt(ctx, sizeof(double) * G);
+    Buf sv(ctx, sizeof(double) * 2 * G), sp(ctx, sizeof(int) * 2 * G), stt(ctx, sizeof(double) * 2 * G);
     RLRA_CUDA(cudaMemsetAsync(out.p, 0, sizeof(int) * 4, ctx.stream));
     RLRA_CUDA(cudaMemsetAsync(res.p, 0, sizeof(double), ctx.stream));
     CpqrArgs a;
@@ -371,9 +693,22 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     a.res = res.d();
     a.bar = ctx.gbar;
     void* args[] = {&a};
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_coop_kernel, dim3(G), dim3(kCpqrThreads), args,
-                                          0, ctx.stream));
+    if (one_bar) {
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_step_kernel, dim3(G), dim3(kCpqrThreads), args,
+                                              step_smem, ctx.stream));
+    } else {
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_coop_kernel, dim3(G), dim3(kCpqrThreads), args,
+                                              0, ctx.stream));
+    }
     ++ctx.launches;
+    if (one_bar) {  // storage order -> position order
+        DMatBuf Wp(ctx, m, n);
+        const int blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, int64_t(ctx.num_sms) * 8));
+        gather_cols_kernel<<<blocks, 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, perm, Wp.m.p, Wp.m.ld);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        std::swap(W, Wp);
+    }
     int h_out[4];
     double h_res = 0.0;
     RLRA_CUDA(cudaMemcpyAsync(h_out, out.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx.stream));
