@@ -4,6 +4,7 @@
 
 #include <cfloat>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -19,6 +20,7 @@ namespace rlra_b200 {
 namespace {
 
 constexpr int kCpqrThreads = 256;
+constexpr int kCpqrStepThreads = 384;  // 12 warps: more L2 round trips in flight per SM
 constexpr int kCpqrRegs = 24;  // register-resident rows per lane in cpqr_step_kernel (m - f <= 768)
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -51,6 +53,7 @@ struct CpqrArgs {
     double* slot_t;
     int* out;  // [0] frank, [1] reached, [2] degenerate
     double* res;
+    long long* phase_clk;  // optional: CTA 0's clock64 per step phase (RLRA_CPQR_PHASES)
 };
 
 __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
@@ -258,22 +261,33 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
 // The pivot column's own rows f..m become (alpha, 0, ...) at the start of the
 // next step (nobody reads them before).  W is left in storage order; the host
 // gathers it into position order afterwards.
-__global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
+__global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a) {
     extern __shared__ double csm[];
     const int m = a.m, n = a.n;
-    double* vsh = csm;                                         // m: H_f's vector
-    int* p2s = reinterpret_cast<int*>(csm + m);                // position -> storage
-    int* s2p = p2s + n;                                        // storage -> position
-    __shared__ double sv[32], st[32], shb[32];
-    __shared__ int sp[32];
-    __shared__ int s_piv;
     const int G = gridDim.x, g = blockIdx.x, t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
     double* W = a.W;
     const int64_t ldw = a.ldw;
     const int cpb = (n + G - 1) / G;
     const int j0 = g * cpb, j1 = min(n, j0 + cpb);
+    double* vsh = csm;                                         // m: H_f's vector
+    double* cnS = csm + m;                                     // own columns' norms (owner-only state)
+    double* rnS = cnS + cpb;
+    int* p2s = reinterpret_cast<int*>(rnS + cpb);              // position -> storage
+    int* s2p = p2s + n;                                        // storage -> position
+    __shared__ double sv[32], st[32], shb[32];
+    __shared__ int sp[32];
+    __shared__ int s_piv;
     for (int i = t; i < n; i += blockDim.x) p2s[i] = s2p[i] = i;
+    const bool clk = a.phase_clk != nullptr && g == 0 && t == 0;
+    long long ph[5] = {0, 0, 0, 0, 0}, c0 = clock64();
+    auto mark = [&](int i) {
+        if (clk) {
+            const long long c1 = clock64();
+            ph[i] += c1 - c0;
+            c0 = c1;
+        }
+    };
 
     // slots are double-buffered by step parity: step f reads buffer f & 1
     // (published during step f - 1) while fast CTAs already publish step f's
@@ -315,8 +329,8 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
             }
             sum = warp_sum(sum);
             if (lane == 0) {
-                a.cn[j] = sum;
-                a.rn[j] = sum;
+                cnS[j - j0] = sum;
+                rnS[j - j0] = sum;
             }
             if (better(sum, j, bv, bp)) {
                 bv = sum;
@@ -372,6 +386,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
         __syncthreads();
         const int piv = s_piv;
         const int sf = p2s[f], spv = p2s[piv];
+        mark(0);
         // 2. householder_step on the pivot column (core/qr.hpp:44-66), in every CTA
         const double* pc = W + int64_t(spv) * ldw;
         double sum = 0.0;
@@ -411,6 +426,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
                 if (zero) a.out[2] = 1;
             }
         }
+        mark(1);
         par ^= 1;  // this step's candidates go to the other buffer
         // 3. apply H_f to own trailing columns, downdate (core/qr.hpp:190-200).
         // Columns up to 32 * kCpqrRegs rows below f are held in registers, two
@@ -419,8 +435,8 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
         double bv = -DBL_MAX, tr = 0.0;
         int bp = INT_MAX;
         auto downdate = [&](int j, int pos, double d, double s2, bool have_s2) {
-            double c = a.cn[j] - d * d;
-            const double ref = a.rn[j];
+            double c = cnS[j - j0] - d * d;
+            const double ref = rnS[j - j0];
             double rr = ref;
             if (c < 1e-6 * ref || a.tol_mode) {
                 if (c < 1e-6 * ref) {
@@ -430,10 +446,12 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
                 tr += s2;
             }
             (void)have_s2;
+            __syncwarp();
             if (lane == 0) {
-                a.cn[j] = c;
-                a.rn[j] = rr;
+                cnS[j - j0] = c;
+                rnS[j - j0] = rr;
             }
+            __syncwarp();
             if (better(c, pos, bv, bp)) {
                 bv = c;
                 bp = pos;
@@ -487,7 +505,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
                 for (int b = 0; b < 2; ++b) {
                     const double d = __shfl_sync(0xffffffffu, x[b][0], 0);  // row f
                     double s2 = 0.0;
-                    const double c0 = a.cn[on[b] ? jj[b] : 0] - d * d, r0 = a.rn[on[b] ? jj[b] : 0];
+                    const double c0 = cnS[on[b] ? jj[b] - j0 : 0] - d * d, r0 = rnS[on[b] ? jj[b] - j0 : 0];
                     if (c0 < 1e-6 * r0 || a.tol_mode) {  // uniform across the warp
 #pragma unroll
                         for (int u = 0; u < kCpqrRegs; ++u) {
@@ -513,14 +531,16 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
                 }
                 const double d = wj[f];
                 double s2 = 0.0;
-                if (a.cn[j] - d * d < 1e-6 * a.rn[j] || a.tol_mode) {
+                if (cnS[j - j0] - d * d < 1e-6 * rnS[j - j0] || a.tol_mode) {
                     for (int i = f + 1 + lane; i < m; i += 32) s2 += wj[i] * wj[i];
                     s2 = warp_sum(s2);
                 }
                 downdate(j, pos, d, s2, true);
             }
         }
+        mark(2);
         publish(bv, bp, tr);
+        mark(3);
         if (spv >= j0 && spv < j1) {
             pend_s = spv;
             pend_f = f;
@@ -528,6 +548,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
         }
         ++frank;
         grid_sync(a.bar);
+        mark(4);
         if (a.tol_mode && frank < a.rmax) {
             double tt = 0.0;
             for (int c = 0; c < G; ++c) tt += a.slot_t[par * G + c];
@@ -537,6 +558,8 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_step_kernel(CpqrArgs a) {
         }
     }
     finish_pending();
+    if (clk)
+        for (int i = 0; i < 5; ++i) a.phase_clk[i] = ph[i];
     if (g == 0) {
         for (int i = t; i < n; i += blockDim.x) a.perm[i] = p2s[i];
         if (t == 0) {
@@ -660,13 +683,17 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     // one-barrier-per-step kernel when its shared maps fit (m + n <= 27k);
     // RLRA_CPQR_TWO_BARRIER=1 forces the two-barrier kernel
     static const bool two_bar = std::getenv("RLRA_CPQR_TWO_BARRIER") != nullptr;
-    const size_t step_smem = sizeof(double) * size_t(m) + 2 * sizeof(int) * size_t(n);
-    const bool one_bar = !two_bar && step_smem <= 220 * 1024;
-    if (one_bar)
-        RLRA_CUDA(cudaFuncSetAttribute(cpqr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(step_smem)));
+    const int cpb_max = ceil_div(n, std::max(1, std::min(ctx.num_sms, ceil_div(n, 4 * (kCpqrThreads / 32)))));
+    const size_t step_smem = sizeof(double) * (size_t(m) + 2 * size_t(cpb_max)) + 2 * sizeof(int) * size_t(n);
+    bool one_bar = !two_bar && step_smem <= 220 * 1024;
     int per_sm = 0;
-    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, one_bar ? cpqr_step_kernel : cpqr_coop_kernel,
-                                                            kCpqrThreads, one_bar ? step_smem : 0));
+    if (one_bar) {
+        RLRA_CUDA(cudaFuncSetAttribute(cpqr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(step_smem)));
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_step_kernel, kCpqrStepThreads, step_smem));
+        one_bar = per_sm >= 1;
+    }
+    if (!one_bar)
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCpqrThreads, 0));
     int G = std::max(1, std::min(ctx.num_sms * std::max(1, per_sm), ceil_div(n, 4 * (kCpqrThreads / 32))));
     G = std::min(G, ctx.num_sms);
     Buf sv(ctx, sizeof(double) * 2 * G), sp(ctx, sizeof(int) * 2 * G), stt(ctx, sizeof(double) * 2 * G);
@@ -692,15 +719,25 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     a.out = out.i();
     a.res = res.d();
     a.bar = ctx.gbar;
+    static const bool want_clk = std::getenv("RLRA_CPQR_PHASES") != nullptr;
+    Buf clkb(ctx, sizeof(long long) * 8);
+    a.phase_clk = (want_clk && one_bar) ? reinterpret_cast<long long*>(clkb.p) : nullptr;
     void* args[] = {&a};
     if (one_bar) {
-        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_step_kernel, dim3(G), dim3(kCpqrThreads), args,
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_step_kernel, dim3(G), dim3(kCpqrStepThreads), args,
                                               step_smem, ctx.stream));
     } else {
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_coop_kernel, dim3(G), dim3(kCpqrThreads), args,
                                               0, ctx.stream));
     }
     ++ctx.launches;
+    if (a.phase_clk) {
+        long long h[5];
+        RLRA_CUDA(cudaMemcpyAsync(h, clkb.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        std::fprintf(stderr, "cpqr_step m=%d n=%d G=%d clocks: pivot %lld householder %lld apply %lld publish %lld sync %lld\n",
+                     m, n, G, h[0], h[1], h[2], h[3], h[4]);
+    }
     if (one_bar) {  // storage order -> position order
         DMatBuf Wp(ctx, m, n);
         const int blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, int64_t(ctx.num_sms) * 8));
