@@ -1149,6 +1149,252 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
         for (int i = 0; i < 6; ++i) a.phase_clk[i] = ph[i];
 }
 
+// ----------------------- streaming Gram block Jacobi, 48-column pairs -------
+// For l x l inputs too tall for shared memory (the C2 R-hat, 6100 x 6100):
+// blocks of 24 columns so the nb/2 = 128 pair CTAs cover most SMs (blocks of
+// 32 leave 52 idle), the cross/intra cyclic schedule of bgram_jacobi_kernel
+// (every column pair once per sweep), point-to-point block versions instead
+// of a grid barrier per round.  Per visit:
+//   1. G = W_p^T W_p streamed in 64-row chunks (register prefetch -> shared),
+//      each warp a k-slice of every chunk for all 21 upper 8x8 tiles, the 8
+//      partial Grams summed in a fixed order;
+//   2. the visit's steps on G: the 24 pair rotations (reference formula and
+//      skip rule, branch-free fast form) then every thread updates its 2x2
+//      pair blocks of G (double-buffered) and J — two barriers per step;
+//   3. W_p J and V_p J streamed in 64-row chunks, 16 x 24 DMMA warp tiles.
+constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 64;
+constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16)
+constexpr int kSGP = kSC2 + 1;   // G / J pitch
+constexpr int kSJP = kSC2 + 4;   // J pitch for B fragments (== 4 mod 16)
+constexpr size_t kSGramSmem =
+    sizeof(double) * (size_t(kSC2) * kSCP + size_t(8) * kSNT * 64 + 3 * kSC2 * kSGP + kSC2 * kSJP + 2 * kSGB);
+
+__global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
+    extern __shared__ double ssm[];
+    double* Cb = ssm;                          // chunk: 48 columns x 64 rows, pitch kSCP
+    double* Pb = Cb + kSC2 * kSCP;             // 8 warps x 21 tiles x 64 partial Grams
+    double* G0 = Pb + 8 * kSNT * 64;           // two 48 x 49 buffers
+    double* J = G0 + 2 * kSC2 * kSGP;          // 48 x 49
+    double* Jb = J + kSC2 * kSGP;              // 48 x 52
+    double* rc = Jb + kSC2 * kSJP;             // per pair: c, s
+    double* rs = rc + kSGB;
+    __shared__ int rpq[kSGB];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+    const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
+    volatile int* flags = a.flags;
+    unsigned R = 0;
+    int sweep = 0;
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            if (blockIdx.x == 0 && t == 0) flags[3] = RLRA_ECONV;
+            break;
+        }
+        if (blockIdx.x == 0 && t == 0) flags[(sweep + 1) % 3] = 0;
+        for (int r = 0; r < nb; ++r) {
+            const bool intra = r == nb - 1;
+            for (int g = blockIdx.x; g < np; g += gridDim.x) {
+                int bI = 2 * g, bJ = 2 * g + 1;
+                if (!intra) {
+                    const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
+                    bI = min(b1, b2);
+                    bJ = max(b1, b2);
+                }
+                auto gcol = [&](int c) { return c < kSGB ? bI * kSGB + c : bJ * kSGB + (c - kSGB); };
+                if (t == 0) {
+                    jb_wait_at_least(a.ver + bI, R);
+                    jb_wait_at_least(a.ver + bJ, R);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                __syncthreads();
+                // each thread's 12 chunk elements: column e / 64, row e % 64
+                int ccol[12];
+#pragma unroll
+                for (int it = 0; it < 12; ++it) ccol[it] = gcol((t + 256 * it) >> 6);
+                double pre[12];
+                auto load_chunk = [&](const double* X, int64_t ld, int rows, int k0) {
+#pragma unroll
+                    for (int it = 0; it < 12; ++it) {
+                        const int e = t + 256 * it, row = k0 + (e & 63);
+                        pre[it] = (ccol[it] < n && row < rows) ? __ldcg(X + row + int64_t(ccol[it]) * ld) : 0.0;
+                    }
+                };
+                auto store_chunk = [&]() {
+#pragma unroll
+                    for (int it = 0; it < 12; ++it) {
+                        const int e = t + 256 * it;
+                        Cb[(e >> 6) * kSCP + (e & 63)] = pre[it];
+                    }
+                };
+                // ---- 1. Gram -------------------------------------------------
+                {
+                    double acc[kSNT][2];
+#pragma unroll
+                    for (int u = 0; u < kSNT; ++u) acc[u][0] = acc[u][1] = 0.0;
+                    load_chunk(a.W, a.ldw, m, 0);
+                    for (int k0 = 0; k0 < m; k0 += kSCR) {
+                        __syncthreads();
+                        store_chunk();
+                        __syncthreads();
+                        if (k0 + kSCR < m) load_chunk(a.W, a.ldw, m, k0 + kSCR);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int kk = (warp + 8 * h) * 4;
+                            double f[kSNB8];
+#pragma unroll
+                            for (int bb = 0; bb < kSNB8; ++bb) f[bb] = Cb[(bb * 8 + lr) * kSCP + kk + lc];
+                            int u = 0;
+#pragma unroll
+                            for (int bi = 0; bi < kSNB8; ++bi)
+#pragma unroll
+                                for (int bj = bi; bj < kSNB8; ++bj, ++u) jac_dmma(acc[u][0], acc[u][1], f[bi], f[bj]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSNT; ++u) {
+                        Pb[(warp * kSNT + u) * 64 + lr * 8 + 2 * lc] = acc[u][0];
+                        Pb[(warp * kSNT + u) * 64 + lr * 8 + 2 * lc + 1] = acc[u][1];
+                    }
+                }
+                __syncthreads();
+                for (int e = t; e < kSNT * 64; e += 256) {
+                    const int u = e >> 6, w = e & 63;
+                    int bi = 0, rem = u;
+                    while (rem >= kSNB8 - bi) rem -= kSNB8 - bi++;
+                    const int bj = bi + rem;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * kSNT + u) * 64 + w];
+                    const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
+                    G0[row * kSGP + col] = sum;
+                    G0[col * kSGP + row] = sum;
+                }
+                for (int e = t; e < kSC2 * kSC2; e += 256) J[(e / kSC2) * kSGP + e % kSC2] = (e / kSC2 == e % kSC2) ? 1.0 : 0.0;
+                __syncthreads();
+                // ---- 2. the visit's steps ------------------------------------
+                int rot = 0;
+                const int nsteps = intra ? kSGB - 1 : kSGB;
+                for (int st = 0; st < nsteps; ++st) {
+                    const double* Gc = G0 + (st & 1) * kSC2 * kSGP;
+                    double* Gn = G0 + ((st & 1) ^ 1) * kSC2 * kSGP;
+                    int act = 0;
+                    if (t < kSGB) {
+                        const int pq = bgram_pair<kSGB>(intra, t, st);
+                        const int p = pq & 255, q = pq >> 8;
+                        const double pp = Gc[p * kSGP + p], qq = Gc[q * kSGP + q], pqv = Gc[p * kSGP + q];
+                        double c, sn;
+                        if (!jac_rotation_fast(pp, qq, pqv, c, sn, act)) act = jac_rotation_ref(pp, qq, pqv, c, sn);
+                        rc[t] = c;
+                        rs[t] = sn;
+                        rpq[t] = pq | (act << 16);
+                    }
+                    rot |= __syncthreads_or(act);
+                    for (int b = t; b < kSGB * kSGB; b += 256) {
+                        const int k = b / kSGB, l = b % kSGB;
+                        const int pqk = rpq[k], pql = rpq[l];
+                        const int pk = pqk & 255, qk = (pqk >> 8) & 255, pl = pql & 255, ql = (pql >> 8) & 255;
+                        const bool ak = (pqk >> 16) != 0, al = (pql >> 16) != 0;
+                        const double ck = rc[k], sk = rs[k], cl = rc[l], sl = rs[l];
+                        if (al) {
+                            const double j0 = J[pk * kSGP + pl], j1 = J[pk * kSGP + ql];
+                            const double j2 = J[qk * kSGP + pl], j3 = J[qk * kSGP + ql];
+                            J[pk * kSGP + pl] = cl * j0 - sl * j1;
+                            J[pk * kSGP + ql] = sl * j0 + cl * j1;
+                            J[qk * kSGP + pl] = cl * j2 - sl * j3;
+                            J[qk * kSGP + ql] = sl * j2 + cl * j3;
+                        }
+                        if (k <= l) {
+                            double b00 = Gc[pk * kSGP + pl], b01 = Gc[pk * kSGP + ql];
+                            double b10 = Gc[qk * kSGP + pl], b11 = Gc[qk * kSGP + ql];
+                            if (al) {
+                                const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
+                                const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
+                                b00 = x0, b01 = x1, b10 = x2, b11 = x3;
+                            }
+                            if (ak) {
+                                const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
+                                const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
+                                b00 = y0, b01 = y1, b10 = y2, b11 = y3;
+                            }
+                            Gn[pk * kSGP + pl] = b00;
+                            Gn[pk * kSGP + ql] = b01;
+                            Gn[qk * kSGP + pl] = b10;
+                            Gn[qk * kSGP + ql] = b11;
+                            Gn[pl * kSGP + pk] = b00;
+                            Gn[ql * kSGP + pk] = b01;
+                            Gn[pl * kSGP + qk] = b10;
+                            Gn[ql * kSGP + qk] = b11;
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (rot) {
+                    if (t == 0) flags[sweep % 3] = 1;
+                    for (int e = t; e < kSC2 * kSC2; e += 256) Jb[(e / kSC2) * kSJP + e % kSC2] = J[(e / kSC2) * kSGP + e % kSC2];
+                    // ---- 3. W_p J, V_p J: warp (wr, wc) owns rows wr*16..+16, cols wc*24..+24 of a chunk
+                    const int wr = warp & 3, wc = warp >> 2;
+                    int ocol[3][2];
+#pragma unroll
+                    for (int ct = 0; ct < 3; ++ct)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(wc * 24 + ct * 8 + 2 * lc + h);
+                    for (int mat = 0; mat < 2; ++mat) {
+                        double* X = mat == 0 ? a.W : a.V;
+                        const int64_t ld = mat == 0 ? a.ldw : a.ldv;
+                        const int rows = mat == 0 ? m : n;
+                        load_chunk(X, ld, rows, 0);
+                        for (int k0 = 0; k0 < rows; k0 += kSCR) {
+                            __syncthreads();
+                            store_chunk();
+                            __syncthreads();
+                            // the next chunk's rows are disjoint from this chunk's outputs
+                            if (k0 + kSCR < rows) load_chunk(X, ld, rows, k0 + kSCR);
+                            double o[2][3][2];
+#pragma unroll
+                            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                                for (int ct = 0; ct < 3; ++ct) o[f][ct][0] = o[f][ct][1] = 0.0;
+#pragma unroll
+                            for (int kf = 0; kf < kSC2 / 4; ++kf) {
+                                double af[2], bf[3];
+#pragma unroll
+                                for (int f = 0; f < 2; ++f) af[f] = Cb[(4 * kf + lc) * kSCP + wr * 16 + f * 8 + lr];
+#pragma unroll
+                                for (int ct = 0; ct < 3; ++ct) bf[ct] = Jb[(4 * kf + lc) * kSJP + wc * 24 + ct * 8 + lr];
+#pragma unroll
+                                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                                    for (int ct = 0; ct < 3; ++ct) jac_dmma(o[f][ct][0], o[f][ct][1], af[f], bf[ct]);
+                            }
+#pragma unroll
+                            for (int f = 0; f < 2; ++f) {
+                                const int row = k0 + wr * 16 + f * 8 + lr;
+                                if (row >= rows) continue;
+#pragma unroll
+                                for (int ct = 0; ct < 3; ++ct)
+#pragma unroll
+                                    for (int h = 0; h < 2; ++h)
+                                        if (ocol[ct][h] < n) X[row + int64_t(ocol[ct][h]) * ld] = o[f][ct][h];
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                if (t == 0) {
+                    __threadfence();
+                    jb_publish(a.ver + bI, R + 1);
+                    jb_publish(a.ver + bJ, R + 1);
+                }
+            }
+            ++R;
+        }
+        grid_sync(a.bar);
+        const int rotated = flags[sweep % 3];
+        ++sweep;
+        if (!rotated || n < 2) break;
+    }
+    if (blockIdx.x == 0 && t == 0) flags[4] = sweep;
+}
+
 int coop_grid(Context& ctx, const void* kern, int want_blocks) {
     int per_sm = 0;
     RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kJacThreads, 0));
@@ -1323,12 +1569,12 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     a.flags = flags.i();
     // kernel choice: the shared-memory-resident Gram block Jacobi when a
     // block pair fits (l up to ~1400), else the streaming Gram variant;
-    // RLRA_SVD_KERNEL=bgram|block|gram|onesided forces one (A/B timing)
+    // RLRA_SVD_KERNEL=bgram|block|sgram|gram|onesided forces one (A/B timing)
     static const int forced = [] {
         const char* e = std::getenv("RLRA_SVD_KERNEL");
         if (!e) return 0;
         const std::string v(e);
-        return v == "bgram" ? 1 : v == "block" ? 2 : v == "gram" ? 3 : v == "onesided" ? 4 : 0;
+        return v == "bgram" ? 1 : v == "block" ? 2 : v == "sgram" ? 3 : v == "onesided" ? 4 : v == "gram" ? 5 : 0;
     }();
     constexpr size_t kSmemCap = 220 * 1024;
     // blocks of 8 columns: twice the CTAs of 16-column blocks, and the
@@ -1386,7 +1632,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_jacobi_kernel<BW>, BW * 32,
                                                                 bj_smem));
     }
-    if (forced != 3 && forced != 4 && per_sm > 0 && nblk / 2 <= per_sm * ctx.num_sms) {
+    if (forced != 3 && forced != 4 && forced != 5 && per_sm > 0 && nblk / 2 <= per_sm * ctx.num_sms) {
         BlockJacArgs b;
         b.W = W.m.p;
         b.ldw = W.m.ld;
@@ -1400,8 +1646,33 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         void* args[] = {&b};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
                                               args, bj_smem, ctx.stream));
+    } else if (forced != 4 && forced != 5 && n > 2 * kSC2 && (ceil_div(n, kSGB) + 1) / 2 <= ctx.num_sms &&
+               m >= 2 * kSCR) {
+        // columns too long for shared memory: streaming Gram block Jacobi, 48-column pairs
+        static bool attr = false;
+        if (!attr) {
+            RLRA_CUDA(cudaFuncSetAttribute(sgram_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kSGramSmem)));
+            attr = true;
+        }
+        GramJacArgs g{};
+        g.bar = ctx.gbar;
+        g.W = W.m.p;
+        g.ldw = W.m.ld;
+        g.m = m;
+        g.n = n;
+        g.V = V.m.p;
+        g.ldv = V.m.ld;
+        g.nb = ceil_div(n, kSGB) + (ceil_div(n, kSGB) & 1);
+        g.flags = flags.i();
+        Buf verb(ctx, sizeof(unsigned) * g.nb);
+        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
+        g.ver = static_cast<unsigned*>(verb.p);
+        void* args[] = {&g};
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)sgram_jacobi_kernel, dim3(g.nb / 2), dim3(256), args, kSGramSmem,
+                                              ctx.stream));
     } else if (forced != 4 && n > 2 * kGB) {
-        // columns too long for shared memory: Gram block Jacobi
+        // columns too long for shared memory: Gram block Jacobi (32-column blocks)
         static int gram_cap = 0;
         if (!gram_cap) {
             RLRA_CUDA(cudaFuncSetAttribute(gram_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
