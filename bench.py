@@ -396,13 +396,16 @@ def main():
                                   R.Omega.philox(seed), Uh.data_ptr(), Sh.data_ptr(), Vh.data_ptr())
             path = "rlra_rsvd(loc=RLRA_HOST), pinned host A, row-chunked upload overlapped with the sketch"
         else:
-            def estep(seed):  # each rank uploads its shard, factors, downloads its U rows
-                Ad.t.copy_(Ah)
-                step(seed)
-                Uh.copy_(out["U"].t[: m_loc * k])
-                Sh.copy_(out["S"].t[:k])
-                Vh.copy_(out["V"].t[: n * k])
-            path = "rlra_rsvd_rowsharded with per-rank pinned host shards"
+            del A, Ad
+            out.clear()
+            torch.cuda.empty_cache()
+
+            def estep(seed):  # each rank's drop-in call with its pinned host shard
+                eng.host_rsvd_rowsharded_ptr(comm.handle, Ah.data_ptr(), m_loc, n, m_loc, m, k, p, q, s,
+                                             R.Omega.philox(seed), Uh.data_ptr(), m_loc, Sh.data_ptr(),
+                                             Vh.data_ptr(), n)
+            path = ("rlra_rsvd_rowsharded(loc=RLRA_HOST) per rank, pinned host shard, row-chunked upload "
+                    "overlapped with the local sketch")
 
         estep(SEED_OMEGA)
         if use_dist:

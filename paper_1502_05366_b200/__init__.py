@@ -613,11 +613,19 @@ class Engine:
         lib().rlra_comm_destroy(h)
 
     def device_rsvd_rowsharded(self, comm, a_ptr, m_local, n, lda, m_total, k, p, q, s, omega, u_ptr, ldu,
-                               sigma_ptr, v_ptr, ldv):
+                               sigma_ptr, v_ptr, ldv, loc=None):
         om = omega.struct()
-        _check(lib().rlra_rsvd_rowsharded(self._ctx, comm, DEVICE, C.c_void_p(a_ptr), m_local, n, _i64(lda),
-                                          _i64(m_total), k, p, q, s, C.byref(om), C.c_void_p(u_ptr), _i64(ldu),
-                                          C.c_void_p(sigma_ptr), C.c_void_p(v_ptr), _i64(ldv)))
+        _check(lib().rlra_rsvd_rowsharded(self._ctx, comm, DEVICE if loc is None else loc, C.c_void_p(a_ptr),
+                                          m_local, n, _i64(lda), _i64(m_total), k, p, q, s, C.byref(om),
+                                          C.c_void_p(u_ptr), _i64(ldu), C.c_void_p(sigma_ptr), C.c_void_p(v_ptr),
+                                          _i64(ldv)))
+
+    def host_rsvd_rowsharded_ptr(self, comm, a_ptr, m_local, n, lda, m_total, k, p, q, s, omega, u_ptr, ldu,
+                                 sigma_ptr, v_ptr, ldv):
+        """rlra_rsvd_rowsharded with this rank's shard in HOST memory: the
+        upload streams in row chunks under the local sketch GEMM."""
+        self.device_rsvd_rowsharded(comm, a_ptr, m_local, n, lda, m_total, k, p, q, s, omega, u_ptr, ldu,
+                                    sigma_ptr, v_ptr, ldv, loc=HOST)
 
     def id_rand_rowsharded(self, comm, a_local, row0, m_total, k, p, q_power, s, rng=None, omega=None):
         """rlra_id_rand_rowsharded with host buffers: a_local is this rank's

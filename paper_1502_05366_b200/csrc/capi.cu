@@ -845,10 +845,19 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
         check_sample_rank(k, p, int(m_total), n);
         check_sample(k + p, q, s, int(m_total), n);
         OmegaSource om = omega_of(omega);
-        In A(C, loc, a, m_local, n, lda, "a");
         Out U(C, loc, u, m_local, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
         OutVec<double> S(C, loc, sigma, k, "sigma");
-        rsvd_v2_rowsharded(C, comm->c, A.m, m_total, k, p, q, s, om, U.m, S.d, V.m);
+        if (loc == RLRA_HOST && m_local > 0 && n > 0) {
+            // host shard: the upload streams in row chunks under the local sketch GEMM
+            need(a, "a");
+            check_ld(lda, m_local, "a");
+            DMatBuf dA(C, m_local, n), Y(C, m_local, k + p);
+            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m);
+            rsvd_v2_rowsharded(C, comm->c, dA.m, m_total, k, p, q, s, om, U.m, S.d, V.m, &Y.m);
+        } else {
+            In A(C, loc, a, m_local, n, lda, "a");
+            rsvd_v2_rowsharded(C, comm->c, A.m, m_total, k, p, q, s, om, U.m, S.d, V.m);
+        }
         U.finish(C);
         V.finish(C);
         S.finish(C);

@@ -181,28 +181,35 @@ void comm_destroy(Comm& cm) {
 }
 
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
-                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V) {
+                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched) {
     const int n = int(A.cols), l = k + p;
-    DMatBuf Y(ctx, A.rows, l), Z(ctx, n, l);
-    sketch(ctx, Op::N, A, l, om, Y.m);                        // sketch.hpp:51-52
+    DMatBuf Yown, Z(ctx, n, l);
+    DMat Y;
+    if (sketched) {
+        Y = *sketched;  // Y_g = A_g Omega already formed (upload_and_sketch)
+    } else {
+        Yown = DMatBuf(ctx, A.rows, l);
+        Y = Yown.m;
+        sketch(ctx, Op::N, A, l, om, Y);                      // sketch.hpp:51-52
+    }
     {
         GemmTag tag(ctx, "gemm_power");
         for (int j = 1; j <= q; ++j) {                        // sketch.hpp:53-58
-            if ((2 * j - 2) % s == 0) orth_rowsharded(ctx, cm, Y.m, m_total, true);
-            gemm(ctx, Op::T, Op::N, 1.0, A, Y.m, 0.0, Z.m);    // Z_g = A_g^T Y_g
+            if ((2 * j - 2) % s == 0) orth_rowsharded(ctx, cm, Y, m_total, true);
+            gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z.m);    // Z_g = A_g^T Y_g
             allreduce(ctx, cm, Z.m.p, size_t(n) * l);          // Z = sum_g
             if ((2 * j - 1) % s == 0) orth_span_inplace(ctx, Z.m);  // replicated
-            gemm(ctx, Op::N, Op::N, 1.0, A, Z.m, 0.0, Y.m);    // Y_g = A_g Z
+            gemm(ctx, Op::N, Op::N, 1.0, A, Z.m, 0.0, Y);    // Y_g = A_g Z
         }
     }
-    orth_rowsharded(ctx, cm, Y.m, m_total, false);             // rsvd.hpp:157
+    orth_rowsharded(ctx, cm, Y, m_total, false);             // rsvd.hpp:157
     DMatBuf Bt(ctx, n, l);
     {
         GemmTag tag(ctx, "gemm_proj");
-        gemm(ctx, Op::T, Op::N, 1.0, A, Y.m, 0.0, Bt.m);       // rsvd.hpp:158
+        gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Bt.m);       // rsvd.hpp:158
         allreduce(ctx, cm, Bt.m.p, size_t(n) * l);
     }
-    finish_qr_bt(ctx, Y.m, Bt.m, k, U, sigma, V);              // replicated QR + Jacobi, local lift
+    finish_qr_bt(ctx, Y, Bt.m, k, U, sigma, V);              // replicated QR + Jacobi, local lift
 }
 
 

@@ -20,7 +20,7 @@ void comm_destroy(Comm& cm);
 // ranks of cm; U_g (m_g x k) row-sharded like A, sigma (device, k) and V
 // (n x k) replicated on every rank.
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
-                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V);
+                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr);
 
 // id_rand (interp.hpp:203-223) on the row-sharded A: jc (device, n) and V
 // (n x k) replicated.  Omega~ is m_total x l, this rank using rows

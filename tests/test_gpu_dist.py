@@ -81,6 +81,37 @@ def test_native_rowsharded_rsvd_world1_matches_engine():
     assert rel <= 1.01 * rel_e
 
 
+def test_native_rowsharded_rsvd_host_shard_matches_device_shard():
+    """rlra_rsvd_rowsharded with the shard in HOST memory (row-chunked upload
+    under the local sketch) gives the device-shard result: same sigma, same
+    reconstruction, U and V equal to rounding."""
+    import torch
+
+    from paper_1502_05366_b200 import dist as D
+    from paper_1502_05366_b200.testmat import gen_test_matrix_device
+
+    eng = R.Engine(0)
+    torch.cuda.set_device(0)
+    m, n, k, p, q = 5000, 2400, 80, 10, 2
+    A, _ = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(1200) / 25.0), seed=19)
+    a_host = np.asfortranarray(A.view(n, m).t().cpu().numpy())
+    comm = D.NcclComm(eng)
+    try:
+        U, S, V = D.rsvd_v2_native(comm, D.DM(A, m, n), m, k, p, q, 1, R.Omega.philox(77))
+        uh = np.zeros((m, k), order="F")
+        vh = np.zeros((n, k), order="F")
+        sh = np.zeros(k)
+        eng.host_rsvd_rowsharded_ptr(comm.handle, a_host.ctypes.data, m, n, m, m, k, p, q, 1, R.Omega.philox(77),
+                                     uh.ctypes.data, m, sh.ctypes.data, vh.ctypes.data, n)
+    finally:
+        comm.close()
+    s_d = S.t.cpu().numpy()
+    assert np.max(np.abs(sh - s_d) / s_d) <= 1e-12
+    u_d = U.t[: m * k].view(k, m).t().cpu().numpy()
+    v_d = V.t[: n * k].view(k, n).t().cpu().numpy()
+    assert np.linalg.norm((uh * sh) @ vh.T - (u_d * s_d) @ v_d.T) <= 1e-10 * np.linalg.norm(a_host)
+
+
 def test_native_rowsharded_row_permutation_invariance():
     """The sharded driver's sums are row-order independent: permuting A's
     rows (what a different row partition does to the association order)
