@@ -235,6 +235,12 @@ rlra_status rlra_qb_hierarchical_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int 
                                             int n, int64_t lda, int64_t m_total, int num_row_blocks, int blk,
                                             int num_blocks, int q_power, const rlra_omega* omega, double* q,
                                             int64_t ldq, double* b, int64_t ldb, double* final_residual);
+/* rsvd_v2 (rsvd.hpp:154-160) with A row-sharded over the ranks: rank g holds
+ * m_local rows of the m_total x n matrix; the Grams and the n x l partials
+ * A_g^T Y_g are allreduced (the north_star exchange), the l x l work is
+ * replicated.  u: this rank's m_local x k rows of U; sigma, v replicated.
+ * loc = RLRA_HOST: the shard is uploaded in row chunks under the local
+ * sketch GEMM (as rlra_rsvd does for a host A). */
 rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const double* a, int m_local, int n,
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,
