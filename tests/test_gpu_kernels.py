@@ -8,6 +8,8 @@ import pytest
 import paper_1502_05366_b200 as R
 from helpers import exact_rank, match_columns_up_to_sign, orthonormality_defect, rel_fro
 
+ROOT = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+
 pytestmark = pytest.mark.gpu
 
 
@@ -100,8 +102,12 @@ def test_orth_rejects_wide(eng):
         eng.orth(np.zeros((3, 5)))
 
 
-@pytest.mark.parametrize("m,n,k", [(60, 40, 15), (35, 50, 20), (50, 30, 25), (610, 3000, 610)])
+@pytest.mark.parametrize("m,n,k", [(60, 40, 15), (35, 50, 20), (50, 30, 25), (610, 3000, 610), (900, 1500, 300),
+                                   (200, 30000, 50)])
 def test_pivoted_qr_vs_oracle(eng, orc, m, n, k):
+    """(900, 1500): trailing columns longer than the register tile take the
+    loop form for the first steps; (200, 30000): the position maps do not fit
+    shared memory, so the two-barrier kernel runs."""
     rs = np.random.default_rng(m * 3 + n)
     a = rs.standard_normal((m, n))
     got = eng.pivoted_qr_partial(a, k)
@@ -222,6 +228,31 @@ def test_small_svd_shared_gram_jacobi_vs_oracle(eng, orc, m, n, kind):
         assert np.max(np.abs(s - so) / so) <= 1e-10
     assert rel_fro((u * s) @ v.T, a) <= 1e-12
     assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
+
+
+@pytest.mark.parametrize("env", [{"RLRA_BGRAM_NOHELP": "1"}, {"RLRA_SVD_KERNEL": "block"},
+                                 {"RLRA_BGRAM_BW": "16"}, {"RLRA_SVD_KERNEL": "gram"}])
+def test_small_svd_variants_agree(eng, env):
+    """The Jacobi variants selectable by environment (bgram without V
+    helpers, 16-column blocks, the one-sided block kernel, the 32-column
+    streaming kernel) give the default path's sigma and reconstruction."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    rs = np.random.default_rng(5)
+    a = rs.standard_normal((600, 400)) * np.exp(-np.arange(400) / 60.0)
+    u, s, v = eng.small_svd(a)
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import paper_1502_05366_b200 as R; "
+            "a = np.random.default_rng(5).standard_normal((600, 400)) * np.exp(-np.arange(400) / 60.0); "
+            "u, s, v = R.Engine(0).small_svd(a); print(json.dumps(s.tolist()))" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    s2 = np.array(json.loads(out.stdout.strip().splitlines()[-1]))
+    assert np.max(np.abs(s2 - s) / s) <= 1e-12
+    assert rel_fro((u * s) @ v.T, a) <= 1e-12
 
 
 def test_small_svd_kats(eng):
