@@ -10,7 +10,8 @@ re-orthonormalisation, projection, QR of B^T, Jacobi SVD of R, lift).
 
 metric  : effective FP64 TFLOP/s = F_gemm / step time with
           F_gemm = 4 m n l (q+1) (SURVEY.md §8d; 2.448e13 flop for C5);
-value   : A resident in HBM, Omega generated in-register (Philox);
+value   : A resident in HBM, Omega drawn from Philox inside the call
+          (materialised once, n x l, then the streaming GEMM);
 e2e     : the same call through the C-ABI with HOST buffers (pinned A in,
           U/sigma/V out), host<->device copies inside the timed region; the
           engine streams the 32 GB upload in row chunks on a copy stream
@@ -357,7 +358,7 @@ def main():
         "data": "synthetic: A = U diag(exp(-j/100)) V^T, U,V orthonormalised Philox Gaussians "
                 "(3685 modes), generated on the GPU",
         "config": {"workload": f"C5 rsvd_v2 m={m} n={n} k={k} p={p} q={q} s={s}",
-                   "omega": "philox in-register", "l2": "A (32 GB) >> L2; no flush needed",
+                   "omega": "philox (materialised per call, n x l)", "l2": "A (32 GB) >> L2; no flush needed",
                    "parallelism": "1 GPU" if not use_dist else
                    f"A row-sharded over {world} GPUs ({m_loc} rows/rank), C++ driver "
                    "(rlra_rsvd_rowsharded) with NCCL allreduce of Grams and n x l partials"},
