@@ -736,6 +736,38 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     return fma(0.5 * y, r, y);
 }
 
+// two Newton steps: ~1e-14 relative — for quantities whose rounding does not
+// reach the rotation's orthogonality (hypot and 1/x inside t; c and s are
+// formed from t consistently, c with the full-precision rsqrt_nr)
+__device__ __forceinline__ double rcp_nr2(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr2(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    double e = fma(-hx * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-hx * y, y, 0.5);
+    return fma(y, e, y);
+}
+
+// OR-reduction barrier over the first `nthreads` threads (named barrier 1)
+__device__ __forceinline__ int bar_or_partial(int nthreads, int pred) {
+    int r;
+    asm volatile(
+        "{\n.reg .pred p, q;\nsetp.ne.s32 p, %1, 0;\nbar.red.or.pred q, 1, %2, p;\nselp.s32 %0, 1, 0, q;\n}\n"
+        : "=r"(r)
+        : "r"(pred), "r"(nthreads)
+        : "memory");
+    return r;
+}
+
 // The reference rotation (core/jacobi.hpp:170-180) for the pair with Gram
 // entries (app, aqq, apq): skip unless |apq| > eps sqrt(app aqq); then
 // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (aqq - app) / (2 apq),
@@ -750,8 +782,8 @@ __device__ __forceinline__ bool jac_rotation_fast(double app, double aqq, double
     const double h2 = fma(d, d, e * e);
     const bool ok = pr > 1e-290 && pr < 1e290 && h2 > 1e-290 && h2 < 1e290;
     act = apq * apq > 1e-30 * pr;
-    const double h = h2 * rsqrt_nr(h2);
-    const double tm = fabs(e) * rcp_nr(fabs(d) + h);
+    const double h = h2 * rsqrt_nr2(h2);
+    const double tm = fabs(e) * rcp_nr2(fabs(d) + h);
     const double t = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? tm : -tm;
     const double cc = rsqrt_nr(fma(t, t, 1.0));
     c = act ? cc : 1.0;
@@ -1008,9 +1040,9 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                 mark(1);
                 // ---- 2. the visit's steps on G: thread (k, l) owns pair block (k, l)
                 int rot = 0;
-                {
+                if (t < BW * BW) {  // the pair-block owners only: a named barrier of BW*BW threads per step
                     const int k = t / BW, l = t % BW;
-                    const bool own = t < BW * BW;
+                    const bool own = true;
                     const int nsteps = intra ? BW - 1 : BW;
                     for (int st = 0; st < nsteps; ++st) {
                         const double* Gc = G0 + (st & 1) * C2 * GP;
@@ -1060,9 +1092,10 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                                 Gn[ql * GP + qk] = b11;
                             }
                         }
-                        rot |= __syncthreads_or(act);
+                        rot |= (BW * BW == 256) ? __syncthreads_or(act) : bar_or_partial(BW * BW, act);
                     }
                 }
+                rot = __syncthreads_or(rot);
                 mark(2);
                 if (rot && t == 0) flags[sweep % 3] = 1;
                 if (helpers) {
