@@ -80,6 +80,7 @@ def c2():
                                          Q.data_ptr(), m, B.data_ptr(), cap, cap)
 
     tq = timed(qb, 1)
+    qb_ph = phases(qb)
     ell = out["f"]["ell"]
     U = torch.empty(m * ell, dtype=torch.float64, device="cuda")
     V = torch.empty(n * ell, dtype=torch.float64, device="cuda")
@@ -94,7 +95,7 @@ def c2():
     stt = st.cpu().numpy()
     return dict(config="C2", entry="qb_blocked(b=100,M=80,tol=1e-6,q=1) + svd_from_qb(k=0)", m=m, n=n,
                 ell=ell, blocks=len(out["f"]["history"]), final_residual=out["f"]["final_residual"],
-                tolerance_reached=out["f"]["tolerance_reached"], qb_time_s=tq, svd_time_s=ts, time_s=tq + ts, svd_phases_ms=ph,
+                tolerance_reached=out["f"]["tolerance_reached"], qb_time_s=tq, svd_time_s=ts, time_s=tq + ts, qb_phases_ms=qb_ph, svd_phases_ms=ph,
                 sigma_top100_rel_vs_true=float(np.max(np.abs(s[:100] - stt[:100]) / stt[:100])))
 
 
