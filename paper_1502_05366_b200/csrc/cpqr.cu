@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
         // arithmetic in the same order as the loop form below).
         double bv = -DBL_MAX, tr = 0.0;
         int bp = INT_MAX;
-        auto downdate = [&](int j, int pos, double d, double s2, bool have_s2) {
+        auto downdate = [&](int j, int pos, double d, double s2) {
             double c = cnS[j - j0] - d * d;
             const double ref = rnS[j - j0];
             double rr = ref;
@@ -445,7 +445,6 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
                 }
                 tr += s2;
             }
-            (void)have_s2;
             __syncwarp();
             if (lane == 0) {
                 cnS[j - j0] = c;
@@ -514,7 +513,7 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
                         }
                         s2 = warp_sum(s2);
                     }
-                    if (on[b]) downdate(jj[b], s2p[jj[b]], d, s2, true);
+                    if (on[b]) downdate(jj[b], s2p[jj[b]], d, s2);
                 }
             }
         } else {
@@ -535,7 +534,7 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
                     for (int i = f + 1 + lane; i < m; i += 32) s2 += wj[i] * wj[i];
                     s2 = warp_sum(s2);
                 }
-                downdate(j, pos, d, s2, true);
+                downdate(j, pos, d, s2);
             }
         }
         mark(2);
