@@ -335,29 +335,53 @@ __global__ void __launch_bounds__(384, 1)
     // ---------------------------------------------------------- epilogue ---
     // C element of acc[i][j][h]: row = arow[i] (this lane's lr), column = the
     // B-fragment row that lane (lr' = 2 lc + h) holds
+    // EPI_RESID loads a group of two row fragments' R values first: C may
+    // alias R (the in-place W <- W - Q_i B_i of the blocked QB), so loads left
+    // inside the store loop would each wait a full memory round trip.  (The
+    // other epilogues keep the plain loop: a load group there costs the
+    // streaming kernels registers at the 168-register cap.)
     double local = 0.0;
+    constexpr int RG = 2;  // row fragments per load group
 #pragma unroll
-    for (int i = 0; i < MF; ++i) {
-        const int row = m0 + arow[i];
+    for (int i0 = 0; i0 < MF; i0 += RG) {
+        double rin[RG][NF][2];
+        if (EPI == EPI_RESID) {
 #pragma unroll
-        for (int j = 0; j < NF; ++j) {
+            for (int ii = 0; ii < RG; ++ii) {
+                const int row = m0 + arow[i0 + ii];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
-                if (row < p.M && col < p.N) {
-                    const double v = acc[i][j][h];
-                    if (EPI == EPI_STORE && tpart >= 0) {
-                        const int64_t slot = int64_t(tile - p.tail_base) * p.tail_split + tpart;
-                        p.tail_ws[slot * (kTBM * kTBN) + (row - m0) + (col - n0) * kTBM] = v;
-                    } else if (EPI == EPI_STORE) {
-                        double* c = p.C + row + int64_t(col) * p.ldc;
-                        *c = p.beta == 0.0 ? p.alpha * v : p.alpha * v + p.beta * *c;
-                    } else if (EPI == EPI_SPLIT) {
-                        p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
-                    } else {
-                        const double d = p.R[row + int64_t(col) * p.ldr] - p.alpha * v;
-                        if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
-                        local += d * d;
+                for (int j = 0; j < NF; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
+                        rin[ii][j][h] = (row < p.M && col < p.N) ? p.R[row + int64_t(col) * p.ldr] : 0.0;
+                    }
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < RG; ++ii) {
+            const int i = i0 + ii;
+            const int row = m0 + arow[i];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
+                    if (row < p.M && col < p.N) {
+                        const double v = acc[i][j][h];
+                        if (EPI == EPI_STORE && tpart >= 0) {
+                            const int64_t slot = int64_t(tile - p.tail_base) * p.tail_split + tpart;
+                            p.tail_ws[slot * (kTBM * kTBN) + (row - m0) + (col - n0) * kTBM] = v;
+                        } else if (EPI == EPI_STORE) {
+                            double* c = p.C + row + int64_t(col) * p.ldc;
+                            *c = p.beta == 0.0 ? p.alpha * v : p.alpha * v + p.beta * *c;
+                        } else if (EPI == EPI_SPLIT) {
+                            p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
+                        } else {
+                            const double d = rin[ii][j][h] - p.alpha * v;
+                            if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
+                            local += d * d;
+                        }
                     }
                 }
             }
