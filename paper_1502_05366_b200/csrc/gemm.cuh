@@ -282,6 +282,18 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) dgemm_kernel(co
 #pragma unroll
     for (int i = 0; i < MF; ++i) {
         const int row = m0 + wm * WM + i * 8 + lr;
+        // EPI_RESID: this fragment row's R values first (C may alias R, so
+        // loads inside the store loop would each wait a round trip)
+        double rin[NF][2];
+        if (EPI == EPI_RESID) {
+#pragma unroll
+            for (int j = 0; j < NF; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = n0 + wn * WN + j * 8 + lc * 2 + h;
+                    rin[j][h] = (row < p.M && col < p.N) ? p.R[row + int64_t(col) * p.ldr] : 0.0;
+                }
+        }
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
 #pragma unroll
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) dgemm_kernel(co
                     } else if (EPI == EPI_SPLIT) {
                         p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
                     } else {
-                        const double d = p.R[row + int64_t(col) * p.ldr] - p.alpha * v;
+                        const double d = rin[j][h] - p.alpha * v;
                         if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
                         local += d * d;
                     }
@@ -441,6 +453,18 @@ __global__ void __launch_bounds__(128 + (BM / WM) * (BN / WN) * 32, 1) dgemm_ws_
 #pragma unroll
     for (int i = 0; i < MF; ++i) {
         const int row = m0 + wm * WM + i * 8 + lr;
+        // EPI_RESID: this fragment row's R values first (C may alias R, so
+        // loads inside the store loop would each wait a round trip)
+        double rin[NF][2];
+        if (EPI == EPI_RESID) {
+#pragma unroll
+            for (int j = 0; j < NF; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = n0 + wn * WN + j * 8 + lc * 2 + h;
+                    rin[j][h] = (row < p.M && col < p.N) ? p.R[row + int64_t(col) * p.ldr] : 0.0;
+                }
+        }
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
 #pragma unroll
@@ -454,7 +478,7 @@ __global__ void __launch_bounds__(128 + (BM / WM) * (BN / WN) * 32, 1) dgemm_ws_
                     } else if (EPI == EPI_SPLIT) {
                         p.ws[int64_t(split) * p.M * p.N + row + int64_t(col) * p.M] = v;
                     } else {
-                        const double d = p.R[row + int64_t(col) * p.ldr] - p.alpha * v;
+                        const double d = rin[j][h] - p.alpha * v;
                         if (p.C) p.C[row + int64_t(col) * p.ldc] = d;
                         local += d * d;
                     }
