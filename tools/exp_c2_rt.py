@@ -1,5 +1,6 @@
 """Experiment: the C2 R-hat (QR of B^T after qb_blocked at C2) — one-sided
-Jacobi on R versus on R^T: sweeps and time.  Prints JSON lines."""
+Jacobi on R versus on R1^T, R P = Q1 R1 a column-pivoted QR (Drmac-Veselic
+preconditioning): sweeps and time.  Prints JSON lines."""
 import json
 import os
 import sys
@@ -26,7 +27,12 @@ t0 = time.perf_counter()
 r = np.linalg.qr(Bh, mode="r")
 print(json.dumps({"ell": ell, "host_qr_s": time.perf_counter() - t0}), flush=True)
 r = np.triu(r)
-for name, mat in (("R", r), ("R^T", np.ascontiguousarray(r.T))):
+import scipy.linalg
+t0 = time.perf_counter()
+_, r1, piv = scipy.linalg.qr(r, pivoting=True, mode="economic")
+print(json.dumps({"host_qrcp_s": time.perf_counter() - t0}), flush=True)
+r1 = np.triu(r1)
+for name, mat in (("R", r), ("R1^T (QRCP-preconditioned)", np.asfortranarray(r1.T))):
     eng.profile(True)
     t0 = time.perf_counter()
     u, s, v = eng.small_svd(mat)
