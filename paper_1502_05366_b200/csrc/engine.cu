@@ -246,9 +246,10 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
         RLRA_CUDA(cudaMemcpyAsync(Om.m.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
                                   ctx.stream));
     }
-    // row chunks of whole 128-row GEMM tiles, ~16 of them for a large A
+    // row chunks of whole 128-row GEMM tiles, ~32 of them for a large A (the
+    // last chunk's sketch is the only part not hidden under the upload)
     const int64_t bytes = m * n * 8;
-    const int64_t nchunk = bytes >= (int64_t(256) << 20) ? 16 : 1;
+    const int64_t nchunk = bytes >= (int64_t(256) << 20) ? 32 : 1;
     const int64_t rows = std::max<int64_t>(128, ((m + nchunk - 1) / nchunk + 127) / 128 * 128);
     std::vector<cudaEvent_t> ev;
     cudaEvent_t ready;
