@@ -394,15 +394,28 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
 #pragma unroll
             for (int u = 0; u < 16; ++u) v[u] = s0[rg + 4 * u][cj];
             long long c_0 = clock64();
+            // The serial chain per column is barrier -> pivot load -> 1/d ->
+            // f -> the next pivot row's update -> store: the pivot test is
+            // branch-free, dref is read before the barrier, and 1/d comes from
+            // MUFU.RCP64H + three Newton steps (no slow-path guard).
+            bool all_ok = true;
             for (int k = 0; k < nb; ++k) {
+                const double dr = dref[k];
                 __syncthreads();
                 double d = s0[k][k];
-                if (!(d > 0.0) || !(d >= dref[k])) {
-                    d = fmax(d, 1e-300);
-                    if (t == 0) bad = 1;
-                }
-                if (t == 0) piv[k] = d;
-                const double f = s0[k][cj] * (1.0 / d);
+                const double skc = s0[k][cj];
+                const bool ok = (d > 0.0) && (d >= dr);
+                all_ok = all_ok && ok;
+                d = ok ? d : fmax(d, 1e-300);
+                double rd;
+                asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(d));
+                double er = fma(-d, rd, 1.0);
+                rd = fma(rd, er, rd);
+                er = fma(-d, rd, 1.0);
+                rd = fma(rd, er, rd);
+                er = fma(-d, rd, 1.0);
+                rd = fma(rd, er, rd);
+                const double f = skc * rd;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int i = rg + 4 * u;
@@ -412,7 +425,9 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
 #pragma unroll
                 for (int u = 0; u < 16; ++u)
                     if (rg + 4 * u == kn) s0[kn][cj] = v[u];
+                if (t == 0) piv[k] = d;
             }
+            if (t == 0 && !all_ok) bad = 1;
             __syncthreads();
             long long c_1 = clock64();
             // R = D^{-1/2} S (rows scaled), written back; X_JJ comes in phase B
