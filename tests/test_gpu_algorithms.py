@@ -157,6 +157,35 @@ def test_qb_exact_rank_stops_at_second_block(eng):
     assert np.linalg.norm(a - f["q"] @ f["b"]) < 1e-8
 
 
+def test_id_row_vs_oracle(eng, orc):
+    """interp.hpp:107-117: the row ID is the column ID of A^T with the roles
+    renamed — pivots identical, W within the reference tolerance."""
+    rs = np.random.default_rng(41)
+    a = rs.standard_normal((90, 12)) @ rs.standard_normal((12, 70)) + 1e-9 * rs.standard_normal((90, 70))
+    got = eng.id_row(a, 12)
+    want = orc.id_column(np.asfortranarray(a.T), 12)
+    np.testing.assert_array_equal(got["jr"][:12], want["jc"][:12])
+    assert rel_fro(got["w"], want["v"]) <= 1e-10
+    assert np.linalg.norm(a - got["w"] @ a[got["jr"][:12], :]) <= 1e-6 * np.linalg.norm(a)
+
+
+def test_id_from_qb_vs_oracle(eng, orc):
+    """interp.hpp:228-236: the column ID of B from a QB factorisation —
+    pivots identical to the oracle's ID of the same B; dimension errors as the
+    reference's."""
+    rs = np.random.default_rng(43)
+    a = rs.standard_normal((120, 15)) @ rs.standard_normal((15, 80))
+    qb = eng.qb_blocked(a, 5, 4, 0.0, 1, 1, rng=R.Rng(9))
+    got = eng.id_from_qb(qb, a, 10)
+    want = orc.id_column(np.asfortranarray(qb["b"]), 10)
+    np.testing.assert_array_equal(got["jc"][:10], want["jc"][:10])
+    assert rel_fro(got["v"], want["v"]) <= 1e-10
+    with pytest.raises(R.DimensionError):
+        eng.id_from_qb(qb, a[:, :50], 10)
+    with pytest.raises(R.DimensionError):
+        eng.id_from_qb(qb, a, qb["ell"] + 1)
+
+
 def test_qb_inplace_equals_copy(eng):
     a = make_test_matrix(60, 50, spectrum_exp(50, 6.0), seed=3)
     f1 = eng.qb_blocked(a, 5, 4, 0.0, 1, 1, rng=R.Rng(8))
