@@ -325,14 +325,30 @@ def test_matmul_tail_wave_split_vs_oracle(eng, orc, ta):
 
 
 def test_sketch_philox_in_register_equals_materialized(eng):
-    """The sketch GEMM's in-register Philox Omega is bit-identical to the
-    materialised Omega (rlra_gaussian_philox) multiplied by the same kernel."""
+    """The sketch (Philox Omega materialised by rlra_gaussian_philox, then the
+    streaming GEMM) equals A times the same materialised Omega, and the
+    in-GEMM generation (RLRA_SKETCH_FUSED=1: producer warps + 2-CTA cluster
+    sharing) produces the same bits."""
+    import json
+    import os
+    import subprocess
+    import sys
+
     rs = np.random.default_rng(11)
     m, n, l = 2048, 1000, 130
     a = rs.standard_normal((m, n))
     y = eng.sample_right(a, l, 0, 1, omega=R.Omega.philox(777))
     om = eng.gaussian_philox(n, l, seed=777)
     assert np.array_equal(y, eng.matmul(a, om))
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import paper_1502_05366_b200 as R; "
+            "a = np.random.default_rng(11).standard_normal((2048, 1000)); "
+            "y = R.Engine(0).sample_right(a, 130, 0, 1, omega=R.Omega.philox(777)); "
+            "print(json.dumps(y.ravel(order='F').tolist()))" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RLRA_SKETCH_FUSED": "1"},
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    yf = np.array(json.loads(out.stdout.strip().splitlines()[-1])).reshape((m, l), order="F")
+    assert np.array_equal(yf, y)
 
 
 @pytest.mark.parametrize("n", [1, 5, 64, 65, 200, 510, 1024, 1100])
