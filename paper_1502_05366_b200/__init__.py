@@ -766,6 +766,19 @@ class Engine:
                                       C.c_void_p(v_ptr), _i64(ldv), C.byref(ko)))
         return ko.value
 
+    def device_cur_rand(self, a_ptr, m, n, lda, k, p, q, s, omega, out):
+        """rlra_cur_rand on device buffers; `out` maps jc, jr, v, w, c, u, r to
+        device pointers (int32 / float64, leading dimensions n, m, m, k, k).
+        Returns (residual, qr_residual)."""
+        om = omega.struct()
+        res, qres = C.c_double(0), C.c_double(0)
+        _check(lib().rlra_cur_rand(self._ctx, DEVICE, C.c_void_p(a_ptr), m, n, _i64(lda), k, p, q, s, C.byref(om),
+                                   C.c_void_p(out["jc"]), C.c_void_p(out["jr"]), C.c_void_p(out["v"]),
+                                   _i64(max(1, n)), C.c_void_p(out["w"]), _i64(max(1, m)), C.c_void_p(out["c"]),
+                                   _i64(max(1, m)), C.c_void_p(out["u"]), _i64(max(1, k)), C.c_void_p(out["r"]),
+                                   _i64(max(1, k)), C.byref(res), C.byref(qres)))
+        return res.value, qres.value
+
     def device_id_rand(self, a_ptr, m, n, lda, k, p, q, s, omega, jc_ptr, v_ptr, ldv):
         om = omega.struct()
         res, cl = C.c_double(0), C.c_int(0)

@@ -115,13 +115,20 @@ def c3():
     t = timed(run, 3)
     ph = phases(run)
     F = 2.0 * m * n * l * (2 * q + 1)
-    # CUR through the public host API (includes the 1.6 GB upload)
+    # CUR on device buffers, then through the public host API (+ the 1.6 GB upload)
+    dev = {"jc": torch.empty(n, dtype=torch.int32, device="cuda"), "jr": torch.empty(m, dtype=torch.int32, device="cuda"),
+           "v": torch.empty(n * k, dtype=torch.float64, device="cuda"), "w": torch.empty(m * k, dtype=torch.float64, device="cuda"),
+           "c": torch.empty(m * k, dtype=torch.float64, device="cuda"), "u": torch.empty(k * k, dtype=torch.float64, device="cuda"),
+           "r": torch.empty(k * n, dtype=torch.float64, device="cuda")}
+    ptrs = {key: t.data_ptr() for key, t in dev.items()}
+    tcur = timed(lambda: eng.device_cur_rand(A.data_ptr(), m, n, m, k, p, q, 1, R.Omega.philox(12345), ptrs), 3)
     a_h = A.view(n, m).t().cpu().numpy()
     t0 = time.perf_counter()
     cur = eng.cur_rand(np.asfortranarray(a_h), k, p, q, 1, omega=R.Omega.philox(12345))
     tc = time.perf_counter() - t0
     return dict(config="C3", entry="id_rand + cur_rand", m=m, n=n, k=k, p=p, q=q, id_time_s=t,
-                id_tflops=F / t / 1e12, id_qr_residual=res["r"]["qr_residual"], cur_wall_s_host_api=tc,
+                id_tflops=F / t / 1e12, id_qr_residual=res["r"]["qr_residual"], cur_time_s=tcur,
+                cur_wall_s_host_api=tc,
                 cur_residual=cur["residual"], time_s=t, id_phases_ms=ph)
 
 
