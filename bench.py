@@ -59,6 +59,26 @@ def dist_env():
     return rank, world, local
 
 
+def self_launch(n):
+    """--gpus N without a launcher: start N ranks of this script (one process
+    per GPU, the environment torch.distributed.run would set) and wait; rank
+    0's stdout is the JSON line."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -237,6 +257,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
 
     import numpy as np
     import torch
@@ -244,11 +266,21 @@ def main():
     import paper_1502_05366_b200 as R
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.dist
     if use_dist:
         import torch.distributed as dist
+        # the driver reads nranks from NCCL's INIT lines; the algorithm and
+        # protocol are pinned so the row sums (and every replicated factor)
+        # are reproducible run to run (csrc/dist.cu pin_nccl_env)
+        if world > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         if world > 1:
             dist.init_process_group("nccl", device_id=dev)
         else:  # --dist at N=1: exercise the row-sharded path with a 1-rank NCCL group
@@ -280,14 +312,13 @@ def main():
         # allreduce of the Grams and of the n x l partials (dist.py)
         from paper_1502_05366_b200 import dist as D
 
-        be = D.GpuBackend(eng)
+        comm = D.NcclComm(eng)  # the C++ driver's own NCCL communicator
         bounds = np.linspace(0, m, world + 1).astype(int)
         row0, m_loc = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
-        Ad, sig_true = D.gen_test_matrix_rowsharded(be, n, row0, m_loc,
+        Ad, sig_true = D.gen_test_matrix_rowsharded(comm, n, row0, m_loc, m,
                                                     np.exp(-np.arange(3685) / 100.0), SEED_GEN)
         A = Ad.t
         out = {}
-        comm = D.NcclComm(eng)  # the C++ driver's own NCCL communicator
 
         def step(seed):  # csrc/dist.cu through rlra_rsvd_rowsharded
             out["U"], out["S"], out["V"] = D.rsvd_v2_native(comm, Ad, m, k, p, q, s, R.Omega.philox(seed))

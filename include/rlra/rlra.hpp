@@ -719,6 +719,19 @@ inline TwoSidedIdFactors two_sided_from_column(const DenseMatrix& a, IdFactors c
     out.jr = Permutation(std::move(jr));
     return out;
 }
+// interp.hpp:143-156: U = argmin ||U R - V^T||_F (compact QR of R^T on the
+// device); a rank-deficient R names the offending skeleton row jr[i].
+inline DenseMatrix cur_linkage(const DenseMatrix& r, const DenseMatrix& v, const Permutation& jr) {
+    const int k = r.rows();
+    DenseMatrix u(k, k);
+    if (k == 0) return u;
+    if (jr.size() < k) throw DimensionError(msg("cur_linkage: %d skeleton rows for rank %d", jr.size(), k));
+    if (v.rows() != r.cols() || v.cols() != k)
+        throw DimensionError(msg("cur_linkage: V is %dx%d, need %dx%d", v.rows(), v.cols(), r.cols(), k));
+    check(rlra_cur_linkage(ctx(), RLRA_HOST, r.data(), k, r.cols(), std::max(1, k), v.data(), std::max(1, v.rows()),
+                           jr.indices().data(), u.data(), std::max(1, k)));
+    return u;
+}
 inline CurFactors cur_from_two_sided(const DenseMatrix& a, const TwoSidedIdFactors& ts) {
     CurFactors out;
     out.k = ts.k;

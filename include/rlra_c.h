@@ -6,7 +6,7 @@
  * C++20 library whose operator API is the free functions of namespace rlra.
  * It has no C ABI of its own; the functions below are what a binding of that
  * API needs, one entry point per reference function on the hot path
- * (SURVEY.md §8b).  include/rlra/*.hpp re-declares the reference API with the
+ * (SURVEY.md §8b).  include/rlra/<name>.hpp re-declares the reference API with the
  * exact signatures and implements it over this header, so C++ callers switch
  * by changing the include path; INTEGRATION.md shows the ctypes binding.
  *
@@ -30,6 +30,7 @@
 #ifndef RLRA_C_H
 #define RLRA_C_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -193,6 +194,47 @@ typedef struct rlra_comm rlra_comm;
 rlra_status rlra_comm_unique_id(unsigned char id[128]);
 rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nranks, int rank, rlra_comm** out);
 rlra_status rlra_comm_destroy(rlra_comm* comm);
+/* Host-staged collectives: the same drivers over collectives the caller
+ * supplies (MPI, gloo, shared memory, ...).  Each exchanged buffer is copied
+ * to pinned host memory after the context stream drains, combined by these
+ * functions (0 = success; anything else fails the call with RLRA_ENCCL), and
+ * copied back, so no kernel of one rank ever waits on another rank.
+ *   allreduce_sum: in-place elementwise sum of count doubles over the ranks;
+ *                  every rank must receive the same bits.
+ *   allgather:     recv[r * count + i] = rank r's send[i].
+ *   gpu_acquire / gpu_release (both or neither): a token held while this
+ *                  rank's GPU work is in flight; the drivers release it while
+ *                  they wait in a collective.  Ranks sharing one GPU use it to
+ *                  keep one rank's kernels on the device at a time. */
+typedef struct rlra_host_collectives {
+    int (*allreduce_sum)(void* user, double* buf, size_t count);
+    int (*allgather)(void* user, const double* send, double* recv, size_t count);
+    void (*gpu_acquire)(void* user);
+    void (*gpu_release)(void* user);
+    void* user;
+} rlra_host_collectives;
+rlra_status rlra_comm_create_host(rlra_ctx* ctx, int nranks, int rank, const rlra_host_collectives* coll,
+                                  rlra_comm** out);
+/* An in-process group of nranks ranks run as threads (one rlra_ctx each):
+ * shared-memory collectives (sums formed in rank order on every rank), a
+ * barrier that fails with RLRA_ENCCL after timeout_s (<= 0: the
+ * RLRA_COMM_TIMEOUT_S default, 600 s) instead of hanging, and a GPU token. */
+typedef struct rlra_local_group rlra_local_group;
+rlra_status rlra_local_group_create(int nranks, double timeout_s, rlra_local_group** out);
+rlra_status rlra_local_group_collectives(rlra_local_group* g, int rank, rlra_host_collectives* out);
+rlra_status rlra_local_group_destroy(rlra_local_group* g);
+/* Failure detection (NCCL communicators): waits poll ncclCommGetAsyncError and
+ * abort the communicator (ncclCommAbort) on an asynchronous error or after
+ * RLRA_COMM_TIMEOUT_S seconds (default 600), failing with RLRA_ENCCL instead of
+ * hanging.  NCCL_ALGO=Ring and NCCL_PROTO=Simple are pinned (unless set) so the
+ * reduction order, and every replicated factor, is fixed run to run. */
+/* Rows [row0, row0 + m_local) of the rlra_gen_test_matrix matrix (testmat.hpp:
+ * 65-74 semantics) of an m_total x n A: U's Philox rows are orthonormalised
+ * across the ranks (distributed CholQR2), V replicated; equal to the
+ * single-GPU generator's rows up to rounding. */
+rlra_status rlra_gen_test_matrix_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, int64_t row0, int m_local,
+                                            int64_t m_total, int n, const double* sigma, int r, uint64_t seed,
+                                            double noise, double* a, int64_t lda);
 /* rsvd_v2 with A's rows [row0, row0 + m_local) on this rank (a: m_local x n,
  * loc host or device); U: this rank's m_local x k rows of U; sigma (k) and V
  * (n x k) replicated.  Omega: Philox (identical on every rank) or a callback
@@ -375,6 +417,13 @@ rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int
                                     int64_t lda, const int* jc, const int* jr, const double* v,
                                     int64_t ldv, int k, double* c, int64_t ldc, double* u,
                                     int64_t ldu, double* r, int64_t ldr, double* residual);
+
+/* interp.hpp:143-156 (rlra::detail::cur_linkage): u (k x k) =
+ * argmin ||U R - V^T||_F via a compact QR of R^T, for r (k x n) and v (n x k).
+ * jr: at least k HOST ints (the skeleton rows, named in the NumericalError
+ * when R is rank-deficient to working precision: |R^(i,i)| < 1e-13 max). */
+rlra_status rlra_cur_linkage(rlra_ctx* ctx, int loc, const double* r, int k, int n, int64_t ldr,
+                             const double* v, int64_t ldv, const int* jr, double* u, int64_t ldu);
 
 /* interp.hpp:240: everything cur_rand produces, plus the column/row ID parts. */
 rlra_status rlra_cur_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,

@@ -198,6 +198,96 @@ def _omega(omega, rng, substream=False):
     return omega
 
 
+class _HostColl(C.Structure):  # rlra_host_collectives
+    _fields_ = [("allreduce_sum", C.c_void_p), ("allgather", C.c_void_p), ("gpu_acquire", C.c_void_p),
+                ("gpu_release", C.c_void_p), ("user", C.c_void_p)]
+
+
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_t)
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t)
+_TOKEN_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+
+class HostCollectives:
+    """Collectives written in Python for rlra_comm_create_host:
+    ``allreduce_sum(buf)`` sums the float64 numpy array over the ranks in
+    place; ``allgather(send, recv)`` fills recv[r*n:(r+1)*n] with rank r's
+    send; ``gpu_acquire`` / ``gpu_release`` (optional) guard the GPU token.
+    A Python exception fails the driver call with RLRA_ENCCL."""
+
+    def __init__(self, allreduce_sum, allgather, gpu_acquire=None, gpu_release=None):
+        import traceback
+
+        def ar(_user, buf, count):
+            try:
+                allreduce_sum(np.ctypeslib.as_array(buf, (count,)))
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def ag(_user, send, recv, count):
+            try:
+                allgather(np.ctypeslib.as_array(send, (count,)),
+                          np.ctypeslib.as_array(recv, (count * self.world_hint,)) if self.world_hint else None)
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        self.world_hint = 0  # set by Engine.comm_create_host
+        self._fns = [_ALLREDUCE_FN(ar), _ALLGATHER_FN(ag)]
+        if (gpu_acquire is None) != (gpu_release is None):
+            raise RlraError("gpu_acquire and gpu_release go together")
+        if gpu_acquire is not None:
+            self._fns += [_TOKEN_FN(lambda _u: gpu_acquire()), _TOKEN_FN(lambda _u: gpu_release())]
+
+    def struct(self):
+        h = _HostColl()
+        h.allreduce_sum = C.cast(self._fns[0], C.c_void_p).value
+        h.allgather = C.cast(self._fns[1], C.c_void_p).value
+        if len(self._fns) == 4:
+            h.gpu_acquire = C.cast(self._fns[2], C.c_void_p).value
+            h.gpu_release = C.cast(self._fns[3], C.c_void_p).value
+        return h
+
+
+class LocalGroup:
+    """rlra_local_group: ranks run as threads of this process (one Engine
+    each), collectives over shared memory in C++ (sums in rank order on every
+    rank), a barrier that fails after ``timeout_s`` instead of hanging, and a
+    GPU token so ranks sharing one device take turns on it."""
+
+    def __init__(self, nranks: int, timeout_s: float = 0.0):
+        self._h = C.c_void_p()
+        _check(lib().rlra_local_group_create(nranks, C.c_double(timeout_s), C.byref(self._h)))
+        self.nranks = nranks
+
+    def collectives(self, rank: int):
+        h = _HostColl()
+        _check(lib().rlra_local_group_collectives(self._h, rank, C.byref(h)))
+
+        class _Fixed:
+            world_hint = self.nranks
+
+            @staticmethod
+            def struct():
+                return h
+
+        return _Fixed()
+
+    def close(self):
+        if self._h:
+            lib().rlra_local_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """One device context (rlra_ctx)."""
 
@@ -607,6 +697,36 @@ class Engine:
         _check(lib().rlra_comm_create(self._ctx, (C.c_ubyte * 128).from_buffer_copy(uid), nranks, rank,
                                       C.byref(h)))
         return h
+
+    def comm_create_host(self, nranks: int, rank: int, collectives):
+        """rlra_comm_create_host over HostCollectives (Python) or
+        LocalGroup.collectives(rank) (C++ shared memory)."""
+        if isinstance(collectives, HostCollectives):
+            collectives.world_hint = nranks
+        h = C.c_void_p()
+        hc = collectives.struct()
+        self._keep_coll = getattr(self, "_keep_coll", []) + [collectives, hc]
+        _check(lib().rlra_comm_create_host(self._ctx, nranks, rank, C.byref(hc), C.byref(h)))
+        return h
+
+    def device_gen_test_matrix_rowsharded(self, comm, row0, m_local, m_total, n, sigma, seed, noise, out_ptr, ld):
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        _check(lib().rlra_gen_test_matrix_rowsharded(self._ctx, comm, DEVICE, _i64(row0), m_local, _i64(m_total), n,
+                                                     _d(sigma), len(sigma), C.c_uint64(seed), C.c_double(noise),
+                                                     C.c_void_p(out_ptr), _i64(ld)))
+
+    def rsvd_rowsharded(self, comm, a_local, m_total, k, p, q, s, rng=None, omega=None):
+        """rlra_rsvd_rowsharded with host buffers: (U_g, sigma, V)."""
+        a = _F(a_local)
+        mg, n = a.shape
+        om = _omega(omega, rng).struct()
+        u = np.zeros((mg, k), order="F")
+        sg = np.zeros(k)
+        v = np.zeros((n, k), order="F")
+        _check(lib().rlra_rsvd_rowsharded(self._ctx, comm, HOST, _d(a), mg, n, _i64(_ld(a)), _i64(m_total), k, p,
+                                          q, s, C.byref(om), _d(u), _i64(max(1, mg)), _d(sg), _d(v),
+                                          _i64(max(1, n))))
+        return u, sg, v
 
     @staticmethod
     def comm_destroy(h):

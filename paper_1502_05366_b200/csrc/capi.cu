@@ -644,6 +644,30 @@ rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const dou
     });
 }
 
+struct rlra_comm {
+    Comm c;
+};
+
+rlra_status rlra_gen_test_matrix_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, int64_t row0, int m_local,
+                                            int64_t m_total, int n, const double* sigma, int r, uint64_t seed,
+                                            double noise, double* a, int64_t lda) {
+    return guard(ctx, [&](Context& C) {
+        if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
+        if (row0 < 0 || m_local < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
+            raise(RLRA_EDIM, fmt("gen_test_matrix_rowsharded: rows [%lld, %lld) of %lld", (long long)row0,
+                                 (long long)(row0 + m_local), (long long)m_total));
+        if (r < 0 || r > std::min<int64_t>(m_total, n))
+            raise(RLRA_EDIM, fmt("gen_test_matrix: %d singular values for %lldx%d", r, (long long)m_total, n));
+        if (r > 0) need(sigma, "sigma");
+        Out A(C, loc, a, m_local, n, lda, "a");
+        gen_test_matrix_rowsharded(C, comm->c, std::vector<double>(sigma, sigma + r), seed, noise, row0, m_total,
+                                   A.m);
+        A.finish(C);
+        sync(C);
+    });
+}
+
 rlra_status rlra_verify_lowrank(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* x,
                                 int64_t ldx, const double* y, int64_t ldy, int k, const double* sigma_true, int r,
                                 double out[5]) {
@@ -710,10 +734,6 @@ rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int 
     });
 }
 
-struct rlra_comm {
-    Comm c;
-};
-
 rlra_status rlra_comm_unique_id(unsigned char id[128]) {
     try {
         if (!id) raise(RLRA_EINVAL, "null id buffer");
@@ -740,6 +760,70 @@ rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nra
     });
 }
 
+rlra_status rlra_comm_create_host(rlra_ctx* ctx, int nranks, int rank, const rlra_host_collectives* coll,
+                                  rlra_comm** out) {
+    return guard(ctx, [&](Context& C) {
+        if (!out || !coll) raise(RLRA_EINVAL, "null argument to rlra_comm_create_host");
+        *out = nullptr;
+        HostCollectives hc;
+        hc.allreduce_sum = coll->allreduce_sum;
+        hc.allgather = coll->allgather;
+        hc.gpu_acquire = coll->gpu_acquire;
+        hc.gpu_release = coll->gpu_release;
+        hc.user = coll->user;
+        auto* cm = new rlra_comm();
+        try {
+            comm_init_host(C, cm->c, nranks, rank, hc);
+        } catch (...) {
+            delete cm;
+            throw;
+        }
+        *out = cm;
+    });
+}
+
+struct rlra_local_group {
+    LocalGroup* g = nullptr;
+};
+
+rlra_status rlra_local_group_create(int nranks, double timeout_s, rlra_local_group** out) {
+    try {
+        if (!out) raise(RLRA_EINVAL, "null argument to rlra_local_group_create");
+        *out = nullptr;
+        auto* h = new rlra_local_group();
+        h->g = local_group_create(nranks, timeout_s);
+        *out = h;
+        return RLRA_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<rlra_status>(e.status);
+    }
+}
+
+rlra_status rlra_local_group_collectives(rlra_local_group* g, int rank, rlra_host_collectives* out) {
+    try {
+        if (!g || !out) raise(RLRA_EINVAL, "null argument to rlra_local_group_collectives");
+        const HostCollectives hc = local_group_collectives(g->g, rank);
+        out->allreduce_sum = hc.allreduce_sum;
+        out->allgather = hc.allgather;
+        out->gpu_acquire = hc.gpu_acquire;
+        out->gpu_release = hc.gpu_release;
+        out->user = hc.user;
+        return RLRA_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<rlra_status>(e.status);
+    }
+}
+
+rlra_status rlra_local_group_destroy(rlra_local_group* g) {
+    if (g) {
+        local_group_destroy(g->g);
+        delete g;
+    }
+    return RLRA_OK;
+}
+
 rlra_status rlra_comm_destroy(rlra_comm* comm) {
     if (!comm) return RLRA_OK;
     comm_destroy(comm->c);
@@ -754,6 +838,7 @@ rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, 
                                        double* hist, int* nhist, double* final_residual, int* reached) {
     return guard(ctx, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
         if (m_total < m_local || m_total > INT32_MAX)
             raise(RLRA_EDIM, fmt("qb_blocked_rowsharded: m_total %lld, local rows %d", (long long)m_total, m_local));
         if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
@@ -802,6 +887,7 @@ rlra_status rlra_qb_hierarchical_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int 
                                             int64_t ldq, double* b, int64_t ldb, double* final_residual) {
     return guard(ctx, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
         const int nrb = num_row_blocks, W = comm->c.nranks;
         if (nrb < 2 || (nrb & (nrb - 1)) != 0)
             raise(RLRA_EDIM, fmt("num_row_blocks must be one of {2,4,8,...} (got %d)", nrb));
@@ -840,6 +926,7 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
                                  int64_t ldv) {
     return guard(ctx, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
         if (m_total < m_local || m_total > INT32_MAX)
             raise(RLRA_EDIM, fmt("rsvd_rowsharded: m_total %lld, local rows %d", (long long)m_total, m_local));
         check_sample_rank(k, p, int(m_total), n);
@@ -871,6 +958,7 @@ rlra_status rlra_id_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, con
                                     double* qr_residual, int* clamped) {
     return guard(ctx, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
         if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
             raise(RLRA_EDIM, fmt("id_rand_rowsharded: rows [%lld, %lld) of %lld", (long long)row0,
                                  (long long)(row0 + m_local), (long long)m_total));
@@ -896,6 +984,7 @@ rlra_status rlra_cur_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, co
                                      int64_t ldr, double* residual, double* qr_residual) {
     return guard(ctx, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
+        CommGpuScope gpu_token(comm->c);
         if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
             raise(RLRA_EDIM, fmt("cur_rand_rowsharded: rows [%lld, %lld) of %lld", (long long)row0,
                                  (long long)(row0 + m_local), (long long)m_total));
@@ -1090,6 +1179,21 @@ rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int
         InVec<int> Jc(C, loc, jc, n, "jc"), Jr(C, loc, jr, m, "jr");
         In V(C, loc, v, n, k, ldv, "v");
         cur_core(C, loc, A.m, Jc.d, Jr.d, V.m, k, c, ldc, u, ldu, r, ldr, residual);
+    });
+}
+
+rlra_status rlra_cur_linkage(rlra_ctx* ctx, int loc, const double* r, int k, int n, int64_t ldr, const double* v,
+                             int64_t ldv, const int* jr, double* u, int64_t ldu) {
+    return guard(ctx, [&](Context& C) {
+        if (k < 0 || n < 0) raise(RLRA_EDIM, fmt("cur_linkage: negative dimensions %dx%d", k, n));
+        if (k == 0) return;
+        if (n < k) raise(RLRA_EDIM, fmt("cur_linkage: R is %dx%d, need at least as many columns as rows", k, n));
+        need(jr, "jr");
+        In R(C, loc, r, k, n, ldr, "r"), V(C, loc, v, n, k, ldv, "v");
+        Out U(C, loc, u, k, k, ldu, "u");
+        cur_linkage(C, R.m, V.m, k, U.m, jr);
+        U.finish(C);
+        sync(C);
     });
 }
 

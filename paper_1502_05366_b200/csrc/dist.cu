@@ -26,8 +26,14 @@
 #include <nccl.h>
 
 #include <cfloat>
+#include <chrono>
 #include <climits>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "cpqr.cuh"
 #include "dist.cuh"
@@ -46,6 +52,8 @@ struct NcclApi {
     decltype(&ncclAllReduce) all_reduce = nullptr;
     decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclCommAbort) comm_abort = nullptr;
+    decltype(&ncclCommGetAsyncError) get_async_error = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
 };
 
@@ -60,9 +68,11 @@ const NcclApi& nccl() {
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
         a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.comm_abort = reinterpret_cast<decltype(a.comm_abort)>(dlsym(h, "ncclCommAbort"));
+        a.get_async_error = reinterpret_cast<decltype(a.get_async_error)>(dlsym(h, "ncclCommGetAsyncError"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
         if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.all_gather || !a.comm_destroy ||
-            !a.error_string)
+            !a.comm_abort || !a.get_async_error || !a.error_string)
             raise(RLRA_ENCCL, "libnccl.so.2 lacks a required symbol");
         return a;
     }();
@@ -73,16 +83,73 @@ void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) raise(RLRA_ENCCL, fmt("%s: %s", what, nccl().error_string(r)));
 }
 
+// The reference promises bit-identical results for a fixed thread count
+// (core/matmul.hpp:13-15); the row sums here are NCCL's, so the
+// algorithm and protocol are pinned (unless the caller set them) to keep the
+// reduction order, and with it every replicated factor, fixed run to run.
+void pin_nccl_env() {
+    setenv("NCCL_ALGO", "Ring", 0);
+    setenv("NCCL_PROTO", "Simple", 0);
+}
+
+double env_timeout() {
+    const char* e = std::getenv("RLRA_COMM_TIMEOUT_S");
+    const double t = e ? std::atof(e) : 0.0;
+    return t > 0.0 ? t : 600.0;
+}
+
+// pinned staging for the host-staged collectives, grown on demand
+double* stage(Comm& cm, size_t count) {
+    if (count > cm.stage_cap) {
+        if (cm.stage) RLRA_CUDA(cudaFreeHost(cm.stage));
+        cm.stage = nullptr;
+        cm.stage_cap = 0;
+        RLRA_CUDA(cudaMallocHost(&cm.stage, sizeof(double) * count));
+        cm.stage_cap = count;
+    }
+    return cm.stage;
+}
+
 // in-place sum over the ranks, stream-ordered on the context stream
 void allreduce(Context& ctx, Comm& cm, double* p, size_t count) {
     if (count == 0) return;  // a 1-rank communicator still runs the collective (tests the plumbing)
-    nccl_check(nccl().all_reduce(p, p, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(cm.handle), ctx.stream),
-               "ncclAllReduce");
+    if (cm.kind == Comm::NCCL) {
+        nccl_check(nccl().all_reduce(p, p, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(cm.handle),
+                                     ctx.stream),
+                   "ncclAllReduce");
+        return;
+    }
+    double* h = stage(cm, count);
+    RLRA_CUDA(cudaMemcpyAsync(h, p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    int rc;
+    {
+        // this rank has no GPU work in flight while it waits for the others
+        if (cm.host.gpu_release) cm.host.gpu_release(cm.host.user);
+        rc = cm.host.allreduce_sum(cm.host.user, h, count);
+        if (cm.host.gpu_acquire) cm.host.gpu_acquire(cm.host.user);
+    }
+    if (rc != 0) raise(RLRA_ENCCL, fmt("host allreduce of %zu doubles failed (status %d)", count, rc));
+    RLRA_CUDA(cudaMemcpyAsync(p, h, sizeof(double) * count, cudaMemcpyHostToDevice, ctx.stream));
 }
 
+// recv[r * count + i] = rank r's send[i]
 void allgather(Context& ctx, Comm& cm, const double* send, double* recv, size_t count) {
-    nccl_check(nccl().all_gather(send, recv, count, ncclFloat64, static_cast<ncclComm_t>(cm.handle), ctx.stream),
-               "ncclAllGather");
+    if (cm.kind == Comm::NCCL) {
+        nccl_check(nccl().all_gather(send, recv, count, ncclFloat64, static_cast<ncclComm_t>(cm.handle),
+                                     ctx.stream),
+                   "ncclAllGather");
+        return;
+    }
+    const size_t tot = count * size_t(cm.nranks);
+    double* h = stage(cm, count + tot);
+    RLRA_CUDA(cudaMemcpyAsync(h, send, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (cm.host.gpu_release) cm.host.gpu_release(cm.host.user);
+    const int rc = cm.host.allgather(cm.host.user, h, h + count, count);
+    if (cm.host.gpu_acquire) cm.host.gpu_acquire(cm.host.user);
+    if (rc != 0) raise(RLRA_ENCCL, fmt("host allgather of %zu doubles failed (status %d)", count, rc));
+    RLRA_CUDA(cudaMemcpyAsync(recv, h + count, sizeof(double) * tot, cudaMemcpyHostToDevice, ctx.stream));
 }
 
 double allreduce_scalar(Context& ctx, Comm& cm, double x) {
@@ -90,7 +157,14 @@ double allreduce_scalar(Context& ctx, Comm& cm, double x) {
     RLRA_CUDA(cudaMemcpyAsync(b.p, &x, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
     allreduce(ctx, cm, b.d(), 1);
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, b.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    comm_sync(ctx, cm);
+    return ctx.h_scalars[0];
+}
+
+// a device scalar's value on the host, through the communicator-aware wait
+double read_scalar_comm(Context& ctx, Comm& cm, const double* d) {
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    comm_sync(ctx, cm);
     return ctx.h_scalars[0];
 }
 
@@ -113,30 +187,98 @@ void apply_rinv(Context& ctx, const DMat& Y, const DMat& Ri) {
     copy_mat(ctx, T, Y);
 }
 
-// shifted CholQR3 of the row-sharded Y (qr.cu shifted_cholqr3, distributed)
-void shifted_cholqr3_rowsharded(Context& ctx, Comm& cm, const DMat& Y, int64_t m_total) {
-    const int n = int(Y.cols);
-    Buf nrm(ctx, sizeof(double));
-    sum_squares(ctx, Y, nrm.d());
-    RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-    const double fro2 = allreduce_scalar(ctx, cm, ctx.h_scalars[0]);
-    const double shift = 11.0 * (double(m_total) * n + double(n) * (n + 1)) * 1.1102230246251565e-16 * fro2;
-    DMatBuf G(ctx, n, n), Ri(ctx, n, n);
-    gram_allreduce(ctx, cm, Y, G);
-    add_diag(ctx, G, shift);
-    if (!chol_upper_inv(ctx, G, Ri, 0.0))
-        raise(RLRA_ENUM, "rsvd (row-sharded): shifted CholQR3 broke down (rank-deficient sketch)");
-    apply_rinv(ctx, Y, Ri);
-    for (int pass = 0; pass < 2; ++pass) {
-        gram_allreduce(ctx, cm, Y, G);
-        if (!chol_upper_inv(ctx, G, Ri, ctx.cholqr_pivot_floor))
-            raise(RLRA_ENUM, "rsvd (row-sharded): sketch is rank deficient to working precision");
-        apply_rinv(ctx, Y, Ri);
+// TSQR of the row-sharded Y (north_star: "TSQR R factors are combined with an
+// allgather"), the rank-deficiency fallback of the distributed orth: a local
+// Householder QR Y_g = Q_g R_g (reference reflector rules), an allgather of
+// the R_g, a replicated Householder QR of their stack (every rank factors the
+// same bits, so every rank gets the same Qhat), and Y_g <- Q_g Qhat_g.  A rank
+// with fewer rows than columns contributes Y_g itself (Q_g = I), so the
+// stack is [R_0; ...] with sum_g min(m_g, n) >= n rows and Q is exactly
+// orthonormal: Q^T Q = sum_g Qhat_g^T Qhat_g = I.  Like the single-GPU
+// fallback (qr.cu householder_qr) it resolves exactly rank-deficient
+// sketches, where the reference's Householder orth (core/qr.hpp:95-129)
+// propagates unit vectors for numerically zero columns.
+void tsqr_rowsharded(Context& ctx, Comm& cm, const DMat& Y) {
+    const int mg = int(Y.rows), n = int(Y.cols), W = cm.nranks;
+    // every rank's row count
+    DMatBuf cnt(ctx, 1, W);
+    {
+        DMatBuf mine(ctx, 1, 1);
+        const double v = double(mg);
+        RLRA_CUDA(cudaMemcpyAsync(mine.m.p, &v, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+        allgather(ctx, cm, mine.m.p, cnt.m.p, 1);
+    }
+    std::vector<double> rows_h(static_cast<size_t>(W));
+    RLRA_CUDA(cudaMemcpyAsync(rows_h.data(), cnt.m.p, sizeof(double) * W, cudaMemcpyDeviceToHost, ctx.stream));
+    comm_sync(ctx, cm);
+    // local factor, padded to n x n
+    DMatBuf Rg(ctx, n, n);
+    zero_mat(ctx, Rg.m);
+    const bool tall = mg >= n;
+    if (tall) {
+        householder_qr(ctx, Y, &Rg.m);  // Y <- Q_g
+    } else if (mg > 0) {
+        copy_mat(ctx, Y, Rg.m.block(0, 0, mg, n));
+    }
+    DMatBuf allR(ctx, n, int64_t(n) * W);  // rank r's n x n block at columns [r n, (r+1) n)
+    allgather(ctx, cm, Rg.m.p, allR.m.p, size_t(n) * n);
+    // compacted stack: rank r contributes min(m_r, n) rows
+    int tot = 0, off = 0;
+    for (int r = 0; r < W; ++r) {
+        const int rr = std::min(int(rows_h[size_t(r)]), n);
+        if (r == cm.rank) off = tot;
+        tot += rr;
+    }
+    if (tot < n) raise(RLRA_EDIM, fmt("tsqr: %d stacked rows for %d columns", tot, n));
+    DMatBuf S(ctx, tot, n);
+    for (int r = 0, row = 0; r < W; ++r) {
+        const int rr = std::min(int(rows_h[size_t(r)]), n);
+        if (rr > 0) copy_mat(ctx, allR.m.block(0, int64_t(r) * n, rr, n), S.m.block(row, 0, rr, n));
+        row += rr;
+    }
+    householder_qr(ctx, S.m, nullptr);  // replicated: S <- Qhat
+    if (mg == 0) return;
+    if (tall) {
+        DMatBuf T(ctx, mg, n);
+        gemm(ctx, Op::N, Op::N, 1.0, Y, S.m.block(off, 0, n, n), 0.0, T.m);
+        copy_mat(ctx, T.m, Y);
+    } else {
+        copy_mat(ctx, S.m.block(off, 0, mg, n), Y);
     }
 }
 
-// CholQR2 (span_only: one pass) of the row-sharded Y, in place
+// shifted CholQR3 of the row-sharded Y (qr.cu shifted_cholqr3, distributed);
+// false when it breaks down (the decision is replicated: it depends only on
+// allreduced data)
+bool shifted_cholqr3_rowsharded(Context& ctx, Comm& cm, const DMat& Y, int64_t m_total) {
+    const int n = int(Y.cols);
+    Buf nrm(ctx, sizeof(double));
+    sum_squares(ctx, Y, nrm.d());
+    const double fro2 = allreduce_scalar(ctx, cm, read_scalar_comm(ctx, cm, nrm.d()));
+    if (!(fro2 > 0.0)) return false;
+    const double shift = 11.0 * (double(m_total) * n + double(n) * (n + 1)) * 1.1102230246251565e-16 * fro2;
+    DMatBuf G(ctx, n, n), Ri(ctx, n, n), Y0(ctx, Y.rows, n);
+    copy_mat(ctx, Y, Y0.m);  // kept for the TSQR fallback
+    gram_allreduce(ctx, cm, Y, G);
+    add_diag(ctx, G, shift);
+    bool ok = chol_upper_inv(ctx, G, Ri, 0.0);
+    if (ok) {
+        apply_rinv(ctx, Y, Ri);
+        for (int pass = 0; pass < 2 && ok; ++pass) {
+            gram_allreduce(ctx, cm, Y, G);
+            ok = chol_upper_inv(ctx, G, Ri, ctx.cholqr_pivot_floor);
+            if (ok) apply_rinv(ctx, Y, Ri);
+        }
+    }
+    if (!ok) copy_mat(ctx, Y0.m, Y);
+    return ok;
+}
+
+}  // namespace
+
+// CholQR2 (span_only: one pass) of the row-sharded Y, in place; shifted
+// CholQR3 when the Gram is too ill-conditioned, TSQR when even that breaks
+// down (an exactly rank-deficient sketch)
 void orth_rowsharded(Context& ctx, Comm& cm, const DMat& Y, int64_t m_total, bool span_only) {
     ProfScope prof(ctx, "orth", int(Y.rows), int(Y.cols), span_only ? 1 : 0, 0.0);
     GemmTag tag(ctx, "gemm_orth");
@@ -145,16 +287,42 @@ void orth_rowsharded(Context& ctx, Comm& cm, const DMat& Y, int64_t m_total, boo
     for (int pass = 0; pass < (span_only ? 1 : 2); ++pass) {
         gram_allreduce(ctx, cm, Y, G);
         if (!chol_upper_inv(ctx, G, Ri, ctx.cholqr_pivot_floor)) {
-            shifted_cholqr3_rowsharded(ctx, cm, Y, m_total);
+            if (!shifted_cholqr3_rowsharded(ctx, cm, Y, m_total)) tsqr_rowsharded(ctx, cm, Y);
             return;
         }
         apply_rinv(ctx, Y, Ri);
     }
 }
 
-}  // namespace
+
+void comm_sync(Context& ctx, Comm& cm) {
+    if (cm.kind != Comm::NCCL || !cm.handle) {
+        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 0;; ++it) {
+        const cudaError_t q = cudaStreamQuery(ctx.stream);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) RLRA_CUDA(q);
+        ncclResult_t as = ncclSuccess;
+        nccl_check(nccl().get_async_error(static_cast<ncclComm_t>(cm.handle), &as), "ncclCommGetAsyncError");
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (as != ncclSuccess || el > cm.timeout_s) {
+            nccl().comm_abort(static_cast<ncclComm_t>(cm.handle));
+            cm.handle = nullptr;
+            if (as != ncclSuccess)
+                raise(RLRA_ENCCL, fmt("NCCL asynchronous error: %s (communicator aborted)", nccl().error_string(as)));
+            raise(RLRA_ENCCL, fmt("collective did not complete within %.0f s (RLRA_COMM_TIMEOUT_S); communicator "
+                                  "aborted",
+                                  cm.timeout_s));
+        }
+        if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(it > 4096 ? 1000 : 20));
+    }
+}
 
 void comm_unique_id(unsigned char out[128]) {
+    pin_nccl_env();
     ncclUniqueId id;
     nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
     static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
@@ -164,20 +332,147 @@ void comm_unique_id(unsigned char out[128]) {
 void comm_init(Context& ctx, Comm& cm, const unsigned char id[128], int nranks, int rank) {
     if (nranks < 1 || rank < 0 || rank >= nranks)
         raise(RLRA_EINVAL, fmt("comm: rank %d of %d", rank, nranks));
+    pin_nccl_env();
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     ncclComm_t c = nullptr;
     RLRA_CUDA(cudaSetDevice(ctx.device));
     nccl_check(nccl().comm_init_rank(&c, nranks, uid, rank), "ncclCommInitRank");
+    cm.kind = Comm::NCCL;
     cm.handle = c;
     cm.nranks = nranks;
     cm.rank = rank;
     cm.device = ctx.device;
+    cm.timeout_s = env_timeout();
+}
+
+void comm_init_host(Context& ctx, Comm& cm, int nranks, int rank, const HostCollectives& hc) {
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        raise(RLRA_EINVAL, fmt("comm: rank %d of %d", rank, nranks));
+    if (!hc.allreduce_sum || !hc.allgather) raise(RLRA_EINVAL, "host collectives: allreduce_sum and allgather needed");
+    if (!hc.gpu_acquire != !hc.gpu_release) raise(RLRA_EINVAL, "host collectives: gpu_acquire without gpu_release");
+    cm.kind = Comm::HOST;
+    cm.handle = nullptr;
+    cm.host = hc;
+    cm.nranks = nranks;
+    cm.rank = rank;
+    cm.device = ctx.device;
+    cm.timeout_s = env_timeout();
 }
 
 void comm_destroy(Comm& cm) {
-    if (cm.handle) nccl().comm_destroy(static_cast<ncclComm_t>(cm.handle));
+    if (cm.kind == Comm::NCCL && cm.handle) nccl().comm_destroy(static_cast<ncclComm_t>(cm.handle));
     cm.handle = nullptr;
+    if (cm.stage) cudaFreeHost(cm.stage);
+    cm.stage = nullptr;
+    cm.stage_cap = 0;
+}
+
+// ------------------------------------------------------- LocalGroup ---
+struct LocalGroup {
+    int n = 1;
+    double timeout_s = 600.0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    bool broken = false;
+    std::vector<const double*> src;
+    std::vector<size_t> cnt;
+    std::mutex gpu;  // the GPU token
+    struct Slot {
+        LocalGroup* g;
+        int rank;
+    };
+    std::vector<Slot> slots;
+
+    // false on timeout (the group is then broken for every rank)
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (broken) return false;
+        const uint64_t gen = generation;
+        if (++arrived == n) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+            return true;
+        }
+        const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
+                                    [&] { return generation != gen || broken; });
+        if (!ok || broken) {
+            broken = true;
+            cv.notify_all();
+            return false;
+        }
+        return true;
+    }
+};
+
+namespace {
+
+int lg_allreduce(void* user, double* buf, size_t count) {
+    auto* sl = static_cast<LocalGroup::Slot*>(user);
+    LocalGroup& g = *sl->g;
+    g.src[size_t(sl->rank)] = buf;
+    g.cnt[size_t(sl->rank)] = count;
+    if (!g.barrier()) return 2;
+    for (int r = 0; r < g.n; ++r)
+        if (g.cnt[size_t(r)] != count) {
+            g.barrier();
+            return 3;  // mismatched collective: every rank sees it
+        }
+    std::vector<double> acc(count, 0.0);
+    for (int r = 0; r < g.n; ++r) {  // rank order on every rank: identical bits
+        const double* x = g.src[size_t(r)];
+        for (size_t i = 0; i < count; ++i) acc[i] += x[i];
+    }
+    if (!g.barrier()) return 2;  // everyone has read every buffer
+    std::memcpy(buf, acc.data(), sizeof(double) * count);
+    return 0;
+}
+
+int lg_allgather(void* user, const double* send, double* recv, size_t count) {
+    auto* sl = static_cast<LocalGroup::Slot*>(user);
+    LocalGroup& g = *sl->g;
+    g.src[size_t(sl->rank)] = send;
+    g.cnt[size_t(sl->rank)] = count;
+    if (!g.barrier()) return 2;
+    for (int r = 0; r < g.n; ++r)
+        if (g.cnt[size_t(r)] != count) {
+            g.barrier();
+            return 3;
+        }
+    for (int r = 0; r < g.n; ++r) std::memcpy(recv + size_t(r) * count, g.src[size_t(r)], sizeof(double) * count);
+    return g.barrier() ? 0 : 2;
+}
+
+void lg_acquire(void* user) { static_cast<LocalGroup::Slot*>(user)->g->gpu.lock(); }
+void lg_release(void* user) { static_cast<LocalGroup::Slot*>(user)->g->gpu.unlock(); }
+
+}  // namespace
+
+LocalGroup* local_group_create(int nranks, double timeout_s) {
+    if (nranks < 1) raise(RLRA_EINVAL, fmt("local group of %d ranks", nranks));
+    auto* g = new LocalGroup();
+    g->n = nranks;
+    g->timeout_s = timeout_s > 0.0 ? timeout_s : env_timeout();
+    g->src.assign(size_t(nranks), nullptr);
+    g->cnt.assign(size_t(nranks), 0);
+    for (int r = 0; r < nranks; ++r) g->slots.push_back({g, r});
+    return g;
+}
+
+void local_group_destroy(LocalGroup* g) { delete g; }
+
+HostCollectives local_group_collectives(LocalGroup* g, int rank) {
+    if (!g || rank < 0 || rank >= g->n) raise(RLRA_EINVAL, "local group: bad rank");
+    HostCollectives hc;
+    hc.allreduce_sum = lg_allreduce;
+    hc.allgather = lg_allgather;
+    hc.gpu_acquire = lg_acquire;
+    hc.gpu_release = lg_release;
+    hc.user = &g->slots[size_t(rank)];
+    return hc;
 }
 
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
@@ -546,7 +841,7 @@ void sketch_left_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0,
         RLRA_CUDA(cudaMemcpy2DAsync(Om.m.p, sizeof(double) * Om.m.ld, h.data() + row0, sizeof(double) * m_total,
                                     sizeof(double) * mg, l, cudaMemcpyHostToDevice, ctx.stream));
         gemm(ctx, Op::T, Op::N, 1.0, A, Om.m, 0.0, Yt);
-        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        comm_sync(ctx, cm);
     }
     allreduce(ctx, cm, Yt.p, size_t(n) * l);
 }
@@ -577,7 +872,7 @@ IdOut id_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, in
         Buf sq(ctx, sizeof(double));
         sum_squares(ctx, S1.m.block(k, k, l - k, n - k), sq.d());  // interp.hpp:213
         RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        comm_sync(ctx, cm);
         out.qr_residual = std::sqrt(ctx.h_scalars[0]);
     }
     DMatBuf T(ctx, k, std::max(1, n - k));
@@ -602,7 +897,7 @@ double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, 
     allreduce(ctx, cm, R.p, size_t(k) * n);
     std::vector<int> jr_host(k);
     RLRA_CUDA(cudaMemcpyAsync(jr_host.data(), jr, sizeof(int) * k, cudaMemcpyDeviceToHost, ctx.stream));
-    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    comm_sync(ctx, cm);
     cur_linkage(ctx, R, V, k, U, jr_host.data());  // replicated
     // ||A - C U R||_F: local fused residual, scalar allreduce
     double loc = 0.0;
@@ -617,7 +912,7 @@ double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, 
         o.resid_sq = sq.d();
         gemm(ctx, Op::N, Op::N, mg, n, k, 1.0, Cg.p, Cg.ld, UR.m.p, UR.m.ld, 0.0, nullptr, 0, o);
         RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        comm_sync(ctx, cm);
         loc = ctx.h_scalars[0];
     }
     return std::sqrt(allreduce_scalar(ctx, cm, loc));
@@ -634,7 +929,7 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
     auto global_fro = [&](double local_sq) { return std::sqrt(allreduce_scalar(ctx, cm, local_sq)); };
     sum_squares(ctx, W, sq.d());
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    comm_sync(ctx, cm);
     double resid = global_fro(ctx.h_scalars[0]);
     DMatBuf Z(ctx, n, blk), P(ctx, std::max(1, int(Q.cols)), blk);
     for (int i = 1; i <= num_blocks; ++i) {  // qb.hpp:116-142
@@ -680,7 +975,7 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
         gemm(ctx, Op::N, Op::N, mg, n, width, 1.0, Qi.p, Qi.ld, Bi.p, Bi.ld, 0.0, W.p, W.ld, o);
         out.ell += width;
         RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-        RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        comm_sync(ctx, cm);
         resid = global_fro(ctx.h_scalars[0]);
         out.hist.push_back(resid);
         if (tol > 0.0 && resid < tol) {
@@ -805,7 +1100,7 @@ double qb_hierarchical_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t
     o.resid_sq = sq.d();
     gemm(ctx, Op::N, Op::N, mg, n, rank, 1.0, Q.p, Q.ld, B.p, B.ld, 0.0, nullptr, 0, o);
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_scalars, sq.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    comm_sync(ctx, cm);
     return std::sqrt(allreduce_scalar(ctx, cm, ctx.h_scalars[0]));
 }
 

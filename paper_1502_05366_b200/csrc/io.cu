@@ -17,6 +17,7 @@
 #include "engine.cuh"
 #include "gemm.cuh"
 #include "io.cuh"
+#include "dist.cuh"
 #include "qr.cuh"
 #include "reduce.cuh"
 
@@ -301,6 +302,39 @@ void gen_test_matrix(Context& ctx, const std::vector<double>& sigma, uint64_t se
         DMatBuf G(ctx, m, n);
         philox_fill(ctx, G.m, seed, 103, 0);
         axpy_mat_kernel<<<grid_for(ctx, int64_t(m) * n), 256, 0, ctx.stream>>>(A.p, A.ld, G.m.p, G.m.ld, m, n, noise);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+    }
+}
+
+void gen_test_matrix_rowsharded(Context& ctx, Comm& cm, const std::vector<double>& sigma, uint64_t seed,
+                                double noise, int64_t row0, int64_t m_total, const DMat& A) {
+    const int mg = int(A.rows), n = int(A.cols), r = int(sigma.size());
+    if (r > std::min<int64_t>(m_total, n))
+        raise(RLRA_EDIM, fmt("gen_test_matrix: %d singular values for a %lldx%d matrix", r, (long long)m_total, n));
+    if (r == 0) {
+        zero_mat(ctx, A);
+    } else {
+        DMatBuf U(ctx, std::max(mg, 1), r), V(ctx, n, r);
+        const DMat Ug = U.m.block(0, 0, mg, r);
+        Buf s(ctx, sizeof(double) * r);
+        if (mg > 0) philox_fill(ctx, Ug, seed, 101, row0);
+        philox_fill(ctx, V.m, seed, 102, 0);
+        orth_rowsharded(ctx, cm, Ug, m_total, false);
+        orth_inplace(ctx, V.m, nullptr);
+        if (mg > 0) {
+            RLRA_CUDA(cudaMemcpyAsync(s.p, sigma.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx.stream));
+            scale_cols_by_kernel<<<grid_for(ctx, int64_t(mg) * r), 256, 0, ctx.stream>>>(Ug.p, Ug.ld, mg, r, s.d());
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+            gemm(ctx, Op::N, Op::T, 1.0, Ug, V.m, 0.0, A);
+        }
+        comm_sync(ctx, cm);  // sigma (host) outlives its copy
+    }
+    if (noise != 0.0 && mg > 0) {
+        DMatBuf G(ctx, mg, n);
+        philox_fill(ctx, G.m, seed, 103, row0);
+        axpy_mat_kernel<<<grid_for(ctx, int64_t(mg) * n), 256, 0, ctx.stream>>>(A.p, A.ld, G.m.p, G.m.ld, mg, n, noise);
         RLRA_LAUNCH_CHECK();
         ++ctx.launches;
     }

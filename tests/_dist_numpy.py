@@ -39,6 +39,7 @@ def omega_rows(seed, draw, row0, rows, l):
 class NumpyBackend:
     def __init__(self):
         self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.allreduces = 0
 
     def new(self, rows, cols):
@@ -97,6 +98,15 @@ class NumpyBackend:
             self.allreduces += 1
             return NM(t.numpy())
         return X
+
+    def allgather(self, X):
+        """list of every rank's X (same shape on every rank)"""
+        if self.world <= 1:
+            return [np.array(X.a)]
+        t = torch.from_numpy(np.ascontiguousarray(X.a))
+        outs = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(outs, t)
+        return [o.numpy() for o in outs]
 
     def allreduce_scalar(self, x):
         if self.world <= 1:

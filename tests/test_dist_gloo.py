@@ -1,4 +1,4 @@
-"""The row-sharded multi-GPU orchestration (paper_1502_05366_b200/dist.py) at
+"""The row-sharded multi-GPU orchestration (tests/_dist_mirror.py, the Python restatement of csrc/dist.cu) at
 world size 2 over gloo on CPU, with the numpy stand-in backend: the sharded
 run must reproduce the single-process run of the same algorithm (identical
 Omega, different association order of the sums) and the true spectrum."""
@@ -40,7 +40,7 @@ def _worker(rank, world, port, m, n, k, p, q, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from _dist_numpy import NM, NumpyBackend, OmegaSeed
 
-    from paper_1502_05366_b200 import dist as D
+    import _dist_mirror as D
 
     a = _matrix(m, n)
     bounds = np.linspace(0, m, world + 1).astype(int)
@@ -219,3 +219,47 @@ def test_rowsharded_hierarchical_qb_matches_single_process(tmp_path, world, nrb)
     slabs = [a[t * base:(t + 1) * base] if t < nrb - 1 else a[t * base:] for t in range(nrb)]
     Qs, Bs = qb_hierarchical_np(slabs, 4, 2, 1, seed=3)
     assert np.max(np.abs(Q - Qs)) <= 1e-12 and np.max(np.abs(parts[0]["B"] - Bs)) <= 1e-12
+
+
+def _tsqr_worker(rank, world, port, bounds, out_dir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import _dist_mirror as D
+    from _dist_numpy import NM, NumpyBackend
+
+    rs = np.random.default_rng(11)
+    m, n, r = bounds[-1], 24, 9
+    y = rs.standard_normal((m, r)) @ rs.standard_normal((r, n))  # exact rank 9 < 24 columns
+    y[:, 5] = 0.0  # and an exactly zero column
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    Q = D.orth_dist(NumpyBackend(), NM(y[r0:r1]))
+    np.savez(os.path.join(out_dir, f"t{rank}.npz"), Q=Q.a, y=y)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("bounds", [[0, 70, 140], [0, 10, 80, 150], [0, 40, 41, 90, 120]])
+def test_rowsharded_orth_rank_deficient_falls_back_to_tsqr(tmp_path, bounds):
+    """dist.cu's distributed orth on an exactly rank-deficient sketch (rank 9 of
+    24 columns plus a zero column; csrc/dist.cu tsqr_rowsharded, mirrored):
+    CholQR2 and shifted CholQR3 break down, TSQR (local QR, allgathered R
+    factors, replicated QR of the compacted stack) still returns an
+    orthonormal Q whose span contains the input's, including ranks that hold
+    fewer rows than columns (the row-sharded path used to raise
+    where the single-GPU and reference orth succeed)."""
+    world = len(bounds) - 1
+    port = _free_port()
+    mp.spawn(_tsqr_worker, args=(world, port, bounds, str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(os.path.join(tmp_path, f"t{r}.npz")) for r in range(world)]
+    Q = np.vstack([x["Q"] for x in parts])
+    y = parts[0]["y"]
+    assert Q.shape == y.shape
+    assert np.linalg.norm(Q.T @ Q - np.eye(y.shape[1])) <= 1e-13
+    assert np.linalg.norm(y - Q @ (Q.T @ y)) <= 1e-13 * np.linalg.norm(y)

@@ -1,6 +1,7 @@
 """The row-sharded path on the GPU engine with a real NCCL process group
 (world size 1 on the single-GPU test box: the collectives run, the sums are
-trivially complete).  Multi-rank logic is covered by tests/test_dist_gloo.py."""
+trivially complete).  World sizes 2-4 of the same C++ drivers run in
+tests/test_gpu_dist_ranks.py (ranks on one GPU, host-staged collectives)."""
 import os
 import socket
 
@@ -10,43 +11,6 @@ import pytest
 import paper_1502_05366_b200 as R
 
 pytestmark = pytest.mark.gpu
-
-
-def test_rowsharded_rsvd_nccl_world1_matches_engine():
-    import torch
-    import torch.distributed as dist
-
-    from paper_1502_05366_b200 import dist as D
-    from paper_1502_05366_b200.testmat import gen_test_matrix_device
-
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    try:
-        eng = R.Engine(0)
-        torch.cuda.set_device(0)
-        m, n, k, p, q = 6000, 3000, 100, 10, 2
-        A, st = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(1500) / 30.0), seed=9)
-        be = D.GpuBackend(eng)
-        assert be.comm
-        U, sg, V = D.rsvd_v2_rowsharded(be, D.DM(A, m, n), m, k, p, q, 1, R.Omega.philox(4242))
-        Ue = torch.empty(m * k, dtype=torch.float64, device="cuda")
-        Ve = torch.empty(n * k, dtype=torch.float64, device="cuda")
-        Se = torch.empty(k, dtype=torch.float64, device="cuda")
-        eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, 1, R.Omega.philox(4242),
-                        Ue.data_ptr(), Se.data_ptr(), Ve.data_ptr())
-        s_d = sg.t[:k].cpu().numpy()
-        s_e = Se.cpu().numpy()
-        assert np.max(np.abs(s_d - s_e) / s_e) <= 1e-10
-        stn = st.cpu().numpy()
-        assert np.max(np.abs(s_d[:20] - stn[:20]) / stn[:20]) <= 1e-10
-        rel = eng.device_rel_error(A.data_ptr(), m, n, U.ptr, sg.ptr, V.ptr, k)
-        rel_e = eng.device_rel_error(A.data_ptr(), m, n, Ue.data_ptr(), Se.data_ptr(), Ve.data_ptr(), k)
-        assert rel <= 1.01 * rel_e
-    finally:
-        dist.destroy_process_group()
 
 
 def test_native_rowsharded_rsvd_world1_matches_engine():

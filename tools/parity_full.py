@@ -1,14 +1,23 @@
 """Full-size parity of the GPU engine against the UNMODIFIED reference
 (oracle/_ref/librlra_ref_fast.so, all host threads) with the reference's own
 Omega injected (parity mode: the RngState stream, seed 12345), for
-  C1  rsvd_v2 (m=2000, n=4000, k=200, p=10, q=2)           sigma, residual
+  C1  rsvd_v2 (m=2000, n=4000, k=200, p=10, q=2)               sigma, residual
   C3  id_rand + cur_rand (m=20000, n=10000, k=600, p=10, q=2)  pivots, residuals
+  C5  rsvd_v2 (m=200000, n=20000, k=500, p=10, q=2)            sigma, residual
+  C4  rsvd_v2 (m=n=50000, k=1000, p=20, q=4; 1e-3 G noise)     sigma, residual
+      (C4:<m> runs the C4 recipe at m=n=<m> when the full size does not fit)
+  C2  qb_blocked (m=n=8000, b=100, tol=1e-6, q=1, reorth=1)    ell, history, B;
+      svd_from_qb sigma against a LAPACK SVD (numpy) of the reference's B
+      (the reference's serial Jacobi at ell ~ 6100 takes hours)
 The test matrices are built on the GPU (paper_1502_05366_b200.testmat) and
-copied to the host; both sides factor the same bytes.  Prints one JSON line
-per config.  TEST INFRASTRUCTURE: the reference is only the checker here.
-Usage: python tools/parity_full.py [C1] [C3]"""
+copied to the host; both sides factor the same bytes.  Residuals of both
+factorizations are evaluated by the same device routine (fused residual GEMM)
+against the device copy of A.  Prints one JSON line per config.
+TEST INFRASTRUCTURE: the reference is only the checker here.
+Usage: python tools/parity_full.py [C1] [C3] [C5] [C4[:m]] [C2]"""
 import json
 import os
+import platform
 import sys
 import time
 
@@ -27,10 +36,45 @@ cores = os.cpu_count() or 1
 ref.lib.ref_set_threads(cores)
 
 
-def host_matrix(m, n, sigma, seed, noise=0.0):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor()
+
+
+def host_matrix(m, n, sigma, seed, noise=0.0, keep_device=False):
     A, st = gen_test_matrix_device(eng, m, n, sigma, seed=seed, noise=noise)
-    a = np.asfortranarray(A.view(n, m).t().cpu().numpy())
-    return a, st.cpu().numpy()
+    import torch
+    a = np.empty((m, n), order="F")
+    torch.from_numpy(a.T.reshape(-1)).copy_(A)  # column-major bytes straight into the F-ordered array
+    return (a, st.cpu().numpy(), A) if keep_device else (a, st.cpu().numpy())
+
+
+def sigma_report(s, s_ref):
+    """north_star: rel 1e-10 per mode; modes at the FP64 floor
+    (u*s1/s_i > 1e-11) get the absolute bound 1e-13*s1 instead."""
+    s, s_ref = np.asarray(s), np.asarray(s_ref)
+    rel = np.abs(s - s_ref) / s_ref
+    floor = 2.2e-16 * s_ref[0] / s_ref > 1e-11
+    ok = bool(np.all((rel <= 1e-10) | (floor & (np.abs(s - s_ref) <= 1e-13 * s_ref[0]))))
+    return dict(sigma_ok=ok, sigma_max_rel_diff=float(rel.max()),
+                sigma_max_rel_diff_above_floor=float(rel[~floor].max()) if np.any(~floor) else 0.0,
+                sigma_modes_at_floor=int(floor.sum()))
+
+
+def dev_resid(Ad, m, n, u, s, v):
+    """||A - U S V^T||_F / ||A||_F on the device (the same routine for both sides)."""
+    import torch
+    dev = f"cuda:{eng.device}"
+    U = torch.from_numpy(np.ascontiguousarray(u.T)).to(dev)  # column-major m x k
+    S = torch.from_numpy(np.ascontiguousarray(s)).to(dev)
+    V = torch.from_numpy(np.ascontiguousarray(v.T)).to(dev)
+    torch.cuda.synchronize()
+    return eng.device_rel_error(Ad.data_ptr(), m, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), len(s))
 
 
 def c1():
@@ -83,6 +127,86 @@ def c3():
     return out
 
 
+def rsvd_big(name, m, n, k, p, q, sigma, seed, noise=0.0):
+    """rsvd_v2 at full size: GPU (host API, parity-mode Omega) vs the reference."""
+    a, st, Ad = host_matrix(m, n, sigma, seed=seed, noise=noise, keep_device=True)
+    t0 = time.perf_counter()
+    u, s, v = eng.rsvd_v2(a, k, p, q, 1, rng=R.Rng(12345))
+    tg = time.perf_counter() - t0
+    eg = dev_resid(Ad, m, n, u, s, v)
+    del u, v
+    print(f"# {name}: GPU done in {tg:.2f} s, reference starting ({cores} threads)", file=sys.stderr, flush=True)
+    t0 = time.perf_counter()
+    uo, so, vo = ref.rsvd(a, k, p, q, 1, ref.rng(12345), 0)
+    tr = time.perf_counter() - t0
+    eo = dev_resid(Ad, m, n, uo, so, vo)
+    out = dict(config=name, m=m, n=n, k=k, p=p, q=q, noise=noise)
+    out.update(sigma_report(s, so))
+    out.update(rel_fro_error=eg, rel_fro_error_ref=eo, residual_ratio=float(eg / eo),
+               residual_ok=bool(eg <= 1.01 * eo),
+               sigma_vs_true_top100_max_rel=float(np.max(np.abs(s[:100] - st[:100]) / st[:100])),
+               gpu_wall_s_host_api=tg, ref_wall_s=tr, ref_threads=cores, cpu=cpu_model(),
+               ref_effective_gflops=4.0 * m * n * (k + p) * (q + 1) / tr / 1e9)
+    return out
+
+
+def c5():
+    return rsvd_big("C5", 200000, 20000, 500, 10, 2, np.exp(-np.arange(3685) / 100.0), seed=5)
+
+
+def c4(size=50000):
+    r = min(4000, size)
+    return rsvd_big("C4" if size == 50000 else f"C4@{size}", size, size, 1000, 20, 4,
+                    1.0 / np.sqrt(np.arange(r) + 1.0), seed=4, noise=1e-3)
+
+
+def c2():
+    m = n = 8000
+    b, tol, q = 100, 1e-6, 1
+    M = -(-min(m, n) // b)
+    a, st, Ad = host_matrix(m, n, (np.arange(min(m, n)) + 1.0) ** -2, seed=2, keep_device=True)
+    t0 = time.perf_counter()
+    f = eng.qb_blocked(a, b, M, tol, q, 1, rng=R.Rng(12345))
+    tqb = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    u, s, v = eng.svd_from_qb(f, 0)
+    tsv = time.perf_counter() - t0
+    eg = dev_resid(Ad, m, n, u, s, v)
+    del u, v
+    print(f"# C2: GPU qb {tqb:.2f} s + svd {tsv:.2f} s, ell={f['ell']}; reference qb starting", file=sys.stderr,
+          flush=True)
+    t0 = time.perf_counter()
+    fo = ref.qb_blocked(a, b, M, tol, q, 1, ref.rng(12345))
+    tr = time.perf_counter() - t0
+    out = dict(config="C2", m=m, n=n, b=b, tol=tol, q=q, ell=f["ell"], ell_ref=fo["ell"],
+               ell_ok=f["ell"] == fo["ell"], reached=f["tolerance_reached"], reached_ref=fo["reached"])
+    hg, ho = np.asarray(f["history"]), np.asarray(fo["history"])
+    nh = min(len(hg), len(ho))
+    out.update(history_len=len(hg), history_len_ref=len(ho),
+               history_max_rel_diff=float(np.max(np.abs(hg[:nh] - ho[:nh]) / ho[:nh])),
+               final_residual=float(hg[-1]), final_residual_ref=float(ho[-1]))
+    # B: the same Omega gives the same blocks up to rounding
+    ell = min(f["ell"], fo["ell"])
+    out["B_max_abs_diff_rel_to_normA"] = float(np.max(np.abs(f["b"][:ell] - fo["b"][:ell])) /
+                                              np.linalg.norm(st))
+    # svd_from_qb sigma vs LAPACK SVD of the reference's B (= sigma(QB), Q orthonormal)
+    t0 = time.perf_counter()
+    s_lapack = np.linalg.svd(fo["b"], compute_uv=False)
+    tl = time.perf_counter() - t0
+    out.update({("svd_" + k_): v_ for k_, v_ in sigma_report(s, s_lapack).items()})
+    # the GPU svd_from_qb on the REFERENCE's Q, B: isolates the Jacobi kernel
+    fo_d = dict(q=fo["q"], b=fo["b"], ell=fo["ell"])
+    _, s_on_ref, _ = eng.svd_from_qb(fo_d, 0)
+    out.update({("svd_on_refB_" + k_): v_ for k_, v_ in sigma_report(s_on_ref, s_lapack).items()})
+    out.update(rel_fro_error=eg, gpu_qb_s_host_api=tqb, gpu_svd_from_qb_s_host_api=tsv, ref_qb_wall_s=tr,
+               lapack_svd_s=tl, ref_threads=cores, cpu=cpu_model())
+    return out
+
+
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["C1", "C3"]:
-        print(json.dumps({"C1": c1, "C3": c3}[nm]()), flush=True)
+        if nm.startswith("C4:"):
+            res = c4(int(nm.split(":")[1]))
+        else:
+            res = {"C1": c1, "C3": c3, "C5": c5, "C4": c4, "C2": c2}[nm]()
+        print(json.dumps(res), flush=True)
