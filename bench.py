@@ -24,7 +24,8 @@ roofline: the dominant kernel is the FP64 DMMA GEMM; achieved = its
 A (32 GB) is far larger than L2 (126 MB), so no flush is needed between steps.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified headers) on a bounded sample of the same workload, all host cores.
+unmodified headers) on a proportional 1/5 sample of the same workload (m, n
+and k + p scaled, see CPU_SCALE), all host cores, --warmup/--steps honoured.
 """
 from __future__ import annotations
 
@@ -132,8 +133,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# The CPU legs time a PROPORTIONAL sample of C5: m, n and l = k + p scaled by
+# 1/5 (p = 10, q = 2 kept), so every phase keeps its share of the work (the
+# threaded GEMMs ~ m n l, the reference's serial Householder orths ~ (m + n)
+# l^2) and one reference rsvd takes ~8 s on the box's 16 threads.  A
+# full-width slab (m' x 20000, k = 500) cannot fit the driver's budget: its
+# n-side serial orths and QR of B^T alone take ~40 s per step.  Measured on the
+# box (tools/ref_sample_timing.py, profiles/r02_ref_sample_timing.jsonl): 23.5-
+# 24.9 GFLOP/s at scales 1/4, 1/5 and 1/8 against 21.5 GFLOP/s for the one-off
+# full C5 reference run (1139 s, profiles/r02_parity_full.jsonl), so the sample
+# rate is within ~13 % of the full-size rate (slightly flattering the CPU).
+CPU_SCALE = 5
+CPU_SAMPLE = dict(m=C5["m"] // CPU_SCALE, n=C5["n"] // CPU_SCALE, k=(C5["k"] + C5["p"]) // CPU_SCALE - C5["p"],
+                  p=C5["p"], q=C5["q"], s=C5["s"])
+FULL_C5_REFERENCE_S = 1138.98  # profiles/r02_parity_full.jsonl: unmodified reference, 16 threads, same A
+
+
 def cpu_reference_step(a_sample, cores):
-    """One rsvd_v2 on the reference CPU build; returns seconds."""
+    """One rsvd_v2 on the reference CPU build (all `cores` threads); seconds."""
     import ctypes as C
 
     import numpy as np
@@ -144,7 +161,7 @@ def cpu_reference_step(a_sample, cores):
     lib = C.CDLL(_oracle.REF_FAST_PATH)
     lib.ref_set_threads(cores)
     m, n = a_sample.shape
-    k, p, q, s = C5["k"], C5["p"], C5["q"], C5["s"]
+    k, p, q, s = CPU_SAMPLE["k"], CPU_SAMPLE["p"], CPU_SAMPLE["q"], CPU_SAMPLE["s"]
     r = _oracle.Rng()
     lib.ref_rng_seed(C.byref(r), C.c_uint64(SEED_OMEGA))
     u = np.zeros((m, k), order="F")
@@ -160,29 +177,35 @@ def cpu_reference_step(a_sample, cores):
 
 
 def cpu_port_step(a_sample):
-    import numpy as np
-
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import _oracle
 
     o = _oracle.orc()
     t0 = time.perf_counter()
-    o.rsvd(a_sample, C5["k"], C5["p"], C5["q"], C5["s"], o.rng(SEED_OMEGA), 0)
+    o.rsvd(a_sample, CPU_SAMPLE["k"], CPU_SAMPLE["p"], CPU_SAMPLE["q"], CPU_SAMPLE["s"], o.rng(SEED_OMEGA), 0)
     return time.perf_counter() - t0
 
 
 def cpu_sample_matrix():
-    """The bounded CPU sample: the leading 600 x 4000 block of a C5-type
-    matrix (same spectrum law, seeded; generated with numpy)."""
+    """The proportional CPU sample of C5: a (m/5) x (n/5) matrix U diag(s) V^T
+    with the C5 law in the scaled index (s_j = exp(-5 j / 100), 737 modes),
+    U, V orthonormalised seeded Gaussians (numpy)."""
     import numpy as np
 
     m, n = CPU_SAMPLE["m"], CPU_SAMPLE["n"]
     rs = np.random.default_rng(SEED_GEN)
-    r = min(m, n)
+    r = 3685 // CPU_SCALE
     U, _ = np.linalg.qr(rs.standard_normal((m, r)))
     V, _ = np.linalg.qr(rs.standard_normal((n, r)))
-    s = np.exp(-np.arange(r) / 100.0)
+    s = np.exp(-CPU_SCALE * np.arange(r) / 100.0)
     return np.asfortranarray((U * s) @ V.T)
+
+
+def cpu_sample_desc():
+    c = CPU_SAMPLE
+    return (f"rsvd_v2 on a proportional C5 sample: m, n, k+p scaled 1/{CPU_SCALE} "
+            f"({c['m']}x{c['n']}, k={c['k']}, p={c['p']}, q={c['q']}); the full C5 reference run took "
+            f"{FULL_C5_REFERENCE_S:.0f} s = {f_gemm(**C5) / FULL_C5_REFERENCE_S / 1e12:.4f} TFLOP/s on 16 threads")
 
 
 def run_reference(args):
@@ -195,26 +218,28 @@ def run_reference(args):
     a = cpu_sample_matrix()
     cores = os.cpu_count() or 1
     use_ref = os.path.exists(_oracle.REF_FAST_PATH)
-    fl = f_gemm(CPU_SAMPLE["m"], CPU_SAMPLE["n"], C5["k"], C5["p"], C5["q"])
-    times = []
-    for i in range(min(args.warmup, 1) + args.steps):
-        dt = cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
-        if i >= min(args.warmup, 1):
-            times.append(dt)
-    t = statistics.median(times)
+    fl = f_gemm(**CPU_SAMPLE)
+    for _ in range(args.warmup):
+        cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
+    total = 0.0
+    for _ in range(args.steps):
+        total += cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
+    t = total / args.steps
     val = fl / t / 1e12
+    c = CPU_SAMPLE
     line = {
         "impl": "reference",
         "metric": "rsvd_v2 effective FP64 TFLOP/s (F_gemm = 4mnl(q+1) / time), C5 workload",
         "value": val, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C5 rsvd_v2 (m=200000,n=20000,k=500,p=10,q=2); CPU sample = "
-                   "leading 600x4000 block, same k,p,q", "sample_m": CPU_SAMPLE["m"],
-                   "sample_n": CPU_SAMPLE["n"]},
+        "config": {"workload": f"C5 rsvd_v2 (m=200000,n=20000,k=500,p=10,q=2); CPU proportional sample "
+                               f"1/{CPU_SCALE}: m={c['m']} n={c['n']} k={c['k']} p={c['p']} q={c['q']}",
+                   "sample_m": c["m"], "sample_n": c["n"], "sample_k": c["k"],
+                   "full_c5_reference_s": FULL_C5_REFERENCE_S,
+                   "full_c5_reference_tflops": f_gemm(**C5) / FULL_C5_REFERENCE_S / 1e12},
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores if use_ref else 1,
-                         "kind": "reference" if use_ref else "port",
-                         "sample": "rsvd_v2 on the leading 600x4000 block of a C5-type matrix"},
+                         "kind": "reference" if use_ref else "port", "sample": cpu_sample_desc()},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -464,12 +489,9 @@ def main():
             cores = os.cpu_count() or 1
             use_ref = os.path.exists(_oracle.REF_FAST_PATH)
             dt = cpu_reference_step(a, cores) if use_ref else cpu_port_step(a)
-            fl = f_gemm(CPU_SAMPLE["m"], CPU_SAMPLE["n"], k, p, q)
             line["cpu_baseline"] = {
-                "value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cores if use_ref else 1,
-                "kind": "reference" if use_ref else "port",
-                "sample": f"rsvd_v2(k={k},p={p},q={q}) on the leading {CPU_SAMPLE['m']}x"
-                          f"{CPU_SAMPLE['n']} block of a C5-type matrix; {dt:.2f} s"}
+                "value": f_gemm(**CPU_SAMPLE) / dt / 1e12, "unit": "TFLOP/s", "cores": cores if use_ref else 1,
+                "kind": "reference" if use_ref else "port", "sample": cpu_sample_desc() + f"; this step {dt:.2f} s"}
         except Exception as e:  # reported, never silently substituted
             line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference",
                                     "sample": f"failed: {e}"}

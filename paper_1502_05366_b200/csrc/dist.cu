@@ -152,6 +152,21 @@ void allgather(Context& ctx, Comm& cm, const double* send, double* recv, size_t 
     RLRA_CUDA(cudaMemcpyAsync(recv, h + count, sizeof(double) * tot, cudaMemcpyHostToDevice, ctx.stream));
 }
 
+// in-place sum of a (possibly strided) device matrix view over the ranks:
+// the collectives move contiguous runs, so a view whose ld exceeds its rows
+// is reduced through a packed copy
+void allreduce_mat(Context& ctx, Comm& cm, const DMat& X) {
+    if (X.rows == 0 || X.cols == 0) return;
+    if (X.ld == X.rows || X.cols == 1) {
+        allreduce(ctx, cm, X.p, size_t(X.rows) * X.cols);
+        return;
+    }
+    DMatBuf T(ctx, X.rows, X.cols);
+    copy_mat(ctx, X, T.m);
+    allreduce(ctx, cm, T.m.p, size_t(X.rows) * X.cols);
+    copy_mat(ctx, T.m, X);
+}
+
 double allreduce_scalar(Context& ctx, Comm& cm, double x) {
     Buf b(ctx, sizeof(double));
     RLRA_CUDA(cudaMemcpyAsync(b.p, &x, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
@@ -175,7 +190,7 @@ void gram_allreduce(Context& ctx, Comm& cm, const DMat& Y, const DMat& G) {
     GemmOpts sy;
     sy.upper_tiles_only = true;
     gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G, sy);
-    allreduce(ctx, cm, G.p, size_t(G.rows) * G.cols);
+    allreduce_mat(ctx, cm, G);
 }
 
 // Y <- Y R^{-1} (R^{-1} upper triangular), through a scratch copy
@@ -492,7 +507,7 @@ void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, 
         for (int j = 1; j <= q; ++j) {                        // sketch.hpp:53-58
             if ((2 * j - 2) % s == 0) orth_rowsharded(ctx, cm, Y, m_total, true);
             gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z.m);    // Z_g = A_g^T Y_g
-            allreduce(ctx, cm, Z.m.p, size_t(n) * l);          // Z = sum_g
+            allreduce_mat(ctx, cm, Z.m);                       // Z = sum_g
             if ((2 * j - 1) % s == 0) orth_span_inplace(ctx, Z.m);  // replicated
             gemm(ctx, Op::N, Op::N, 1.0, A, Z.m, 0.0, Y);    // Y_g = A_g Z
         }
@@ -502,7 +517,7 @@ void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, 
     {
         GemmTag tag(ctx, "gemm_proj");
         gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Bt.m);       // rsvd.hpp:158
-        allreduce(ctx, cm, Bt.m.p, size_t(n) * l);
+        allreduce_mat(ctx, cm, Bt.m);
     }
     finish_qr_bt(ctx, Y, Bt.m, k, U, sigma, V);              // replicated QR + Jacobi, local lift
 }
@@ -843,7 +858,7 @@ void sketch_left_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0,
         gemm(ctx, Op::T, Op::N, 1.0, A, Om.m, 0.0, Yt);
         comm_sync(ctx, cm);
     }
-    allreduce(ctx, cm, Yt.p, size_t(n) * l);
+    allreduce_mat(ctx, cm, Yt);
 }
 
 }  // namespace
@@ -861,7 +876,7 @@ IdOut id_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, in
             gemm(ctx, Op::N, Op::N, 1.0, A, Yt.m, 0.0, Zm);                 // Z_g = A_g Yt (local)
             if ((2 * j - 1) % s == 0) orth_rowsharded(ctx, cm, Zm, m_total, true);
             gemm(ctx, Op::T, Op::N, 1.0, A, Zm, 0.0, Yt.m);                 // Yt = sum_g A_g^T Z_g
-            allreduce(ctx, cm, Yt.m.p, size_t(n) * l);
+            allreduce_mat(ctx, cm, Yt.m);
         }
     }
     transpose_mat(ctx, Yt.m, Y.m);
@@ -894,7 +909,7 @@ double cur_rand_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t row0, 
                                                                                     R.p, R.ld);
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
-    allreduce(ctx, cm, R.p, size_t(k) * n);
+    allreduce_mat(ctx, cm, R.block(0, 0, k, n));
     std::vector<int> jr_host(k);
     RLRA_CUDA(cudaMemcpyAsync(jr_host.data(), jr, sizeof(int) * k, cudaMemcpyDeviceToHost, ctx.stream));
     comm_sync(ctx, cm);
@@ -942,7 +957,7 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
         orth_rowsharded(ctx, cm, Qi, m_total, q_power > 0 || reorth);
         for (int j = 0; j < q_power; ++j) {
             gemm(ctx, Op::T, Op::N, 1.0, W, Qi, 0.0, Zi);
-            allreduce(ctx, cm, Zi.p, size_t(n) * width);
+            allreduce_mat(ctx, cm, Zi);
             orth_span_inplace(ctx, Zi);  // replicated
             gemm(ctx, Op::N, Op::N, 1.0, W, Zi, 0.0, Qi);
             orth_rowsharded(ctx, cm, Qi, m_total, j + 1 < q_power || reorth);
@@ -952,20 +967,14 @@ QbOut qb_blocked_rowsharded(Context& ctx, Comm& cm, const DMat& W, int64_t m_tot
                 const DMat Qp = Q.block(0, 0, mg, out.ell);
                 const DMat Pi = P.m.block(0, 0, out.ell, width);
                 gemm(ctx, Op::T, Op::N, 1.0, Qp, Qi, 0.0, Pi);
-                allreduce(ctx, cm, Pi.p, size_t(out.ell) * width);  // Q^T Q_i, l x b
+                allreduce_mat(ctx, cm, Pi);  // Q^T Q_i, l x b (a strided view of P)
                 gemm(ctx, Op::N, Op::N, -1.0, Qp, Pi, 1.0, Qi);
             }
             orth_rowsharded(ctx, cm, Qi, m_total, false);
         }
         const DMat Bi = B.block(out.ell, 0, width, n);
         gemm(ctx, Op::T, Op::N, 1.0, Qi, W, 0.0, Bi);  // B_i = sum_g Q_i,g^T W_g
-        {
-            // B_i lives inside B (ld = cap): reduce through a contiguous copy
-            DMatBuf Bc(ctx, width, n);
-            copy_mat(ctx, Bi, Bc.m);
-            allreduce(ctx, cm, Bc.m.p, size_t(width) * n);
-            copy_mat(ctx, Bc.m, Bi);
-        }
+        allreduce_mat(ctx, cm, Bi);  // B_i lives inside B (ld = cap)
         // W_g <- W_g - Q_i,g B_i and ||W_g||^2 in one pass, then the sum over ranks
         GemmOpts o;
         o.epi = EPI_RESID;

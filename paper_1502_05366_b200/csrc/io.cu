@@ -419,6 +419,7 @@ QbOut qb_single(Context& ctx, const DMat& A, double tol, int max_rank, OmegaSour
         sc(ctx, sizeof(double) * 2);
     std::vector<double> h(n);
     QbOut out;
+    out.reached = false;  // set when the residual drops below tol (qb.hpp:58-61)
     double resid = 0.0;
     {
         Buf s2(ctx, sizeof(double));

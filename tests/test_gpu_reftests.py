@@ -39,7 +39,9 @@ def test_reference_unit_suite_passes_on_the_engine():
     failed = re.findall(r"^\[  FAILED  \] (\S+)$", out, re.M)
     print(f"reference unit suite on the B200 engine: {ran} ran, {ran - len(set(failed))} passed")
     assert ran >= 150, ran  # 162 TEST() bodies in proj/tests
-    assert p.returncode == 0 and not failed, "\n".join(sorted(set(failed))) + "\n" + out[-6000:]
+    blocks = re.split(r"^(?=\[ RUN      \] )", out, flags=re.M)
+    detail = "\n".join(b for b in blocks if "[  FAILED  ]" in b.split("\n", 1)[-1])
+    assert p.returncode == 0 and not failed, "\n".join(sorted(set(failed))) + "\n" + detail[-8000:]
 
 
 def test_reference_acceptance_gate_tally():
