@@ -855,6 +855,7 @@ rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, 
         DMat W;
         if (loc == RLRA_DEVICE && inplace) {
             need(a, "a");
+            check_ld(lda, m_local, "a");  // the EPI_RESID GEMM writes W in place through lda
             W.p = a;
             W.rows = m_local;
             W.cols = n;
@@ -1034,7 +1035,9 @@ rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int
         DMatBuf Wown;
         DMat W;
         if (loc == RLRA_DEVICE && inplace) {
+            if (m < 0 || n < 0) raise(RLRA_EDIM, fmt("a: negative dimensions %dx%d", m, n));
             need(a, "a");
+            check_ld(lda, m, "a");  // the EPI_RESID GEMM writes W in place through lda
             W.p = a;
             W.rows = m;
             W.cols = n;

@@ -625,6 +625,7 @@ __global__ void trailing_sq_kernel(const double* W, int64_t ldw, int m, int n, i
 // ---------------------------------------------------------- tri-solve ---
 // One warp per right-hand side: column-oriented back substitution in shared
 // memory.  t_i = b_i / s_ii, then b[0:i] -= t_i * S(0:i, i) (coalesced column).
+// B and T may alias (each warp reads its whole column before writing it).
 __global__ void trisolve_kernel(const double* S, int64_t lds, int k, const double* B, int64_t ldb,
                                 int nc, double* T, int64_t ldt) {
     extern __shared__ double xs[];
@@ -832,16 +833,26 @@ bool upper_tri_solve(Context& ctx, const DMat& S11, const DMat& S12, const DMat&
         dmin = std::min(dmin, hd[i]);
     }
     if (nc > 0) {
-        int wpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (160 * 1024) / (int64_t(k) * 8))));
-        const size_t smem = sizeof(double) * size_t(k) * wpb;
-        if (smem > 227 * 1024) raise(RLRA_EDIM, fmt("upper_tri_solve: k=%d too large", k));
-        RLRA_CUDA(cudaFuncSetAttribute(trisolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
-        const int blocks = std::max(1, std::min(ctx.num_sms * 2, ceil_div(nc, wpb)));
-        trisolve_kernel<<<blocks, wpb * 32, smem, ctx.stream>>>(S11.p, S11.ld, k, S12.p, S12.ld, nc,
-                                                                T.p, T.ld);
-        RLRA_LAUNCH_CHECK();
-        ++ctx.launches;
+        // Blocked back substitution on DMMA: for the diagonal blocks from the
+        // bottom up, T_I <- S_II^{-1} T_I (one warp per right-hand side, the
+        // block's column in shared memory), then the rank-kTriNB update
+        // T[0:i0, :] -= S[0:i0, I] T_I on the tensor-core GEMM.  Shared memory
+        // holds one kTriNB slice per warp, so k is unbounded; the
+        // contraction's k^2 (n - k) flops run on DMMA.
+        constexpr int kTriNB = 64, kWpb = 8;
+        copy_mat(ctx, S12, T);
+        const size_t smem = sizeof(double) * size_t(kTriNB) * kWpb;
+        const int blocks = std::max(1, std::min(ctx.num_sms * 4, ceil_div(nc, kWpb)));
+        for (int i0 = ((k - 1) / kTriNB) * kTriNB; i0 >= 0; i0 -= kTriNB) {  // block rows aligned at 0
+            const int nb = std::min(k, i0 + kTriNB) - i0;
+            trisolve_kernel<<<blocks, kWpb * 32, smem, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
+                                                                     T.p + i0, T.ld, nc, T.p + i0, T.ld);
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+            if (i0 > 0)
+                gemm(ctx, Op::N, Op::N, -1.0, S11.block(0, i0, i0, nb), T.block(i0, 0, nb, nc), 1.0,
+                     T.block(0, 0, i0, nc));
+        }
     }
     if (dmax / dmin > 1e12) {
         if (nc > 0) {

@@ -828,8 +828,10 @@ bool row_id_rowsharded(Context& ctx, Comm& cm, const DMat& Cg, int64_t row0, int
         RLRA_LAUNCH_CHECK();
         ctx.launches += 2;
     }
-    bool clamped = false;
-    if (mg > 0) clamped = upper_tri_solve(ctx, S11.m, X.m.block(0, 0, k, mg), T.m.block(0, 0, k, mg));
+    // every rank runs the solve (mg may be 0): its zero-diagonal check and the
+    // clamp decision depend only on the replicated S11, so an error is raised
+    // on all ranks together instead of stranding the others in a collective
+    const bool clamped = upper_tri_solve(ctx, S11.m, X.m.block(0, 0, k, mg), T.m.block(0, 0, k, mg));
     if (mg > 0) {
         dc_interp_kernel<<<dc_blocks(ctx, int64_t(mg) * k), 256, 0, ctx.stream>>>(pos.d(), T.m.p, k, mg, Wg.p,
                                                                                   Wg.ld);
