@@ -1195,7 +1195,8 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
 //      skip rule, branch-free fast form) then every thread updates its 2x2
 //      pair blocks of G (double-buffered) and J — two barriers per step;
 //   3. W_p J and V_p J streamed in 64-row chunks, 16 x 24 DMMA warp tiles.
-constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 64;
+constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 128;
+constexpr int kSPer = kSC2 * kSCR / 256;  // chunk elements per thread (in flight per load)
 constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16)
 constexpr int kSGP = kSC2 + 1;   // G / J pitch
 constexpr int kSJP = kSC2 + 4;   // J pitch for B fragments (== 4 mod 16)
@@ -1204,7 +1205,7 @@ constexpr size_t kSGramSmem =
 
 __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
     extern __shared__ double ssm[];
-    double* Cb = ssm;                          // chunk: 48 columns x 64 rows, pitch kSCP
+    double* Cb = ssm;                          // chunk: 48 columns x kSCR rows, pitch kSCP
     double* Pb = Cb + kSC2 * kSCP;             // 8 warps x 21 tiles x 64 partial Grams
     double* G0 = Pb + 8 * kSNT * 64;           // two 48 x 49 buffers
     double* J = G0 + 2 * kSC2 * kSGP;          // 48 x 49
@@ -1239,23 +1240,23 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 }
                 __syncthreads();
-                // each thread's 12 chunk elements: column e / 64, row e % 64
-                int ccol[12];
+                // each thread's kSPer chunk elements: column e / kSCR, row e % kSCR
+                int ccol[kSPer];
 #pragma unroll
-                for (int it = 0; it < 12; ++it) ccol[it] = gcol((t + 256 * it) >> 6);
-                double pre[12];
+                for (int it = 0; it < kSPer; ++it) ccol[it] = gcol((t + 256 * it) / kSCR);
+                double pre[kSPer];
                 auto load_chunk = [&](const double* X, int64_t ld, int rows, int k0) {
 #pragma unroll
-                    for (int it = 0; it < 12; ++it) {
-                        const int e = t + 256 * it, row = k0 + (e & 63);
+                    for (int it = 0; it < kSPer; ++it) {
+                        const int e = t + 256 * it, row = k0 + (e % kSCR);
                         pre[it] = (ccol[it] < n && row < rows) ? __ldcg(X + row + int64_t(ccol[it]) * ld) : 0.0;
                     }
                 };
                 auto store_chunk = [&]() {
 #pragma unroll
-                    for (int it = 0; it < 12; ++it) {
+                    for (int it = 0; it < kSPer; ++it) {
                         const int e = t + 256 * it;
-                        Cb[(e >> 6) * kSCP + (e & 63)] = pre[it];
+                        Cb[(e / kSCR) * kSCP + (e % kSCR)] = pre[it];
                     }
                 };
                 // ---- 1. Gram -------------------------------------------------
@@ -1270,7 +1271,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                         __syncthreads();
                         if (k0 + kSCR < m) load_chunk(a.W, a.ldw, m, k0 + kSCR);
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < kSCR / 32; ++h) {
                             const int kk = (warp + 8 * h) * 4;
                             double f[kSNB8];
 #pragma unroll
@@ -1363,7 +1364,8 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 if (rot) {
                     if (t == 0) flags[sweep % 3] = 1;
                     for (int e = t; e < kSC2 * kSC2; e += 256) Jb[(e / kSC2) * kSJP + e % kSC2] = J[(e / kSC2) * kSGP + e % kSC2];
-                    // ---- 3. W_p J, V_p J: warp (wr, wc) owns rows wr*16..+16, cols wc*24..+24 of a chunk
+                    // ---- 3. W_p J, V_p J: warp (wr, wc) owns rows wr*RF*8..+RF*8, cols wc*24..+24 of a chunk
+                    constexpr int RF = kSCR / 32;  // 8-row fragments per warp
                     const int wr = warp & 3, wc = warp >> 2;
                     int ocol[3][2];
 #pragma unroll
@@ -1381,26 +1383,26 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             __syncthreads();
                             // the next chunk's rows are disjoint from this chunk's outputs
                             if (k0 + kSCR < rows) load_chunk(X, ld, rows, k0 + kSCR);
-                            double o[2][3][2];
+                            double o[RF][3][2];
 #pragma unroll
-                            for (int f = 0; f < 2; ++f)
+                            for (int f = 0; f < RF; ++f)
 #pragma unroll
                                 for (int ct = 0; ct < 3; ++ct) o[f][ct][0] = o[f][ct][1] = 0.0;
 #pragma unroll
                             for (int kf = 0; kf < kSC2 / 4; ++kf) {
-                                double af[2], bf[3];
+                                double af[RF], bf[3];
 #pragma unroll
-                                for (int f = 0; f < 2; ++f) af[f] = Cb[(4 * kf + lc) * kSCP + wr * 16 + f * 8 + lr];
+                                for (int f = 0; f < RF; ++f) af[f] = Cb[(4 * kf + lc) * kSCP + wr * (RF * 8) + f * 8 + lr];
 #pragma unroll
                                 for (int ct = 0; ct < 3; ++ct) bf[ct] = Jb[(4 * kf + lc) * kSJP + wc * 24 + ct * 8 + lr];
 #pragma unroll
-                                for (int f = 0; f < 2; ++f)
+                                for (int f = 0; f < RF; ++f)
 #pragma unroll
                                     for (int ct = 0; ct < 3; ++ct) jac_dmma(o[f][ct][0], o[f][ct][1], af[f], bf[ct]);
                             }
 #pragma unroll
-                            for (int f = 0; f < 2; ++f) {
-                                const int row = k0 + wr * 16 + f * 8 + lr;
+                            for (int f = 0; f < RF; ++f) {
+                                const int row = k0 + wr * (RF * 8) + f * 8 + lr;
                                 if (row >= rows) continue;
 #pragma unroll
                                 for (int ct = 0; ct < 3; ++ct)
