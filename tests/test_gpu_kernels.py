@@ -246,7 +246,8 @@ def test_small_svd_shared_gram_jacobi_vs_oracle(eng, orc, m, n, kind):
 
 
 @pytest.mark.parametrize("env", [{"RLRA_BGRAM_NOHELP": "1"}, {"RLRA_SVD_KERNEL": "block"},
-                                 {"RLRA_BGRAM_BW": "16"}, {"RLRA_SVD_KERNEL": "gram"}])
+                                 {"RLRA_BGRAM_BW": "16"}, {"RLRA_SVD_KERNEL": "gram"},
+                                 {"RLRA_SVD_KERNEL": "sgram"}])
 def test_small_svd_variants_agree(eng, env):
     """The Jacobi variants selectable by environment (bgram without V
     helpers, 16-column blocks, the one-sided block kernel, the 32-column
