@@ -69,10 +69,15 @@ typedef struct rlra_ctx rlra_ctx;
  *      id_rand / cur_rand : one m x l draw             (interp.hpp:208)
  *      qb_blocked  : draw i = block i, n x width_i; the callback performs the
  *                    per-block rng.substream() itself  (qb.hpp:119-120)
- *  RLRA_OMEGA_PHILOX (performance mode): entries are generated inside the
- *    sketch GEMM from Philox4x32-10 keyed by `seed` (counter = row, column,
- *    draw); Omega never exists in HBM.  The caller's RNG is not consumed by
- *    the engine (the shim derives `seed` from one next_u64()).            */
+ *  RLRA_OMEGA_PHILOX (performance mode): entries are Philox4x32-10 normals
+ *    keyed by `seed` (counter = row, column, draw), identical on every GPU of
+ *    a row-sharded run.  By default Omega is generated once per call into an
+ *    n x l device buffer (82 MB at C5: 0.25% of A's bytes) that the streaming
+ *    GEMM reads; RLRA_SKETCH_FUSED=1 generates it in-register inside the
+ *    GEMM's producer warps instead (never in HBM, the same bits), which
+ *    measured slower at C5 (122.8 vs 115.7 ms: every cluster of M-tiles
+ *    regenerates its slice).  The caller's RNG is not
+ *    consumed by the engine (the shim derives `seed` from one next_u64()). */
 enum { RLRA_OMEGA_CALLBACK = 0, RLRA_OMEGA_PHILOX = 1 };
 typedef void (*rlra_omega_fill_fn)(void* user, int draw, int rows, int cols, double* host_out);
 typedef struct {

@@ -158,8 +158,11 @@ class Omega:
 
     ``Omega.from_rng(rng)``      parity mode: the reference's stream, drawn on
                                  the host from ``rng`` in the reference's order.
-    ``Omega.philox(seed)``       performance mode: generated in-register inside
-                                 the sketch GEMM, never materialised.
+    ``Omega.philox(seed)``       performance mode: Philox4x32-10 normals keyed
+                                 by (seed, row, column, draw), materialised once
+                                 per call (n x l) for the streaming GEMM, or
+                                 generated in-register inside it with
+                                 RLRA_SKETCH_FUSED=1 (same bits).
     """
 
     def __init__(self, mode, rng=None, seed=0, substream=False):

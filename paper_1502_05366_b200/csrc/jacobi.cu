@@ -441,6 +441,10 @@ struct GramJacArgs {
     unsigned* ver;         // bgram: block versions + J hand-off flags (zeroed; see the kernel)
     double* jbuf;          // bgram with helpers: 2 J slots per pair
     int helpers;           // bgram: V helper CTAs (grid = nb)
+    // sgram: exact skip of clean pairs (zeroed per call; see sgram_jacobi_kernel)
+    unsigned* mod;                 // [nb] stamp of the block's last modification
+    unsigned* clean;               // [nb * nb + nb / 2] stamp of the pair's last rotation-free visit
+    unsigned long long* counters;  // [0] visits, [1] skipped, [2] rotating
 };
 
 // ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
@@ -1195,7 +1199,7 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
 //      skip rule, branch-free fast form) then every thread updates its 2x2
 //      pair blocks of G (double-buffered) and J — two barriers per step;
 //   3. W_p J and V_p J streamed in 64-row chunks, 16 x 24 DMMA warp tiles.
-constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 128;
+constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 64;
 constexpr int kSPer = kSC2 * kSCR / 256;  // chunk elements per thread (in flight per load)
 constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16)
 constexpr int kSGP = kSC2 + 1;   // G / J pitch
@@ -1213,6 +1217,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
     double* rc = Jb + kSC2 * kSJP;             // per pair: c, s
     double* rs = rc + kSGB;
     __shared__ int rpq[kSGB];
+    __shared__ int s_skip;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
     const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
     volatile int* flags = a.flags;
@@ -1234,12 +1239,30 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     bJ = max(b1, b2);
                 }
                 auto gcol = [&](int c) { return c < kSGB ? bI * kSGB + c : bJ * kSGB + (c - kSGB); };
+                // Exact skip: a visit whose two blocks are unchanged since this
+                // pair's last rotation-free visit would recompute the same Gram
+                // bits and again rotate nothing (the reference's skip rule is a
+                // pure function of them), so it only publishes.  Stamps are
+                // round numbers + 1; block visits are ordered by the versions,
+                // so the stamps read after the acquire are current.
+                const int pid = intra ? nb * nb + g : bI * nb + bJ;
                 if (t == 0) {
                     jb_wait_at_least(a.ver + bI, R);
                     jb_wait_at_least(a.ver + bJ, R);
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    const unsigned c = __ldcg(a.clean + pid);
+                    s_skip = c != 0u && c >= __ldcg(a.mod + bI) && c >= __ldcg(a.mod + bJ);
+                    atomicAdd(a.counters + 0, 1ull);
+                    if (s_skip) atomicAdd(a.counters + 1, 1ull);
                 }
                 __syncthreads();
+                if (s_skip) {
+                    if (t == 0) {
+                        jb_publish(a.ver + bI, R + 1);
+                        jb_publish(a.ver + bJ, R + 1);
+                    }
+                    continue;
+                }
                 // each thread's kSPer chunk elements: column e / kSCR, row e % kSCR
                 int ccol[kSPer];
 #pragma unroll
@@ -1415,6 +1438,13 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 }
                 __syncthreads();
                 if (t == 0) {
+                    if (rot) {
+                        __stcg(a.mod + bI, R + 1u);
+                        __stcg(a.mod + bJ, R + 1u);
+                        atomicAdd(a.counters + 2, 1ull);
+                    } else {
+                        __stcg(a.clean + pid, R + 1u);
+                    }
                     __threadfence();
                     jb_publish(a.ver + bI, R + 1);
                     jb_publish(a.ver + bJ, R + 1);
@@ -1703,9 +1733,22 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         Buf verb(ctx, sizeof(unsigned) * g.nb);
         RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
         g.ver = static_cast<unsigned*>(verb.p);
+        const size_t nst = size_t(g.nb) + size_t(g.nb) * g.nb + g.nb / 2;
+        Buf stamps(ctx, sizeof(unsigned) * nst), cnt(ctx, sizeof(unsigned long long) * 4);
+        RLRA_CUDA(cudaMemsetAsync(stamps.p, 0, sizeof(unsigned) * nst, ctx.stream));
+        RLRA_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * 4, ctx.stream));
+        g.mod = static_cast<unsigned*>(stamps.p);
+        g.clean = g.mod + g.nb;
+        g.counters = static_cast<unsigned long long*>(cnt.p);
         void* args[] = {&g};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)sgram_jacobi_kernel, dim3(g.nb / 2), dim3(256), args, kSGramSmem,
                                               ctx.stream));
+        if (std::getenv("RLRA_JACOBI_STATS")) {
+            unsigned long long h[3];
+            RLRA_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+            RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+            std::fprintf(stderr, "sgram: %llu visits, %llu skipped (clean), %llu rotating\n", h[0], h[1], h[2]);
+        }
     } else if (forced != 4 && n > 2 * kGB) {
         // columns too long for shared memory: Gram block Jacobi (32-column blocks)
         static int gram_cap = 0;
