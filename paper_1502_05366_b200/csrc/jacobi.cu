@@ -1186,32 +1186,51 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
         for (int i = 0; i < 6; ++i) a.phase_clk[i] = ph[i];
 }
 
+__device__ __forceinline__ void sg_cp16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(jb_smem(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void sg_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void sg_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // ----------------------- streaming Gram block Jacobi, 48-column pairs -------
 // For l x l inputs too tall for shared memory (the C2 R-hat, 6100 x 6100):
 // blocks of 24 columns so the nb/2 = 128 pair CTAs cover most SMs (blocks of
 // 32 leave 52 idle), the cross/intra cyclic schedule of bgram_jacobi_kernel
 // (every column pair once per sweep), point-to-point block versions instead
-// of a grid barrier per round.  Per visit:
-//   1. G = W_p^T W_p streamed in 64-row chunks (register prefetch -> shared),
-//      each warp a k-slice of every chunk for all 21 upper 8x8 tiles, the 8
-//      partial Grams summed in a fixed order;
+// of a grid barrier per round.  W and V are the engine's own padded copies
+// (small_svd_tall): leading dimensions a multiple of kSCR rows, columns
+// padded to nb * kSGB, padding zero, so every chunk of a pair is 48 full
+// columns of kSCR doubles.  Per visit the chunks (64 rows x 48 columns) stream
+// through a kSNST-stage shared-memory ring filled by cp.async (16 bytes per
+// thread request, 6 per thread per chunk: 1-D bulk copies of 512 B measured
+// 1.65x slower), kSNST - 1 chunks in flight while the 8 warps work on one; the
+// sequence is: the Gram's chunks of W_p, then (speculatively, issued while
+// the Gram's tail and the rotation steps run) W_p's chunks again for W_p J,
+// then V_p's for V_p J (drained unused when nothing rotated).
+//   1. G = W_p^T W_p: each warp a k-slice of every chunk for all 21 upper 8x8
+//      tiles (registers), the 8 partial Grams summed in a fixed order;
 //   2. the visit's steps on G: the 24 pair rotations (reference formula and
 //      skip rule, branch-free fast form) then every thread updates its 2x2
 //      pair blocks of G (double-buffered) and J — two barriers per step;
-//   3. W_p J and V_p J streamed in 64-row chunks, 16 x 24 DMMA warp tiles.
-constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 64;
-constexpr int kSPer = kSC2 * kSCR / 256;  // chunk elements per thread (in flight per load)
-constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16)
+//   3. W_p J and V_p J on DMMA (16 x 24 warp tiles), written straight out.
+// A visit whose blocks are unchanged since the pair's last rotation-free
+// visit is skipped exactly (same Gram bits, again no rotation).
+constexpr int kSGB = 24, kSC2 = 48, kSNB8 = 6, kSNT = 21, kSCR = 64, kSNST = 4;
+constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16), 16-byte aligned rows
 constexpr int kSGP = kSC2 + 1;   // G / J pitch
 constexpr int kSJP = kSC2 + 4;   // J pitch for B fragments (== 4 mod 16)
-constexpr size_t kSGramSmem =
-    sizeof(double) * (size_t(kSC2) * kSCP + size_t(8) * kSNT * 64 + 3 * kSC2 * kSGP + kSC2 * kSJP + 2 * kSGB);
+constexpr int kSPT = 7;          // tiles per partial-Gram reduction round (3 rounds of 7)
+constexpr size_t kSGramSmem = sizeof(double) * (size_t(kSNST) * kSC2 * kSCP + size_t(8) * kSPT * 64 +
+                                                3 * kSC2 * kSGP + kSC2 * kSJP + 2 * kSGB);
 
 __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
-    extern __shared__ double ssm[];
-    double* Cb = ssm;                          // chunk: 48 columns x kSCR rows, pitch kSCP
-    double* Pb = Cb + kSC2 * kSCP;             // 8 warps x 21 tiles x 64 partial Grams
-    double* G0 = Pb + 8 * kSNT * 64;           // two 48 x 49 buffers
+    extern __shared__ __align__(16) double ssm[];
+    double* Ring = ssm;                        // kSNST stages: 48 columns x kSCR rows, pitch kSCP
+    double* Pb = Ring + kSNST * kSC2 * kSCP;   // 8 warps x kSPT tiles x 64 partial Grams
+    double* G0 = Pb + 8 * kSPT * 64;           // two 48 x 49 buffers
     double* J = G0 + 2 * kSC2 * kSGP;          // 48 x 49
     double* Jb = J + kSC2 * kSGP;              // 48 x 52
     double* rc = Jb + kSC2 * kSJP;             // per pair: c, s
@@ -1220,8 +1239,12 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
     __shared__ int s_skip;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
     const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
+    const int ncw = int(a.ldw / kSCR), ncv = int(a.ldv / kSCR);  // chunks of W / V columns
     volatile int* flags = a.flags;
     unsigned R = 0;
+    // ring counters (identical in every thread): qn chunks issued (one
+    // cp.async group each), qu consumed; chunk q uses stage q % kSNST
+    unsigned qn = 0, qu = 0;
     int sweep = 0;
     for (;;) {
         if (sweep >= kOneSidedSweepCap) {
@@ -1239,17 +1262,11 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     bJ = max(b1, b2);
                 }
                 auto gcol = [&](int c) { return c < kSGB ? bI * kSGB + c : bJ * kSGB + (c - kSGB); };
-                // Exact skip: a visit whose two blocks are unchanged since this
-                // pair's last rotation-free visit would recompute the same Gram
-                // bits and again rotate nothing (the reference's skip rule is a
-                // pure function of them), so it only publishes.  Stamps are
-                // round numbers + 1; block visits are ordered by the versions,
-                // so the stamps read after the acquire are current.
                 const int pid = intra ? nb * nb + g : bI * nb + bJ;
                 if (t == 0) {
                     jb_wait_at_least(a.ver + bI, R);
                     jb_wait_at_least(a.ver + bJ, R);
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the previous writers' stores
                     const unsigned c = __ldcg(a.clean + pid);
                     s_skip = c != 0u && c >= __ldcg(a.mod + bI) && c >= __ldcg(a.mod + bJ);
                     atomicAdd(a.counters + 0, 1ull);
@@ -1263,67 +1280,91 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     }
                     continue;
                 }
-                // each thread's kSPer chunk elements: column e / kSCR, row e % kSCR
-                int ccol[kSPer];
+                // the visit's chunk sequence: [0, ncw) Gram of W, [ncw, 2 ncw)
+                // W for the apply, [2 ncw, 2 ncw + ncv) V for the apply
+                const int kend = 2 * ncw + ncv;
+                int kin = 0;  // next sequence position to issue
+                auto issue = [&]() {  // sequence position kin into stage qn % kSNST (all threads)
+                    const int k = kin;
+                    const bool isv = k >= 2 * ncw;
+                    const double* X = isv ? a.V : a.W;
+                    const int64_t ld = isv ? a.ldv : a.ldw;
+                    const int row0 = (isv ? k - 2 * ncw : (k < ncw ? k : k - ncw)) * kSCR;
+                    double* dst = Ring + (qn % kSNST) * (kSC2 * kSCP);
 #pragma unroll
-                for (int it = 0; it < kSPer; ++it) ccol[it] = gcol((t + 256 * it) / kSCR);
-                double pre[kSPer];
-                auto load_chunk = [&](const double* X, int64_t ld, int rows, int k0) {
-#pragma unroll
-                    for (int it = 0; it < kSPer; ++it) {
-                        const int e = t + 256 * it, row = k0 + (e % kSCR);
-                        pre[it] = (ccol[it] < n && row < rows) ? __ldcg(X + row + int64_t(ccol[it]) * ld) : 0.0;
+                    for (int it = 0; it < kSC2 * kSCR / 2 / 256; ++it) {  // 16-byte pieces: 32 per column
+                        const int e = t + 256 * it, c = e >> 5, r2 = (e & 31) * 2;
+                        sg_cp16(dst + c * kSCP + r2, X + row0 + r2 + int64_t(gcol(c)) * ld);
                     }
                 };
-                auto store_chunk = [&]() {
-#pragma unroll
-                    for (int it = 0; it < kSPer; ++it) {
-                        const int e = t + 256 * it;
-                        Cb[(e / kSCR) * kSCP + (e % kSCR)] = pre[it];
+                for (; qn - qu < unsigned(kSNST - 1) && kin < kend; ++qn, ++kin) {
+                    issue();
+                    sg_commit();
+                }
+                // consume the next chunk: wait for its group (kSNST - 2 younger
+                // groups may stay in flight), run body on its stage, then refill
+                // the ring (the stage of chunk qn - kSNST = qu - 1, released by the
+                // barrier) kSNST - 1 chunks ahead; an empty group keeps the
+                // group count aligned at the sequence's end
+                // (the barrier after the wait also retires every thread's reads of
+                // chunk q - 1's stage, the one refilled below)
+                auto consume = [&](auto&& body) {
+                    const unsigned q = qu++;
+                    if (qn - qu >= unsigned(kSNST - 2)) sg_wait<kSNST - 2>(); else sg_wait<0>();
+                    __syncthreads();
+                    body(Ring + (q % kSNST) * (kSC2 * kSCP));
+                    if (kin < kend) {
+                        issue();
+                        ++qn;
+                        ++kin;
                     }
+                    sg_commit();
                 };
                 // ---- 1. Gram -------------------------------------------------
                 {
                     double acc[kSNT][2];
 #pragma unroll
                     for (int u = 0; u < kSNT; ++u) acc[u][0] = acc[u][1] = 0.0;
-                    load_chunk(a.W, a.ldw, m, 0);
-                    for (int k0 = 0; k0 < m; k0 += kSCR) {
-                        __syncthreads();
-                        store_chunk();
-                        __syncthreads();
-                        if (k0 + kSCR < m) load_chunk(a.W, a.ldw, m, k0 + kSCR);
+                    for (int ch = 0; ch < ncw; ++ch) {
+                        consume([&](const double* Cb) {
 #pragma unroll
-                        for (int h = 0; h < kSCR / 32; ++h) {
-                            const int kk = (warp + 8 * h) * 4;
-                            double f[kSNB8];
+                            for (int h = 0; h < kSCR / 32; ++h) {
+                                const int kk = (warp + 8 * h) * 4;
+                                double f[kSNB8];
 #pragma unroll
-                            for (int bb = 0; bb < kSNB8; ++bb) f[bb] = Cb[(bb * 8 + lr) * kSCP + kk + lc];
-                            int u = 0;
+                                for (int bb = 0; bb < kSNB8; ++bb) f[bb] = Cb[(bb * 8 + lr) * kSCP + kk + lc];
+                                int u = 0;
 #pragma unroll
-                            for (int bi = 0; bi < kSNB8; ++bi)
+                                for (int bi = 0; bi < kSNB8; ++bi)
 #pragma unroll
-                                for (int bj = bi; bj < kSNB8; ++bj, ++u) jac_dmma(acc[u][0], acc[u][1], f[bi], f[bj]);
+                                    for (int bj = bi; bj < kSNB8; ++bj, ++u)
+                                        jac_dmma(acc[u][0], acc[u][1], f[bi], f[bj]);
+                            }
+                        });
+                    }
+                    // the 8 warps' partials summed in a fixed order, kSPT tiles a round
+#pragma unroll
+                    for (int u0 = 0; u0 < kSNT; u0 += kSPT) {
+#pragma unroll
+                        for (int u = u0; u < u0 + kSPT; ++u) {
+                            Pb[(warp * kSPT + (u - u0)) * 64 + lr * 8 + 2 * lc] = acc[u][0];
+                            Pb[(warp * kSPT + (u - u0)) * 64 + lr * 8 + 2 * lc + 1] = acc[u][1];
                         }
-                    }
+                        __syncthreads();
+                        for (int e = t; e < kSPT * 64; e += 256) {
+                            const int u = u0 + (e >> 6), w = e & 63;
+                            int bi = 0, rem = u;
+                            while (rem >= kSNB8 - bi) rem -= kSNB8 - bi++;
+                            const int bj = bi + rem;
+                            double sum = 0.0;
 #pragma unroll
-                    for (int u = 0; u < kSNT; ++u) {
-                        Pb[(warp * kSNT + u) * 64 + lr * 8 + 2 * lc] = acc[u][0];
-                        Pb[(warp * kSNT + u) * 64 + lr * 8 + 2 * lc + 1] = acc[u][1];
+                            for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * kSPT + (u - u0)) * 64 + w];
+                            const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
+                            G0[row * kSGP + col] = sum;
+                            G0[col * kSGP + row] = sum;
+                        }
+                        __syncthreads();
                     }
-                }
-                __syncthreads();
-                for (int e = t; e < kSNT * 64; e += 256) {
-                    const int u = e >> 6, w = e & 63;
-                    int bi = 0, rem = u;
-                    while (rem >= kSNB8 - bi) rem -= kSNB8 - bi++;
-                    const int bj = bi + rem;
-                    double sum = 0.0;
-#pragma unroll
-                    for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * kSNT + u) * 64 + w];
-                    const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
-                    G0[row * kSGP + col] = sum;
-                    G0[col * kSGP + row] = sum;
                 }
                 for (int e = t; e < kSC2 * kSC2; e += 256) J[(e / kSC2) * kSGP + e % kSC2] = (e / kSC2 == e % kSC2) ? 1.0 : 0.0;
                 __syncthreads();
@@ -1387,54 +1428,61 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 if (rot) {
                     if (t == 0) flags[sweep % 3] = 1;
                     for (int e = t; e < kSC2 * kSC2; e += 256) Jb[(e / kSC2) * kSJP + e % kSC2] = J[(e / kSC2) * kSGP + e % kSC2];
-                    // ---- 3. W_p J, V_p J: warp (wr, wc) owns rows wr*RF*8..+RF*8, cols wc*24..+24 of a chunk
-                    constexpr int RF = kSCR / 32;  // 8-row fragments per warp
+                    __syncthreads();
+                    // ---- 3. W_p J, V_p J: warp (wr, wc) owns rows wr*16..+16, cols wc*24..+24 of a chunk
                     const int wr = warp & 3, wc = warp >> 2;
                     int ocol[3][2];
 #pragma unroll
                     for (int ct = 0; ct < 3; ++ct)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(wc * 24 + ct * 8 + 2 * lc + h);
+                    double bf[kSC2 / 4][3];
+#pragma unroll
+                    for (int kf = 0; kf < kSC2 / 4; ++kf)
+#pragma unroll
+                        for (int ct = 0; ct < 3; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * kSJP + wc * 24 + ct * 8 + lr];
                     for (int mat = 0; mat < 2; ++mat) {
                         double* X = mat == 0 ? a.W : a.V;
                         const int64_t ld = mat == 0 ? a.ldw : a.ldv;
                         const int rows = mat == 0 ? m : n;
-                        load_chunk(X, ld, rows, 0);
-                        for (int k0 = 0; k0 < rows; k0 += kSCR) {
-                            __syncthreads();
-                            store_chunk();
-                            __syncthreads();
-                            // the next chunk's rows are disjoint from this chunk's outputs
-                            if (k0 + kSCR < rows) load_chunk(X, ld, rows, k0 + kSCR);
-                            double o[RF][3][2];
+                        const int nch = mat == 0 ? ncw : ncv;
+                        for (int ch = 0; ch < nch; ++ch) {
+                            const int k0 = ch * kSCR;
+                            consume([&](const double* Cb) {
+                                double o[2][3][2];
 #pragma unroll
-                            for (int f = 0; f < RF; ++f)
+                                for (int f = 0; f < 2; ++f)
 #pragma unroll
-                                for (int ct = 0; ct < 3; ++ct) o[f][ct][0] = o[f][ct][1] = 0.0;
+                                    for (int ct = 0; ct < 3; ++ct) o[f][ct][0] = o[f][ct][1] = 0.0;
 #pragma unroll
-                            for (int kf = 0; kf < kSC2 / 4; ++kf) {
-                                double af[RF], bf[3];
+                                for (int kf = 0; kf < kSC2 / 4; ++kf) {
+                                    double af[2];
 #pragma unroll
-                                for (int f = 0; f < RF; ++f) af[f] = Cb[(4 * kf + lc) * kSCP + wr * (RF * 8) + f * 8 + lr];
+                                    for (int f = 0; f < 2; ++f) af[f] = Cb[(4 * kf + lc) * kSCP + wr * 16 + f * 8 + lr];
 #pragma unroll
-                                for (int ct = 0; ct < 3; ++ct) bf[ct] = Jb[(4 * kf + lc) * kSJP + wc * 24 + ct * 8 + lr];
+                                    for (int f = 0; f < 2; ++f)
 #pragma unroll
-                                for (int f = 0; f < RF; ++f)
+                                        for (int ct = 0; ct < 3; ++ct)
+                                            jac_dmma(o[f][ct][0], o[f][ct][1], af[f], bf[kf][ct]);
+                                }
 #pragma unroll
-                                    for (int ct = 0; ct < 3; ++ct) jac_dmma(o[f][ct][0], o[f][ct][1], af[f], bf[ct]);
-                            }
+                                for (int f = 0; f < 2; ++f) {
+                                    const int row = k0 + wr * 16 + f * 8 + lr;
+                                    if (row >= rows) continue;
 #pragma unroll
-                            for (int f = 0; f < RF; ++f) {
-                                const int row = k0 + wr * (RF * 8) + f * 8 + lr;
-                                if (row >= rows) continue;
+                                    for (int ct = 0; ct < 3; ++ct)
 #pragma unroll
-                                for (int ct = 0; ct < 3; ++ct)
-#pragma unroll
-                                    for (int h = 0; h < 2; ++h)
-                                        if (ocol[ct][h] < n) X[row + int64_t(ocol[ct][h]) * ld] = o[f][ct][h];
-                            }
+                                        for (int h = 0; h < 2; ++h)
+                                            if (ocol[ct][h] < n) X[row + int64_t(ocol[ct][h]) * ld] = o[f][ct][h];
+                                }
+                            });
                         }
                     }
+                } else {
+                    // nothing rotated: drain the speculatively issued apply chunks
+                    // (the rest of the sequence is never issued)
+                    sg_wait<0>();
+                    qu = qn;
                 }
                 __syncthreads();
                 if (t == 0) {
@@ -1609,29 +1657,6 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     const int m = int(A.rows), n = int(A.cols);
     if (n == 0) return;
     ProfScope prof(ctx, "small_svd", m, n, 0, 0.0);
-    // W's leading dimension even and its pad row zero: bgram stages columns
-    // with 16-byte bulk copies
-    const int ldw = (m + 1) & ~1;
-    const int ldv = (n + 1) & ~1;
-    DMatBuf Wb(ctx, ldw, n), V(ctx, ldv, n);
-    RLRA_CUDA(cudaMemsetAsync(Wb.m.p, 0, sizeof(double) * size_t(ldw) * n, ctx.stream));
-    RLRA_CUDA(cudaMemsetAsync(V.m.p, 0, sizeof(double) * size_t(ldv) * n, ctx.stream));
-    DMatBuf& W = Wb;
-    W.m.rows = m;
-    V.m.rows = n;
-    copy_mat(ctx, A, W);
-    eye_mat(ctx, V);
-    Buf flags(ctx, sizeof(int) * 8), sg(ctx, sizeof(double) * n), rank(ctx, sizeof(int) * n),
-        needs(ctx, sizeof(int) * n);
-    RLRA_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 8, ctx.stream));
-    OneSidedArgs a;
-    a.W = W.m.p;
-    a.ldw = W.m.ld;
-    a.m = m;
-    a.n = n;
-    a.V = V.m.p;
-    a.ldv = V.m.ld;
-    a.flags = flags.i();
     // kernel choice: the shared-memory-resident Gram block Jacobi when a
     // block pair fits (l up to ~1400), else the streaming Gram variant;
     // RLRA_SVD_KERNEL=bgram|block|sgram|gram|onesided forces one (A/B timing)
@@ -1648,7 +1673,38 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     static const int bw_env = std::getenv("RLRA_BGRAM_BW") ? std::atoi(std::getenv("RLRA_BGRAM_BW")) : 0;
     int bgw = (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
     if (bw_env == 16 && n > 32 && bgram_smem<16>(m) <= kSmemCap) bgw = 16;
-    if ((forced == 0 || forced == 1) && bgw > 0) {
+    const bool use_bgram = (forced == 0 || forced == 1) && bgw > 0;
+    const int snb = ceil_div(n, kSGB) + (ceil_div(n, kSGB) & 1);
+    const bool use_sgram = !use_bgram && forced != 2 && forced != 4 && forced != 5 && n > 2 * kSC2 &&
+                           snb / 2 <= ctx.num_sms && m >= 2 * kSCR;
+    // W's leading dimension even and its pad row zero: bgram stages columns
+    // with 16-byte bulk copies; sgram streams whole kSCR-row chunks of
+    // snb * kSGB columns, so its W and V are padded to those (zeros)
+    const int ldw = use_sgram ? ceil_div(m, kSCR) * kSCR : (m + 1) & ~1;
+    const int ldv = use_sgram ? ceil_div(n, kSCR) * kSCR : (n + 1) & ~1;
+    const int ncol = use_sgram ? snb * kSGB : n;
+    DMatBuf Wb(ctx, ldw, ncol), V(ctx, ldv, ncol);
+    RLRA_CUDA(cudaMemsetAsync(Wb.m.p, 0, sizeof(double) * size_t(ldw) * ncol, ctx.stream));
+    RLRA_CUDA(cudaMemsetAsync(V.m.p, 0, sizeof(double) * size_t(ldv) * ncol, ctx.stream));
+    DMatBuf& W = Wb;
+    W.m.rows = m;
+    W.m.cols = n;
+    V.m.rows = n;
+    V.m.cols = n;
+    copy_mat(ctx, A, W);
+    eye_mat(ctx, V);
+    Buf flags(ctx, sizeof(int) * 8), sg(ctx, sizeof(double) * n), rank(ctx, sizeof(int) * n),
+        needs(ctx, sizeof(int) * n);
+    RLRA_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 8, ctx.stream));
+    OneSidedArgs a;
+    a.W = W.m.p;
+    a.ldw = W.m.ld;
+    a.m = m;
+    a.n = n;
+    a.V = V.m.p;
+    a.ldv = V.m.ld;
+    a.flags = flags.i();
+    if (use_bgram) {
         GramJacArgs g;
         g.bar = ctx.gbar;
         g.W = W.m.p;
@@ -1711,8 +1767,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         void* args[] = {&b};
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<BW>, dim3(nblk / 2), dim3(BW * 32),
                                               args, bj_smem, ctx.stream));
-    } else if (forced != 4 && forced != 5 && n > 2 * kSC2 && (ceil_div(n, kSGB) + 1) / 2 <= ctx.num_sms &&
-               m >= 2 * kSCR) {
+    } else if (use_sgram) {
         // columns too long for shared memory: streaming Gram block Jacobi, 48-column pairs
         static bool attr = false;
         if (!attr) {
