@@ -537,8 +537,11 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
             need(a, "a");
             check_ld(lda, m, "a");
             DMatBuf dA(C, m, n), Y(C, m, k + p);
-            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m);
-            rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m);
+            // rsvd_v1/v2 with power steps: A^T Y is summed under the upload too
+            const bool zt = variant != RLRA_RSVD_BASIC && q > 0 && m >= k + p;
+            DMatBuf Zt(C, zt ? n : 0, zt ? k + p : 0);
+            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, zt ? &Zt.m : nullptr);
+            rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m, zt ? &Zt.m : nullptr);
         } else {
             In A(C, loc, a, m, n, lda, "a");
             rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
@@ -940,9 +943,10 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
             // host shard: the upload streams in row chunks under the local sketch GEMM
             need(a, "a");
             check_ld(lda, m_local, "a");
-            DMatBuf dA(C, m_local, n), Y(C, m_local, k + p);
-            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m);
-            rsvd_v2_rowsharded(C, comm->c, dA.m, m_total, k, p, q, s, om, U.m, S.d, V.m, &Y.m);
+            DMatBuf dA(C, m_local, n), Y(C, m_local, k + p), Zt(C, q > 0 ? n : 0, q > 0 ? k + p : 0);
+            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, q > 0 ? &Zt.m : nullptr);
+            rsvd_v2_rowsharded(C, comm->c, dA.m, m_total, k, p, q, s, om, U.m, S.d, V.m, &Y.m,
+                               q > 0 ? &Zt.m : nullptr);
         } else {
             In A(C, loc, a, m_local, n, lda, "a");
             rsvd_v2_rowsharded(C, comm->c, A.m, m_total, k, p, q, s, om, U.m, S.d, V.m);

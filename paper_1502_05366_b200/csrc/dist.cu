@@ -491,7 +491,8 @@ HostCollectives local_group_collectives(LocalGroup* g, int rank) {
 }
 
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
-                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched) {
+                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched,
+                        const DMat* zpre) {
     const int n = int(A.cols), l = k + p;
     DMatBuf Yown, Z(ctx, n, l);
     DMat Y;
@@ -505,6 +506,26 @@ void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, 
     {
         GemmTag tag(ctx, "gemm_power");
         for (int j = 1; j <= q; ++j) {                        // sketch.hpp:53-58
+            if (j == 1 && zpre) {
+                // Z = (sum_g A_g^T Y_g) R^{-1}, R from the allreduced Gram of Y:
+                // the span of A^T orth(Y) without streaming A again (the local
+                // A_g^T Y_g were summed under the shard's upload)
+                DMatBuf G(ctx, l, l), Ri(ctx, l, l);
+                gram_allreduce(ctx, cm, Y, G.m);
+                if (chol_upper_inv(ctx, G.m, Ri.m, ctx.cholqr_pivot_floor)) {
+                    copy_mat(ctx, *zpre, Z.m);
+                    allreduce_mat(ctx, cm, Z.m);
+                    DMatBuf T(ctx, n, l);
+                    GemmOpts tri;
+                    tri.tri_b_upper = true;
+                    gemm(ctx, Op::N, Op::N, 1.0, Z.m, Ri.m, 0.0, T.m, tri);
+                    copy_mat(ctx, T.m, Z.m);
+                    if ((2 * j - 1) % s == 0) orth_span_inplace(ctx, Z.m);  // replicated
+                    gemm(ctx, Op::N, Op::N, 1.0, A, Z.m, 0.0, Y);           // Y_g = A_g Z
+                    continue;
+                }
+                // too ill-conditioned for one CholQR pass: the standard step
+            }
             if ((2 * j - 2) % s == 0) orth_rowsharded(ctx, cm, Y, m_total, true);
             gemm(ctx, Op::T, Op::N, 1.0, A, Y, 0.0, Z.m);    // Z_g = A_g^T Y_g
             allreduce_mat(ctx, cm, Z.m);                       // Z = sum_g

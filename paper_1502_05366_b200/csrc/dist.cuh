@@ -86,8 +86,11 @@ void gen_test_matrix_rowsharded(Context& ctx, Comm& cm, const std::vector<double
 // rsvd_v2 on the row block A_g (m_g x n) of an m_total x n matrix held by the
 // ranks of cm; U_g (m_g x k) row-sharded like A, sigma (device, k) and V
 // (n x k) replicated on every rank.
+// sketched: Y_g = A_g Omega already formed; zpre: A_g^T Y_g summed under the
+// upload (the first power step then needs no pass over A_g).
 void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, int k, int p, int q, int s,
-                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr);
+                        OmegaSource& om, const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr,
+                        const DMat* zpre = nullptr);
 
 // id_rand (interp.hpp:203-223) on the row-sharded A: jc (device, n) and V
 // (n x k) replicated.  Omega~ is m_total x l, this rank using rows

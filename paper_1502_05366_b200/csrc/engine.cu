@@ -189,7 +189,7 @@ static void orth_mid(Context& ctx, const DMat& Y, bool span_only) {
 }
 
 void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
-                  bool span_only, bool sketched) {
+                  bool span_only, bool sketched, const DMat* zpre) {
     const int n = int(A.cols);
     if (!sketched) sketch(ctx, Op::N, A, l, om, Y);  // Y = A * Omega
     if (q == 0) return;
@@ -197,6 +197,22 @@ void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource&
     if (span_only) Y2 = DMatBuf(ctx, Y.rows, l);  // span-only orth output: no copy back into Y
     GemmTag tag(ctx, "gemm_power");
     for (int j = 1; j <= q; ++j) {
+        if (j == 1 && zpre && span_only) {
+            // A^T Q = (A^T Y) R^{-1} with Y = Q R the CholQR pass sketch.hpp:54
+            // asks for: the span the reference's orth(Y) then A^T Q produce,
+            // without streaming A a second time (A^T Y was summed under the
+            // upload).  Rounding differs from A^T (Y R^{-1}) by ~u kappa(Y).
+            DMatBuf Ri(ctx, l, l);
+            if (span_rinv(ctx, Y, Ri.m)) {
+                GemmOpts tri;
+                tri.tri_b_upper = true;
+                gemm(ctx, Op::N, Op::N, 1.0, *zpre, Ri.m, 0.0, Z.m, tri);
+                if ((2 * j - 1) % s == 0) orth_mid(ctx, Z, span_only);
+                gemm(ctx, Op::N, Op::N, 1.0, A, Z, 0.0, Y);  // Y = A Z
+                continue;
+            }
+            // too ill-conditioned for one CholQR pass: the standard step below
+        }
         DMat Yc = Y;
         if ((2 * j - 2) % s == 0) {
             if (span_only && orth_span_into(ctx, Y, Y2.m))
@@ -226,9 +242,12 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
 }
 
 void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
-                       const DMat& Y) {
+                       const DMat& Y, const DMat* Zt) {
     const int64_t m = dA.rows, n = dA.cols;
-    if (m <= 0 || n <= 0) return;
+    if (m <= 0 || n <= 0) {
+        if (Zt) zero_mat(ctx, *Zt);
+        return;
+    }
     if (!ctx.copy_stream) RLRA_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
     // Omega once (callback mode: the reference's draw, uploaded; Philox: philox_fill)
     const int draw = om.next_draw++;
@@ -276,6 +295,10 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
         } else {
             gemm(ctx, Op::N, Op::N, 1.0, Ar, Om.m, 0.0, Yr);
         }
+        if (Zt) {  // Zt += A_c^T Y_c, chunks summed in order (deterministic)
+            GemmTag zt(ctx, "gemm_power");
+            gemm(ctx, Op::T, Op::N, 1.0, Ar, Yr, r0 == 0 ? 0.0 : 1.0, *Zt);
+        }
     }
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));  // h (callback Omega) outlives its copy; events done
     for (auto e : ev) cudaEventDestroy(e);
@@ -283,7 +306,7 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
 }
 
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
-          const DMat& U, double* sigma, const DMat& V, const DMat* sketched) {
+          const DMat& U, double* sigma, const DMat& V, const DMat* sketched, const DMat* zpre) {
     const int m = int(A.rows), n = int(A.cols), l = k + p;
     DMatBuf Yown;
     DMat Y;
@@ -308,7 +331,7 @@ void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, 
         RLRA_CUDA(cudaMemcpyAsync(sigma, sb.p, sizeof(double) * k, cudaMemcpyDeviceToDevice, ctx.stream));
         return;
     }
-    sample_right(ctx, A, l, q, s, om, Y, /*span_only=*/true, /*sketched=*/sketched != nullptr);
+    sample_right(ctx, A, l, q, s, om, Y, /*span_only=*/true, /*sketched=*/sketched != nullptr, zpre);
     orth(ctx, Y);
     GemmTag tag(ctx, "gemm_proj");
     if (variant == RLRA_RSVD_V2) {

@@ -19,15 +19,21 @@ struct OmegaSource {
 // sketch.hpp:44-60 — Y (m x l)
 // span_only: intermediate re-orthonormalisations keep the span but not an
 // orthonormal basis (callers that never expose the sample).
+// zpre (optional, with sketched): A^T Y of the sketch, accumulated while A
+// was uploaded; the first power step then forms Z = (A^T Y) R^{-1} from the
+// CholQR factor of Y instead of streaming A again (span-equal to A^T Q).
 void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Y,
-                  bool span_only = false, bool sketched = false);
+                  bool span_only = false, bool sketched = false, const DMat* zpre = nullptr);
 
 // Host-resident A: upload it into the device buffer dA in row chunks on the
 // context's copy stream and compute the sketch Y = A Omega chunk by chunk as
 // the rows land (the chunk GEMMs are the unchunked GEMM's tiles, so Y is
 // bit-identical); consumes one Omega draw.
+// With Zt (n x l) non-null, also Zt = A^T Y accumulated chunk by chunk
+// (sum over the row chunks in order, under the upload): the first power
+// product of rsvd (sample_right's zpre).
 void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
-                       const DMat& Y);
+                       const DMat& Y, const DMat* Zt = nullptr);
 // sketch.hpp:65-67 — returns Y^T (n x l) of the reference's l x n sample,
 // computed on A directly (the reference materialises A^T; we never do).
 void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource& om, const DMat& Yt,
@@ -47,7 +53,8 @@ void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat
 
 // rsvd.hpp:127-160; U m x k, sigma (device) k, V n x k
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,
-          const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr);
+          const DMat& U, double* sigma, const DMat& V, const DMat* sketched = nullptr,
+          const DMat* zpre = nullptr);
 
 struct QbOut {
     int ell = 0;
