@@ -66,6 +66,12 @@ def self_launch(n):
     0's stdout is the JSON line."""
     import socket
 
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} GPU(s) visible", file=sys.stderr)
+        return 1
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
     port = sk.getsockname()[1]
@@ -304,6 +310,9 @@ def main():
         if world > 1:
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # NCCL's log lines (INIT info, its version banner) go to stderr: stdout
+        # carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         os.environ.setdefault("NCCL_ALGO", "Ring")
         os.environ.setdefault("NCCL_PROTO", "Simple")
         if world > 1:
