@@ -17,6 +17,7 @@
 #include "dist.cuh"
 #include "engine.cuh"
 #include "io.cuh"
+#include "hostio.cuh"
 #include "gemm.cuh"
 #include "jacobi.cuh"
 #include "qr.cuh"
@@ -227,6 +228,7 @@ rlra_status rlra_ctx_destroy(rlra_ctx* ctx) {
         cudaStreamDestroy(ctx->c.stream);
     }
     if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
+    stager_destroy(ctx->c);
     if (ctx->c.h_scalars) cudaFreeHost(ctx->c.h_scalars);
     if (ctx->c.h_flags) cudaFreeHost(ctx->c.h_flags);
     if (ctx->c.gbar) cudaFree(ctx->c.gbar);

@@ -91,6 +91,8 @@ struct Context {
     std::vector<ProfRec> prof;
     // label the profiler gives the next GEMM launches (see GemmTag)
     const char* gemm_tag = "gemm";
+    // pinned staging slots + host copy threads for pageable buffers (hostio.cu, lazy)
+    void* stager = nullptr;
 };
 
 // Scoped label for GEMM launches (profiling/accounting only).

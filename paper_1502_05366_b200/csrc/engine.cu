@@ -12,6 +12,7 @@
 
 #include "cpqr.cuh"
 #include "engine.cuh"
+#include "hostio.cuh"
 #include "gemm.cuh"
 #include "jacobi.cuh"
 #include "qr.cuh"
@@ -278,8 +279,7 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
     GemmTag tag(ctx, "gemm_sketch");
     for (int64_t r0 = 0; r0 < m; r0 += rows) {
         const int64_t nr = std::min(rows, m - r0);
-        RLRA_CUDA(cudaMemcpy2DAsync(dA.p + r0, sizeof(double) * dA.ld, hA + r0, sizeof(double) * lda,
-                                    sizeof(double) * nr, n, cudaMemcpyHostToDevice, ctx.copy_stream));
+        h2d_copy(ctx, ctx.copy_stream, hA + r0, lda, dA.block(r0, 0, nr, n));  // pageable: staged
         cudaEvent_t e;
         RLRA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         RLRA_CUDA(cudaEventRecord(e, ctx.copy_stream));

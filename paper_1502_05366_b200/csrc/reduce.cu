@@ -1,5 +1,6 @@
 // reduce.cu — deterministic reductions and small data-movement kernels.
 #include "reduce.cuh"
+#include "hostio.cuh"
 
 namespace rlra_b200 {
 
@@ -148,17 +149,11 @@ void symmetrize_upper(Context& ctx, const DMat& a) {
 }
 
 void h2d_mat(Context& ctx, const double* h, int64_t ldh, const DMat& d) {
-    if (d.rows <= 0 || d.cols <= 0) return;
-    RLRA_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double) * d.ld, h, sizeof(double) * ldh,
-                                sizeof(double) * d.rows, d.cols, cudaMemcpyHostToDevice,
-                                ctx.stream));
+    h2d_copy(ctx, ctx.stream, h, ldh, d);  // pageable host memory is staged (hostio.cu)
 }
 
 void d2h_mat(Context& ctx, const DMat& d, double* h, int64_t ldh) {
-    if (d.rows <= 0 || d.cols <= 0) return;
-    RLRA_CUDA(cudaMemcpy2DAsync(h, sizeof(double) * ldh, d.p, sizeof(double) * d.ld,
-                                sizeof(double) * d.rows, d.cols, cudaMemcpyDeviceToHost,
-                                ctx.stream));
+    d2h_copy(ctx, d, h, ldh);  // returns with h filled
 }
 
 }  // namespace rlra_b200

@@ -351,3 +351,29 @@ def test_qb_hierarchical_vs_reference(eng, nrb):
     with pytest.raises(R.DimensionError) as e:
         eng.qb_hierarchical(a, 3, b, M, 1, R.Rng(1))
     assert "num_row_blocks must be one of {2,4,8,...} (got 3)" in str(e.value)
+
+
+def test_pageable_host_buffers_staged_bit_identical_to_pinned(eng):
+    """A reference user's DenseMatrix is pageable memory: the C-ABI stages it
+    through pinned slots with a pool of copy threads (csrc/hostio.cu) in both
+    directions.  Results equal the pinned-buffer call bit for bit (48 MB A:
+    over the staging threshold; U 16 MB comes back staged too)."""
+    import torch
+
+    m, n, k, p, q = 4000, 1500, 500, 10, 2
+    a = make_test_matrix(m, n, np.exp(-np.arange(1500) / 80.0), seed=71)
+    outs = []
+    for pinned in (True, False):
+        A = torch.from_numpy(a.T.copy().reshape(-1))  # column-major bytes
+        if pinned:
+            A = A.pin_memory()
+        U = torch.zeros(m * k, dtype=torch.float64, pin_memory=pinned)
+        V = torch.zeros(n * k, dtype=torch.float64, pin_memory=pinned)
+        S = torch.zeros(k, dtype=torch.float64, pin_memory=pinned)
+        eng.host_rsvd_ptr(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, 1, R.Omega.philox(5), U.data_ptr(),
+                          S.data_ptr(), V.data_ptr())
+        outs.append((U.numpy().copy(), S.numpy().copy(), V.numpy().copy()))
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+    u = outs[1][0].reshape(k, m).T
+    assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-11
