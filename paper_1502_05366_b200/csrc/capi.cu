@@ -34,7 +34,8 @@ namespace {
 thread_local std::string g_err;
 
 template <class F>
-rlra_status guard(rlra_ctx* ctx, F&& f) {
+rlra_status guard(rlra_ctx* ctx, const char* name, F&& f) {
+    NvtxRange range(name);  // the entry point on the Nsight timeline
     try {
         if (!ctx) raise(RLRA_EINVAL, "null rlra_ctx");
         RLRA_CUDA(cudaSetDevice(ctx->c.device));
@@ -237,13 +238,13 @@ rlra_status rlra_ctx_destroy(rlra_ctx* ctx) {
 }
 
 rlra_status rlra_ctx_synchronize(rlra_ctx* ctx) {
-    return guard(ctx, [&](Context& c) { sync(c); });
+    return guard(ctx, __func__, [&](Context& c) { sync(c); });
 }
 
 uint64_t rlra_ctx_launch_count(const rlra_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
 rlra_status rlra_ctx_profile(rlra_ctx* ctx, int enable) {
-    return guard(ctx, [&](Context& c) {
+    return guard(ctx, __func__, [&](Context& c) {
         sync(c);
         for (auto& r : c.prof) {
             cudaEventDestroy(r.start);
@@ -258,7 +259,7 @@ int rlra_ctx_profile_count(const rlra_ctx* ctx) { return ctx ? int(ctx->c.prof.s
 
 rlra_status rlra_ctx_profile_get(rlra_ctx* ctx, int i, char* name, int name_cap, int* M, int* N, int* K,
                                  double* flops, double* ms) {
-    return guard(ctx, [&](Context& c) {
+    return guard(ctx, __func__, [&](Context& c) {
         if (i < 0 || i >= int(c.prof.size())) raise(RLRA_EINVAL, "profile index out of range");
         sync(c);
         const auto& r = c.prof[i];
@@ -279,7 +280,7 @@ void* rlra_ctx_stream(const rlra_ctx* ctx) { return ctx ? (void*)ctx->c.stream :
 rlra_status rlra_matmul(rlra_ctx* ctx, int loc, int ta, int tb, const double* a, int ar, int ac,
                         int64_t lda, const double* b, int br, int bc, int64_t ldb, double* c,
                         int64_t ldc) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         const int m = ta ? ac : ar, ka = ta ? ar : ac, kb = tb ? bc : br, n = tb ? br : bc;
         if (ka != kb)
             raise(RLRA_EDIM, fmt("matmul: inner dimensions disagree: op(%dx%d) * op(%dx%d)", ar, ac, br,
@@ -295,7 +296,7 @@ rlra_status rlra_matmul(rlra_ctx* ctx, int loc, int ta, int tb, const double* a,
 
 rlra_status rlra_compact_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                             double* q, int64_t ldq, double* r, int64_t ldr, int* degenerate) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (m < n) raise(RLRA_EDIM, fmt("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
         In A(C, loc, a, m, n, lda, "a");
         Out Q(C, loc, q, m, n, ldq, "q");
@@ -319,7 +320,7 @@ rlra_status rlra_compact_qr(rlra_ctx* ctx, int loc, const double* a, int m, int 
 rlra_status rlra_pivoted_qr(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k,
                             double tol, double* q1, int64_t ldq1, double* s1, int64_t lds1, int* perm,
                             int* frank, double* residual, int* reached, int* degenerate) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         const int rmax = std::min(m, n);
         const bool tol_mode = (k == 0 && tol > 0.0);
         if (!tol_mode && (k < 1 || k > rmax || tol != 0.0))
@@ -352,7 +353,7 @@ rlra_status rlra_pivoted_qr(rlra_ctx* ctx, int loc, const double* a, int m, int 
 rlra_status rlra_upper_tri_solve(rlra_ctx* ctx, int loc, const double* s11, int k, int64_t lds11,
                                  const double* s12, int nc, int64_t lds12, double* t, int64_t ldt,
                                  int* clamped) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         In S11(C, loc, s11, k, k, lds11, "s11"), S12(C, loc, s12, k, nc, lds12, "s12");
         Out T(C, loc, t, k, nc, ldt, "t");
         const bool cl = upper_tri_solve(C, S11.m, S12.m, T.m);
@@ -364,7 +365,7 @@ rlra_status rlra_upper_tri_solve(rlra_ctx* ctx, int loc, const double* s11, int 
 
 rlra_status rlra_small_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                            double* u, int64_t ldu, double* sigma, double* v, int64_t ldv) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         const int r = std::min(m, n);
         In A(C, loc, a, m, n, lda, "a");
         Out U(C, loc, u, m, r, ldu, "u"), V(C, loc, v, n, r, ldv, "v");
@@ -379,7 +380,7 @@ rlra_status rlra_small_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n
 
 rlra_status rlra_sym_eig(rlra_ctx* ctx, int loc, const double* t, int n, int64_t ldt, double* values,
                          double* vectors, int64_t ldv) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         In T(C, loc, t, n, n, ldt, "t");
         Out V(C, loc, vectors, n, n, ldv, "vectors");
         OutVec<double> D(C, loc, values, n, "values");
@@ -392,7 +393,7 @@ rlra_status rlra_sym_eig(rlra_ctx* ctx, int loc, const double* t, int n, int64_t
 
 rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                                 double* out) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(out, "out");
         In A(C, loc, a, m, n, lda, "a");
         *out = frobenius(C, A.m);
@@ -401,7 +402,7 @@ rlra_status rlra_frobenius_norm(rlra_ctx* ctx, int loc, const double* a, int m, 
 
 rlra_status rlra_sketch(rlra_ctx* ctx, int loc, int trans, const double* a, int m, int n, int64_t lda, int l,
                         const rlra_omega* omega, int draw, int64_t row0, double* y, int64_t ldy) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (l < 1) raise(RLRA_EDIM, fmt("sketch: width %d", l));
         const rlra_omega* o = omega;
         if (!o) raise(RLRA_EINVAL, "null rlra_omega");
@@ -429,7 +430,7 @@ rlra_status rlra_sketch(rlra_ctx* ctx, int loc, int trans, const double* a, int 
 
 rlra_status rlra_gram(rlra_ctx* ctx, int loc, const double* y, int m, int n, int64_t ldy, double* g,
                       int64_t ldg) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         In Y(C, loc, y, m, n, ldy, "y");
         Out G(C, loc, g, n, n, ldg, "g");
         GemmOpts sy;
@@ -443,7 +444,7 @@ rlra_status rlra_gram(rlra_ctx* ctx, int loc, const double* y, int m, int n, int
 
 rlra_status rlra_chol_inv(rlra_ctx* ctx, int loc, const double* g, int n, int64_t ldg, double floor, double* r,
                           int64_t ldr, double* rinv, int64_t ldri, int* ok) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         In G(C, loc, g, n, n, ldg, "g");
         Out Rm(C, loc, r, n, n, ldr, "r"), Ri(C, loc, rinv, n, n, ldri, "rinv");
         copy_mat(C, G.m, Rm.m);
@@ -457,7 +458,7 @@ rlra_status rlra_chol_inv(rlra_ctx* ctx, int loc, const double* g, int n, int64_
 
 rlra_status rlra_trmm_right_upper(rlra_ctx* ctx, int loc, const double* y, int m, int n, int64_t ldy,
                                   const double* t, int64_t ldt, double* out, int64_t ldo) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (y == out) raise(RLRA_EINVAL, "trmm_right_upper: out aliases y");
         In Y(C, loc, y, m, n, ldy, "y"), T(C, loc, t, n, n, ldt, "t");
         Out O(C, loc, out, m, n, ldo, "out");
@@ -473,7 +474,7 @@ rlra_status rlra_trmm_right_upper(rlra_ctx* ctx, int loc, const double* y, int m
 rlra_status rlra_lowrank_residual(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                                   const double* x, int64_t ldx, const double* y, int64_t ldy, int k,
                                   double* out) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(out, "out");
         In A(C, loc, a, m, n, lda, "a"), X(C, loc, x, m, k, ldx, "x"), Y(C, loc, y, n, k, ldy, "y");
         Buf sq(C, sizeof(double));
@@ -491,7 +492,7 @@ rlra_status rlra_lowrank_residual(rlra_ctx* ctx, int loc, const double* a, int m
 
 rlra_status rlra_gaussian_philox(rlra_ctx* ctx, int loc, int rows, int cols, uint64_t seed, int draw,
                                  int64_t row0, double* out, int64_t ld) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         Out O(C, loc, out, rows, cols, ld, "out");
         philox_fill(C, O.m, seed, draw, row0);
         O.finish(C);
@@ -501,7 +502,7 @@ rlra_status rlra_gaussian_philox(rlra_ctx* ctx, int loc, int rows, int cols, uin
 
 rlra_status rlra_sample(rlra_ctx* ctx, int loc, int left, const double* a, int m, int n, int64_t lda,
                         int l, int q, int s, const rlra_omega* omega, double* y, int64_t ldy) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (left)
             check_sample(l, q, s, n, m);
         else
@@ -527,7 +528,7 @@ rlra_status rlra_sample(rlra_ctx* ctx, int loc, int left, const double* a, int m
 rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int m, int n, int64_t lda,
                       int k, int p, int q, int s, const rlra_omega* omega, double* u, int64_t ldu,
                       double* sigma, double* v, int64_t ldv) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (variant < 0 || variant > 2) raise(RLRA_EINVAL, fmt("unknown rsvd variant %d", variant));
         check_sample_rank(k, p, m, n);
         if (variant != RLRA_RSVD_BASIC) check_sample(k + p, q, s, m, n);
@@ -558,7 +559,7 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
 rlra_status rlra_qb_parallel(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int blk,
                              int num_blocks, int q_power, const rlra_omega* omega, double* q, int64_t ldq,
                              double* b, int64_t ldb, double* final_residual) {
-    return guard(ctx, [&](Context& C) {  // qb.hpp:161-170 checks and messages
+    return guard(ctx, __func__, [&](Context& C) {  // qb.hpp:161-170 checks and messages
         if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
         if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
         if (q_power < 0) raise(RLRA_EDIM, fmt("power iteration count must be >= 0 (got %d)", q_power));
@@ -580,7 +581,7 @@ rlra_status rlra_qb_parallel(rlra_ctx* ctx, int loc, const double* a, int m, int
 rlra_status rlra_qb_hierarchical(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                                  int num_row_blocks, int blk, int num_blocks, int q_power, const rlra_omega* omega,
                                  double* q, int64_t ldq, double* b, int64_t ldb, double* final_residual) {
-    return guard(ctx, [&](Context& C) {  // qb.hpp:213-226 checks and messages
+    return guard(ctx, __func__, [&](Context& C) {  // qb.hpp:213-226 checks and messages
         const int blocks = num_row_blocks;
         if (blocks < 2 || (blocks & (blocks - 1)) != 0)
             raise(RLRA_EDIM, fmt("num_row_blocks must be one of {2,4,8,...} (got %d)", blocks));
@@ -618,7 +619,7 @@ rlra_status rlra_binary_header(const char* path, int* rows, int* cols) {
 
 rlra_status rlra_load_binary(rlra_ctx* ctx, int loc, const char* path, int64_t row0, int rows, double* a,
                              int64_t lda) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(path, "path");
         const BinaryHeader h = read_binary_header(path);
         Out A(C, loc, a, rows, h.cols, lda, "a");
@@ -629,7 +630,7 @@ rlra_status rlra_load_binary(rlra_ctx* ctx, int loc, const char* path, int64_t r
 }
 
 rlra_status rlra_save_binary(rlra_ctx* ctx, int loc, const char* path, const double* a, int m, int n, int64_t lda) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(path, "path");
         if (m <= 0 || n <= 0) raise(RLRA_EDIM, fmt("save_binary: %dx%d matrix", m, n));
         In A(C, loc, a, m, n, lda, "a");
@@ -639,7 +640,7 @@ rlra_status rlra_save_binary(rlra_ctx* ctx, int loc, const char* path, const dou
 
 rlra_status rlra_gen_test_matrix(rlra_ctx* ctx, int loc, int m, int n, const double* sigma, int r, uint64_t seed,
                                  double noise, double* a, int64_t lda) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (r < 0 || r > std::min(m, n)) raise(RLRA_EDIM, fmt("gen_test_matrix: %d singular values for %dx%d", r, m, n));
         if (r > 0) need(sigma, "sigma");
         Out A(C, loc, a, m, n, lda, "a");
@@ -656,7 +657,7 @@ struct rlra_comm {
 rlra_status rlra_gen_test_matrix_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, int64_t row0, int m_local,
                                             int64_t m_total, int n, const double* sigma, int r, uint64_t seed,
                                             double noise, double* a, int64_t lda) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         if (row0 < 0 || m_local < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
@@ -676,7 +677,7 @@ rlra_status rlra_gen_test_matrix_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int 
 rlra_status rlra_verify_lowrank(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* x,
                                 int64_t ldx, const double* y, int64_t ldy, int k, const double* sigma_true, int r,
                                 double out[5]) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(out, "out");
         // k may exceed min(m, n): a QB with ell > min(m, n) columns (test_report.cpp:95-108)
         if (k < 0) raise(RLRA_EDIM, "verify: factor shapes do not match the matrix");
@@ -695,7 +696,7 @@ rlra_status rlra_verify_lowrank(rlra_ctx* ctx, int loc, const double* a, int m, 
 rlra_status rlra_qb_single(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, double tol,
                            int max_rank, const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,
                            int* ell, double* hist, int* nhist, double* final_residual, int* reached) {
-    return guard(ctx, [&](Context& C) {  // qb.hpp:44-50 checks and messages
+    return guard(ctx, __func__, [&](Context& C) {  // qb.hpp:44-50 checks and messages
         if (tol <= 0.0) raise(RLRA_EDIM, fmt("qb_single needs tol > 0 (got %g)", tol));
         const int rmax = std::min(m, n);
         if (max_rank < 1 || max_rank > rmax)
@@ -719,7 +720,7 @@ rlra_status rlra_qb_single(rlra_ctx* ctx, int loc, const double* a, int m, int n
 rlra_status rlra_verify_svd(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, const double* u,
                             int64_t ldu, const double* sigma, const double* v, int64_t ldv, int k,
                             const double* sigma_true, int r, double out[5]) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         need(out, "out");
         if (k < 0 || k > std::min(m, n)) raise(RLRA_EDIM, "verify: SVD factor shapes do not match the matrix");
         In A(C, loc, a, m, n, lda, "a"), U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
@@ -752,7 +753,7 @@ rlra_status rlra_comm_unique_id(unsigned char id[128]) {
 }
 
 rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nranks, int rank, rlra_comm** out) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!out || !id) raise(RLRA_EINVAL, "null argument to rlra_comm_create");
         *out = nullptr;
         auto* cm = new rlra_comm();
@@ -768,7 +769,7 @@ rlra_status rlra_comm_create(rlra_ctx* ctx, const unsigned char id[128], int nra
 
 rlra_status rlra_comm_create_host(rlra_ctx* ctx, int nranks, int rank, const rlra_host_collectives* coll,
                                   rlra_comm** out) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!out || !coll) raise(RLRA_EINVAL, "null argument to rlra_comm_create_host");
         *out = nullptr;
         HostCollectives hc;
@@ -842,7 +843,7 @@ rlra_status rlra_qb_blocked_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, 
                                        double tol, int q_power, int reorth_period, const rlra_omega* omega,
                                        double* q, int64_t ldq, double* b, int64_t ldb, int cap, int* ell,
                                        double* hist, int* nhist, double* final_residual, int* reached) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         if (m_total < m_local || m_total > INT32_MAX)
@@ -892,7 +893,7 @@ rlra_status rlra_qb_hierarchical_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int 
                                             int n, int64_t lda, int64_t m_total, int num_row_blocks, int blk,
                                             int num_blocks, int q_power, const rlra_omega* omega, double* q,
                                             int64_t ldq, double* b, int64_t ldb, double* final_residual) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         const int nrb = num_row_blocks, W = comm->c.nranks;
@@ -931,7 +932,7 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
                                  int64_t lda, int64_t m_total, int k, int p, int q, int s,
                                  const rlra_omega* omega, double* u, int64_t ldu, double* sigma, double* v,
                                  int64_t ldv) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         if (m_total < m_local || m_total > INT32_MAX)
@@ -964,7 +965,7 @@ rlra_status rlra_id_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, con
                                     int64_t lda, int64_t row0, int64_t m_total, int k, int p, int q, int s,
                                     const rlra_omega* omega, int* jc, double* v, int64_t ldv,
                                     double* qr_residual, int* clamped) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
@@ -990,7 +991,7 @@ rlra_status rlra_cur_rand_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, co
                                      const rlra_omega* omega, int* jc, int* jr, double* v, int64_t ldv, double* w,
                                      int64_t ldw, double* c, int64_t ldc, double* u, int64_t ldu, double* r,
                                      int64_t ldr, double* residual, double* qr_residual) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (!comm) raise(RLRA_EINVAL, "null rlra_comm");
         CommGpuScope gpu_token(comm->c);
         if (row0 < 0 || row0 + m_local > m_total || m_total > INT32_MAX)
@@ -1024,7 +1025,7 @@ rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int
                             const rlra_omega* omega, double* q, int64_t ldq, double* b, int64_t ldb,
                             int cap, int* ell, double* hist, int* nhist, double* final_residual,
                             int* reached) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (blk < 1) raise(RLRA_EDIM, fmt("block size b must be >= 1 (got %d)", blk));
         if (num_blocks < 1) raise(RLRA_EDIM, fmt("block count M must be >= 1 (got %d)", num_blocks));
         if (tol < 0.0) raise(RLRA_EDIM, fmt("tol must be >= 0 (got %g)", tol));
@@ -1073,7 +1074,7 @@ rlra_status rlra_qb_blocked(rlra_ctx* ctx, int loc, double* a, int m, int n, int
 rlra_status rlra_svd_from_qb(rlra_ctx* ctx, int loc, const double* q, int m, int64_t ldq, const double* b,
                              int n, int64_t ldb, int ell, int k, int vnum, double* u, int64_t ldu,
                              double* sigma, double* v, int64_t ldv, int* k_out) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (k < 0 || k > ell) raise(RLRA_EDIM, fmt("rank k = %d outside [0, rank(B) = %d]", k, ell));
         if (k == 0) k = ell;
         if (k_out) *k_out = k;
@@ -1092,7 +1093,7 @@ rlra_status rlra_svd_from_qb(rlra_ctx* ctx, int loc, const double* q, int m, int
 rlra_status rlra_id_column(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k,
                            double tol, int* jc, double* v, int64_t ldv, int* k_out, double* qr_residual,
                            int* reached, int* clamped) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         const int rmax = std::min(m, n);
         const bool tol_mode = (k == 0 && tol > 0.0);
         if (!tol_mode && (k < 1 || k > rmax || tol != 0.0))
@@ -1119,7 +1120,7 @@ rlra_status rlra_id_column(rlra_ctx* ctx, int loc, const double* a, int m, int n
 rlra_status rlra_id_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda, int k, int p,
                          int q, int s, const rlra_omega* omega, int* jc, double* v, int64_t ldv,
                          double* qr_residual, int* clamped) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         check_sample_rank(k, p, m, n);
         check_sample(k + p, q, s, n, m);
         OmegaSource om = omega_of(omega);
@@ -1137,7 +1138,7 @@ rlra_status rlra_id_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n, 
 
 rlra_status rlra_two_sided_from_column(rlra_ctx* ctx, int loc, const double* a, int m, int n, int64_t lda,
                                        const int* jc, int k, int* jr, double* w, int64_t ldw) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (k < 0 || k > std::min(m, n)) raise(RLRA_EDIM, fmt("two_sided_from_column: rank %d", k));
         OutVec<int> J(C, loc, jr, m, "jr");
         if (k == 0) {
@@ -1184,7 +1185,7 @@ rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int
                                     const int* jc, const int* jr, const double* v, int64_t ldv, int k,
                                     double* c, int64_t ldc, double* u, int64_t ldu, double* r,
                                     int64_t ldr, double* residual) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         In A(C, loc, a, m, n, lda, "a");
         InVec<int> Jc(C, loc, jc, n, "jc"), Jr(C, loc, jr, m, "jr");
         In V(C, loc, v, n, k, ldv, "v");
@@ -1194,7 +1195,7 @@ rlra_status rlra_cur_from_two_sided(rlra_ctx* ctx, int loc, const double* a, int
 
 rlra_status rlra_cur_linkage(rlra_ctx* ctx, int loc, const double* r, int k, int n, int64_t ldr, const double* v,
                              int64_t ldv, const int* jr, double* u, int64_t ldu) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         if (k < 0 || n < 0) raise(RLRA_EDIM, fmt("cur_linkage: negative dimensions %dx%d", k, n));
         if (k == 0) return;
         if (n < k) raise(RLRA_EDIM, fmt("cur_linkage: R is %dx%d, need at least as many columns as rows", k, n));
@@ -1211,7 +1212,7 @@ rlra_status rlra_cur_rand(rlra_ctx* ctx, int loc, const double* a, int m, int n,
                           int q, int s, const rlra_omega* omega, int* jc, int* jr, double* v,
                           int64_t ldv, double* w, int64_t ldw, double* c, int64_t ldc, double* u,
                           int64_t ldu, double* r, int64_t ldr, double* residual, double* qr_residual) {
-    return guard(ctx, [&](Context& C) {
+    return guard(ctx, __func__, [&](Context& C) {
         check_sample_rank(k, p, m, n);
         check_sample(k + p, q, s, n, m);
         OmegaSource om = omega_of(omega);

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdarg>
 #include <cstdint>
@@ -103,12 +104,15 @@ struct GemmTag {
     ~GemmTag() { ctx.gemm_tag = prev; }
 };
 
-// Records one interval on ctx.stream when profiling is enabled.
+// Records one interval on ctx.stream when profiling is enabled, and always
+// an NVTX range of the same name (host timeline for Nsight tools; a no-op
+// without a tool attached).
 struct ProfScope {
     Context& ctx;
     int idx = -1;
     ProfScope(Context& c, const char* name, int M = 0, int N = 0, int K = 0, double flops = 0.0)
         : ctx(c) {
+        nvtxRangePushA(name);
         if (!ctx.profile) return;
         Context::ProfRec r{name, nullptr, nullptr, M, N, K, flops};
         cudaEventCreate(&r.start);
@@ -119,7 +123,16 @@ struct ProfScope {
     }
     ~ProfScope() {
         if (idx >= 0) cudaEventRecord(ctx.prof[idx].stop, ctx.stream);
+        nvtxRangePop();
     }
+};
+
+// NVTX range for a C-ABI entry point (rlra_rsvd, rlra_qb_blocked, ...)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // RAII device scratch buffer on the context's pool.
