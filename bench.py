@@ -60,7 +60,7 @@ def dist_env():
     return rank, world, local
 
 
-def self_launch(n):
+def self_launch(n, share_gpus=False):
     """--gpus N without a launcher: start N ranks of this script (one process
     per GPU, the environment torch.distributed.run would set) and wait; rank
     0's stdout is the JSON line."""
@@ -69,7 +69,7 @@ def self_launch(n):
     import torch
 
     have = torch.cuda.device_count()
-    if have < n:
+    if have < n and not share_gpus:  # (--comm host lets ranks share GPUs)
         print(f"bench.py: --gpus {n} but only {have} GPU(s) visible", file=sys.stderr)
         return 1
     sk = socket.socket()
@@ -285,11 +285,14 @@ def main():
     ap.add_argument("--n", type=int, default=C5["n"])
     ap.add_argument("--dist", action="store_true",
                     help="use the row-sharded NCCL path even at N=1 (exercises dist.py)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="host: the drivers' host-staged collectives over gloo with a GPU token, so "
+                         "ranks may share a GPU (functional test of the N-rank path; not a timing)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        sys.exit(self_launch(args.gpus))
+        sys.exit(self_launch(args.gpus, share_gpus=args.comm == "host"))
 
     import numpy as np
     import torch
@@ -299,6 +302,8 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
+    if args.comm == "host":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.dist
@@ -316,7 +321,10 @@ def main():
         os.environ.setdefault("NCCL_ALGO", "Ring")
         os.environ.setdefault("NCCL_PROTO", "Simple")
         if world > 1:
-            dist.init_process_group("nccl", device_id=dev)
+            if args.comm == "host":
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=dev)
         else:  # --dist at N=1: exercise the row-sharded path with a 1-rank NCCL group
             import socket
             sk = socket.socket()
@@ -346,7 +354,9 @@ def main():
         # allreduce of the Grams and of the n x l partials (dist.py)
         from paper_1502_05366_b200 import dist as D
 
-        comm = D.NcclComm(eng)  # the C++ driver's own NCCL communicator
+        # the C++ driver's own NCCL communicator (or, --comm host, its
+        # host-staged collectives over the gloo group with a GPU token)
+        comm = D.HostComm(eng, share_gpu=True) if args.comm == "host" else D.NcclComm(eng)
         bounds = np.linspace(0, m, world + 1).astype(int)
         row0, m_loc = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
         Ad, sig_true = D.gen_test_matrix_rowsharded(comm, n, row0, m_loc, m,
@@ -380,8 +390,9 @@ def main():
     eng.profile(False)
     clk = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
+    rdev = dev if (use_dist and args.comm == "nccl") else torch.device("cpu")  # collective tensors
     if use_dist:
-        t = torch.tensor([ms_total], device=dev)
+        t = torch.tensor([ms_total], device=rdev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -408,7 +419,7 @@ def main():
         U, S, V = out["U"].t, out["S"].t[:k], out["V"].t
         e_loc = eng.device_rel_error(A.data_ptr(), m_loc, n, U.data_ptr(), S.data_ptr(), V.data_ptr(), k)
         a2 = float(torch.sum(A ** 2))
-        tt = torch.tensor([e_loc ** 2 * a2, a2], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e_loc ** 2 * a2, a2], dtype=torch.float64, device=rdev)
         torch.distributed.all_reduce(tt)
         err = float(torch.sqrt(tt[0] / tt[1]))
     sig = S.cpu().numpy()
@@ -426,7 +437,10 @@ def main():
                    "omega": "philox (materialised per call, n x l)", "l2": "A (32 GB) >> L2; no flush needed",
                    "parallelism": "1 GPU" if not use_dist else
                    f"A row-sharded over {world} GPUs ({m_loc} rows/rank), C++ driver "
-                   "(rlra_rsvd_rowsharded) with NCCL allreduce of Grams and n x l partials"},
+                   "(rlra_rsvd_rowsharded) with NCCL allreduce of Grams and n x l partials"
+                   if args.comm == "nccl" else
+                   f"FUNCTIONAL TEST, not a timing: {world} ranks sharing GPUs through host-staged "
+                   "collectives over gloo with a GPU token (rlra_comm_create_host)"},
         "time_s": ms_step / 1e3,
         "frac_of_fp64_peak": value / world / FP64_DMMA_PEAK_TFLOPS,
         "phases_ms": {k_: round(v_, 3) for k_, v_ in sorted(phases.items())},
@@ -476,12 +490,19 @@ def main():
         estep(SEED_OMEGA)
         if use_dist:
             torch.distributed.barrier()
-        t0 = time.perf_counter()
+        torch.cuda.synchronize()
+        # CUDA events on the engine stream bracket the calls (each call is
+        # synchronous: H2D, compute, D2H all inside); max over the ranks
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for i in range(e2e_steps):
             estep(SEED_OMEGA + 200 + i)
-        te = (time.perf_counter() - t0) / e2e_steps
+        e1.record(stream)
+        e1.synchronize()
+        te = e0.elapsed_time(e1) * 1e-3 / e2e_steps
         if use_dist:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            tt = torch.tensor([te], dtype=torch.float64, device=rdev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
         line["e2e"] = {"value": F / te / 1e12, "unit": "TFLOP/s",

@@ -1,3 +1,3 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_algorithms.py tests/test_gpu_io.py tests/test_gpu_cli.py tests/test_gpu_reftests.py -q -x -p no:cacheprovider > gpurun_out/t7.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/t7.log
-python tools/e2e_pageable_c5.py > gpurun_out/e2e_pageable.json 2>&1; cat gpurun_out/e2e_pageable.json
+timeout 900 python bench.py --gpus 2 --comm host --steps 2 --warmup 1 --no-cpu > gpurun_out/b2h.json 2> gpurun_out/b2h.err; echo "rc=$?"; cat gpurun_out/b2h.json; grep -v "^NCCL\|INFO" gpurun_out/b2h.err | tail -5
+timeout 900 python bench.py --gpus 4 --comm host --m 40000 --steps 2 --warmup 1 --no-cpu > gpurun_out/b4h.json 2> gpurun_out/b4h.err; echo "rc=$?"; cat gpurun_out/b4h.json; tail -5 gpurun_out/b4h.err
