@@ -393,3 +393,28 @@ def test_chol_inv_flags_rank_deficiency(eng):
     assert not ok
     _, _, ok = eng.chol_inv(-np.eye(4), 0.0)  # non-positive pivot
     assert not ok
+
+
+def test_upper_tri_solve_k_beyond_the_old_shared_memory_bound(eng):
+    """k = 30000 > the round-1 kernel's ~29k shared-memory cap:
+    the blocked solve has no bound on k.  Device buffers through the C-ABI;
+    S11 = diag(1..2) + a small strictly upper part, X known, S12 = S11 X."""
+    import ctypes as C
+
+    import torch
+
+    k, nc = 30000, 16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    S = torch.triu(torch.randn(k, k, device="cuda", dtype=torch.float64, generator=g), 1) * (0.3 / k ** 0.5)
+    S += torch.diag(torch.linspace(1.0, 2.0, k, device="cuda", dtype=torch.float64))
+    X = torch.randn(k, nc, device="cuda", dtype=torch.float64, generator=g)
+    B = S @ X
+    S_c, B_c = S.t().contiguous(), B.t().contiguous()  # column-major storage
+    T = torch.empty(nc, k, device="cuda", dtype=torch.float64)
+    cl = C.c_int(0)
+    st = R.lib().rlra_upper_tri_solve(eng._ctx, R.DEVICE, C.c_void_p(S_c.data_ptr()), k, C.c_int64(k),
+                                      C.c_void_p(B_c.data_ptr()), nc, C.c_int64(k), C.c_void_p(T.data_ptr()),
+                                      C.c_int64(k), C.byref(cl))
+    assert st == 0, R.lib().rlra_last_error()
+    err = torch.linalg.norm(T.t() - X) / torch.linalg.norm(X)
+    assert float(err) <= 1e-12 and cl.value == 0
