@@ -411,6 +411,7 @@ def test_upper_tri_solve_k_beyond_the_old_shared_memory_bound(eng):
     B = S @ X
     S_c, B_c = S.t().contiguous(), B.t().contiguous()  # column-major storage
     T = torch.empty(nc, k, device="cuda", dtype=torch.float64)
+    torch.cuda.synchronize()  # the engine runs on its own stream
     cl = C.c_int(0)
     st = R.lib().rlra_upper_tri_solve(eng._ctx, R.DEVICE, C.c_void_p(S_c.data_ptr()), k, C.c_int64(k),
                                       C.c_void_p(B_c.data_ptr()), nc, C.c_int64(k), C.c_void_p(T.data_ptr()),
