@@ -197,51 +197,26 @@ __global__ void __launch_bounds__(256) householder_coop_kernel(HhArgs a) {
 // form_q (reference core/qr.hpp:82-89): Q = H_0 ... H_{r-1} [I_r; 0], the
 // reflectors (columns of V, scalars beta) applied in reverse order.  Rows are
 // partitioned over CTAs; two grid barriers per reflector.
-struct FormQArgs {
-    unsigned* bar;  // grid_sync state (Context::gbar)
-    const double* V;
-    int64_t ldv;
-    const double* beta;
-    int m, r;
-    double* part;  // G x r
-    double* dots;  // r
-    double* Q;
-    int64_t ldq;
-};
-
-__global__ void __launch_bounds__(256) formq_coop_kernel(FormQArgs a) {
-    const int G = gridDim.x, g = blockIdx.x;
-    const int rows_per = (a.m + G - 1) / G;
-    const int r0 = g * rows_per, r1 = min(a.m, r0 + rows_per);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    const int n = a.r;
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-        for (int j = 0; j < n; ++j) a.Q[i + int64_t(j) * a.ldq] = (i == j) ? 1.0 : 0.0;
+// T (nb x nb upper) of the compact WY form H_0 ... H_{nb-1} = I - V T V^T
+// (Schreiber-Van Loan): T_jj = beta_j, T(0:j, j) = -beta_j T(0:j, 0:j) S(0:j, j)
+// with S = V^T V.  One CTA; a zero beta (a skipped, numerically zero column)
+// gives a zero row and column, i.e. that H is the identity.
+__global__ void formq_t_kernel(const double* S, int64_t lds, const double* beta, int nb, double* T, int64_t ldt) {
+    extern __shared__ double ts[];  // nb x nb, column-major
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) ts[e] = 0.0;
     __syncthreads();
-    for (int k = n - 1; k >= 0; --k) {
-        const double beta = a.beta[k];
-        if (beta == 0.0) continue;  // uniform across CTAs
-        for (int j = k + warp; j < n; j += nwarps) {
-            double s = 0.0;
-            for (int i = max(r0, k) + lane; i < r1; i += 32)
-                s += a.V[i + int64_t(k) * a.ldv] * a.Q[i + int64_t(j) * a.ldq];
-            s = warp_sum(s);
-            if (lane == 0) a.part[int64_t(g) * n + j] = s;
+    for (int j = 0; j < nb; ++j) {
+        const double bj = beta[j];
+        // row i of column j: -beta_j * sum_{p=i}^{j-1} T(i, p) S(p, j)
+        for (int i = threadIdx.x; i < j; i += blockDim.x) {
+            double acc = 0.0;
+            for (int p = i; p < j; ++p) acc += ts[i + p * nb] * S[p + int64_t(j) * lds];
+            ts[i + j * nb] = -bj * acc;
         }
-        grid_sync(a.bar);
-        for (int j = k + g * blockDim.x + threadIdx.x; j < n; j += G * blockDim.x) {
-            double s = 0.0;
-            for (int c = 0; c < G; ++c) s += a.part[int64_t(c) * n + j];
-            a.dots[j] = s;
-        }
-        grid_sync(a.bar);
-        for (int j = k; j < n; ++j) {
-            const double f = beta * a.dots[j];
-            for (int i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x)
-                a.Q[i + int64_t(j) * a.ldq] -= f * a.V[i + int64_t(k) * a.ldv];
-        }
+        if (threadIdx.x == 0) ts[j + j * nb] = bj;
         __syncthreads();
     }
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e % nb + int64_t(e / nb) * ldt] = ts[e];
 }
 
 // R = W(0:n, 0:n) upper; sign fix diag(R) >= 0 (core/qr.hpp:113-119).
@@ -263,27 +238,31 @@ __global__ void hh_finish_kernel(const double* W, int64_t ldw, int m, int n, dou
 
 void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int m, int r,
             const DMat& Q) {
+    // Q = H_0 ... H_{r-1} [I_r; 0] (core/qr.hpp:82-89) applied blockwise from the
+    // last block of kFqNB reflectors to the first, each block in compact WY
+    // form on the DMMA GEMM: Q[b0:, b0:] -= V_b (T_b (V_b^T Q[b0:, b0:])).
+    // Columns < b0 and rows < b0 of those columns are untouched by reflectors
+    // >= b0 (v_k is zero above row k).  Same product as the reference's
+    // reflector-by-reflector loop; the rounding order differs.
     if (r == 0) return;
-    int G = std::max(1, std::min(ctx.num_sms, m / 256));
-    int per_sm = 0;
-    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, formq_coop_kernel, 256, 0));
-    G = std::min(G, std::max(1, per_sm) * ctx.num_sms);
-    Buf part(ctx, sizeof(double) * size_t(G) * r), dots(ctx, sizeof(double) * r);
-    FormQArgs a;
-    a.V = V;
-    a.ldv = ldv;
-    a.beta = beta;
-    a.m = m;
-    a.r = r;
-    a.part = part.d();
-    a.dots = dots.d();
-    a.Q = Q.p;
-    a.ldq = Q.ld;
-    a.bar = ctx.gbar;
-    void* args[] = {&a};
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)formq_coop_kernel, dim3(G), dim3(256), args, 0,
-                                          ctx.stream));
-    ++ctx.launches;
+    constexpr int kFqNB = 64;
+    eye_mat(ctx, Q);
+    const DMat Vm{const_cast<double*>(V), m, r, ldv};
+    DMatBuf S(ctx, kFqNB, kFqNB), T(ctx, kFqNB, kFqNB), Wb(ctx, kFqNB, r), W2(ctx, kFqNB, r);
+    for (int b0 = ((r - 1) / kFqNB) * kFqNB; b0 >= 0; b0 -= kFqNB) {
+        const int nb = std::min(kFqNB, r - b0), rows = m - b0, cols = r - b0;
+        const DMat Vb = Vm.block(b0, b0, rows, nb);
+        const DMat Qs = Q.block(b0, b0, rows, cols);
+        const DMat Sb = S.m.block(0, 0, nb, nb), Tb = T.m.block(0, 0, nb, nb);
+        const DMat W1 = Wb.m.block(0, 0, nb, cols), W2b = W2.m.block(0, 0, nb, cols);
+        gemm(ctx, Op::T, Op::N, 1.0, Vb, Vb, 0.0, Sb);
+        formq_t_kernel<<<1, 256, sizeof(double) * nb * nb, ctx.stream>>>(Sb.p, Sb.ld, beta + b0, nb, Tb.p, Tb.ld);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        gemm(ctx, Op::T, Op::N, 1.0, Vb, Qs, 0.0, W1);
+        gemm(ctx, Op::N, Op::N, 1.0, Tb, W1, 0.0, W2b);
+        gemm(ctx, Op::N, Op::N, -1.0, Vb, W2b, 1.0, Qs);
+    }
 }
 
 namespace {
@@ -635,37 +614,62 @@ bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor)
 }
 
 QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R) {
+    // Blocked Householder QR (the reference's compact_qr, core/qr.hpp:95-121):
+    // panels of kHhNB columns factored by the cooperative reflector kernel
+    // (reference rules: zero-column floor 1e-300, beta = 0, propagated unit
+    // vectors), the trailing columns updated once per panel in compact WY form
+    // on the DMMA GEMM, W_tr -= V_p (T_p^T (V_p^T W_tr)) — the same product of
+    // reflectors as applying them one by one, in a different rounding order.
     const int m = int(Y.rows), n = int(Y.cols);
     QrResult res;
     res.used_householder = true;
     if (n == 0) return res;
-    int G = std::max(1, std::min(ctx.num_sms, m / 256));
-    {
-        int per_sm = 0;
-        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, householder_coop_kernel,
-                                                                256, 0));
-        G = std::min(G, std::max(1, per_sm) * ctx.num_sms);
-    }
-    DMatBuf W(ctx, m, n), V(ctx, m, n);
+    constexpr int kHhNB = 32;
+    int per_sm = 0;
+    RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, householder_coop_kernel, 256, 0));
+    const int gcap = std::max(1, per_sm) * ctx.num_sms;
+    DMatBuf W(ctx, m, n), V(ctx, m, n), Vp(ctx, m, kHhNB), S(ctx, kHhNB, kHhNB), T(ctx, kHhNB, kHhNB);
     copy_mat(ctx, Y, W);
-    Buf beta(ctx, sizeof(double) * n), part(ctx, sizeof(double) * (size_t(G) + size_t(G) * n)),
-        dots(ctx, sizeof(double) * n), deg(ctx, sizeof(int));
+    zero_mat(ctx, V);
+    const int Gmax = std::max(1, std::min({ctx.num_sms, m / 256, gcap}));
+    Buf beta(ctx, sizeof(double) * n), part(ctx, sizeof(double) * (size_t(Gmax) + size_t(Gmax) * kHhNB)),
+        dots(ctx, sizeof(double) * kHhNB), deg(ctx, sizeof(int));
     RLRA_CUDA(cudaMemsetAsync(deg.p, 0, sizeof(int), ctx.stream));
-    HhArgs a;
-    a.W = W.m.p;
-    a.ldw = W.m.ld;
-    a.m = m;
-    a.n = n;
-    a.V = V.m.p;
-    a.beta = beta.d();
-    a.part = part.d();
-    a.dots = dots.d();
-    a.degenerate = deg.i();
-    a.bar = ctx.gbar;
-    void* args[] = {&a};
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)householder_coop_kernel, dim3(G), dim3(256), args, 0,
-                                          ctx.stream));
-    ++ctx.launches;
+    for (int j0 = 0; j0 < n; j0 += kHhNB) {
+        const int nb = std::min(kHhNB, n - j0), rows = m - j0, ntr = n - j0 - nb;
+        const DMat panel = W.m.block(j0, j0, rows, nb);
+        HhArgs a;
+        a.W = panel.p;
+        a.ldw = panel.ld;
+        a.m = rows;
+        a.n = nb;
+        a.V = Vp.m.p;  // rows x nb, ld rows
+        a.beta = beta.d() + j0;
+        a.part = part.d();
+        a.dots = dots.d();
+        a.degenerate = deg.i();
+        a.bar = ctx.gbar;
+        void* args[] = {&a};
+        const int G = std::max(1, std::min(Gmax, rows / 256));
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)householder_coop_kernel, dim3(G), dim3(256), args, 0,
+                                              ctx.stream));
+        ++ctx.launches;
+        const DMat Vpb{Vp.m.p, rows, nb, std::max(rows, 1)};
+        copy_mat(ctx, Vpb, V.m.block(j0, j0, rows, nb));
+        if (ntr > 0) {
+            const DMat Sb = S.m.block(0, 0, nb, nb), Tb = T.m.block(0, 0, nb, nb);
+            gemm(ctx, Op::T, Op::N, 1.0, Vpb, Vpb, 0.0, Sb);
+            formq_t_kernel<<<1, 256, sizeof(double) * nb * nb, ctx.stream>>>(Sb.p, Sb.ld, beta.d() + j0, nb, Tb.p,
+                                                                            Tb.ld);
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+            const DMat Wt = W.m.block(j0, j0 + nb, rows, ntr);
+            DMatBuf X1(ctx, nb, ntr), X2(ctx, nb, ntr);
+            gemm(ctx, Op::T, Op::N, 1.0, Vpb, Wt, 0.0, X1.m);
+            gemm(ctx, Op::T, Op::N, 1.0, Tb, X1.m, 0.0, X2.m);
+            gemm(ctx, Op::N, Op::N, -1.0, Vpb, X2.m, 1.0, Wt);
+        }
+    }
     form_q(ctx, V.m.p, V.m.ld, beta.d(), m, n, Y);
     const int blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, int64_t(ctx.num_sms) * 8));
     hh_finish_kernel<<<blocks, 256, 0, ctx.stream>>>(W.m.p, W.m.ld, m, n, Y.p, Y.ld,
