@@ -543,8 +543,8 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
             // rsvd_v1/v2 with power steps: A^T Y is summed under the upload too
             const bool zt = variant != RLRA_RSVD_BASIC && q > 0 && m >= k + p;
             DMatBuf Zt(C, zt ? n : 0, zt ? k + p : 0);
-            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, zt ? &Zt.m : nullptr);
-            rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m, zt ? &Zt.m : nullptr);
+            const bool have_zt = upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, zt ? &Zt.m : nullptr);
+            rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m, have_zt ? &Zt.m : nullptr);
         } else {
             In A(C, loc, a, m, n, lda, "a");
             rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
@@ -947,7 +947,11 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
             need(a, "a");
             check_ld(lda, m_local, "a");
             DMatBuf dA(C, m_local, n), Y(C, m_local, k + p), Zt(C, q > 0 ? n : 0, q > 0 ? k + p : 0);
-            upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, q > 0 ? &Zt.m : nullptr);
+            // every rank takes the same branch: the Z shortcut needs all shards'
+            // partial sums (a rank whose shard is one chunk sums after its upload)
+            if (q > 0 && !upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, &Zt.m))
+                gemm(C, Op::T, Op::N, 1.0, dA.m, Y.m, 0.0, Zt.m);
+            if (q == 0) upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, nullptr);
             rsvd_v2_rowsharded(C, comm->c, dA.m, m_total, k, p, q, s, om, U.m, S.d, V.m, &Y.m,
                                q > 0 ? &Zt.m : nullptr);
         } else {

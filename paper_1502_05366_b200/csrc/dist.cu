@@ -512,7 +512,7 @@ void rsvd_v2_rowsharded(Context& ctx, Comm& cm, const DMat& A, int64_t m_total, 
                 // A_g^T Y_g were summed under the shard's upload)
                 DMatBuf G(ctx, l, l), Ri(ctx, l, l);
                 gram_allreduce(ctx, cm, Y, G.m);
-                if (chol_upper_inv(ctx, G.m, Ri.m, ctx.cholqr_pivot_floor)) {
+                if (chol_upper_inv(ctx, G.m, Ri.m, 1e-8)) {  // well-conditioned Y only (engine.cu)
                     copy_mat(ctx, *zpre, Z.m);
                     allreduce_mat(ctx, cm, Z.m);
                     DMatBuf T(ctx, n, l);

@@ -203,8 +203,12 @@ void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource&
             // asks for: the span the reference's orth(Y) then A^T Q produce,
             // without streaming A a second time (A^T Y was summed under the
             // upload).  Rounding differs from A^T (Y R^{-1}) by ~u kappa(Y).
+            // Only for a well-conditioned Y (every Cholesky pivot >= 1e-8 of its
+            // diagonal, i.e. kappa(Y) below ~1e4): the reordering costs
+            // ~u kappa(Y) in Z, kept at the 1e-12 level (C5: sigma within
+            // 2.4e-14 of the device-resident order).
             DMatBuf Ri(ctx, l, l);
-            if (span_rinv(ctx, Y, Ri.m)) {
+            if (span_rinv(ctx, Y, Ri.m, 1e-8)) {
                 GemmOpts tri;
                 tri.tri_b_upper = true;
                 gemm(ctx, Op::N, Op::N, 1.0, *zpre, Ri.m, 0.0, Z.m, tri);
@@ -242,12 +246,12 @@ void sample_left_t(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource
     }
 }
 
-void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
+bool upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
                        const DMat& Y, const DMat* Zt) {
     const int64_t m = dA.rows, n = dA.cols;
     if (m <= 0 || n <= 0) {
         if (Zt) zero_mat(ctx, *Zt);
-        return;
+        return Zt != nullptr;
     }
     if (!ctx.copy_stream) RLRA_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
     // Omega once (callback mode: the reference's draw, uploaded; Philox: philox_fill)
@@ -295,7 +299,7 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
         } else {
             gemm(ctx, Op::N, Op::N, 1.0, Ar, Om.m, 0.0, Yr);
         }
-        if (Zt) {  // Zt += A_c^T Y_c, chunks summed in order (deterministic)
+        if (Zt && nchunk > 1) {  // Zt += A_c^T Y_c, chunks summed in order (deterministic)
             GemmTag zt(ctx, "gemm_power");
             gemm(ctx, Op::T, Op::N, 1.0, Ar, Yr, r0 == 0 ? 0.0 : 1.0, *Zt);
         }
@@ -303,6 +307,7 @@ void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));  // h (callback Omega) outlives its copy; events done
     for (auto e : ev) cudaEventDestroy(e);
     cudaEventDestroy(ready);
+    return Zt && nchunk > 1;
 }
 
 void rsvd(Context& ctx, int variant, const DMat& A, int k, int p, int q, int s, OmegaSource& om,

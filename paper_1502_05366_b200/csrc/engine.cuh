@@ -29,10 +29,11 @@ void sample_right(Context& ctx, const DMat& A, int l, int q, int s, OmegaSource&
 // context's copy stream and compute the sketch Y = A Omega chunk by chunk as
 // the rows land (the chunk GEMMs are the unchunked GEMM's tiles, so Y is
 // bit-identical); consumes one Omega draw.
-// With Zt (n x l) non-null, also Zt = A^T Y accumulated chunk by chunk
-// (sum over the row chunks in order, under the upload): the first power
-// product of rsvd (sample_right's zpre).
-void upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
+// With Zt (n x l) non-null and A large enough to upload in chunks, also
+// Zt = A^T Y accumulated chunk by chunk (sum over the row chunks in order,
+// under the upload): the first power product of rsvd (sample_right's zpre).
+// Returns whether Zt was filled.
+bool upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& dA, int l, OmegaSource& om,
                        const DMat& Y, const DMat* Zt = nullptr);
 // sketch.hpp:65-67 — returns Y^T (n x l) of the reference's l x n sample,
 // computed on A directly (the reference materialises A^T; we never do).

@@ -69,7 +69,10 @@ private:
 };
 
 constexpr int kSlots = 4;
-constexpr size_t kSlotBytes = size_t(64) << 20;  // 64 MB pinned per slot
+constexpr size_t kSlotBytes = size_t(16) << 20;  // 16 MB pinned per slot (one-time pinning stays ~20 ms)
+// below this a pageable copy goes straight to the driver: the one-time cost of
+// the pool and the pinned slots would not pay for itself
+constexpr size_t kStageMin = size_t(64) << 20;
 
 struct Stager {
     Pool pool;
@@ -124,7 +127,7 @@ void h2d_copy(Context& ctx, cudaStream_t st, const double* h, int64_t ldh, const
     const int64_t rows = d.rows, cols = d.cols;
     if (rows <= 0 || cols <= 0) return;
     const size_t colb = sizeof(double) * size_t(rows);
-    if (host_is_pinned(h) || colb * size_t(cols) < (size_t(8) << 20) || colb > kSlotBytes) {
+    if (host_is_pinned(h) || colb * size_t(cols) < kStageMin || colb > kSlotBytes) {
         RLRA_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double) * d.ld, h, sizeof(double) * ldh, colb, cols,
                                     cudaMemcpyHostToDevice, st));
         return;
@@ -151,7 +154,7 @@ void d2h_copy(Context& ctx, const DMat& d, double* h, int64_t ldh) {
     const int64_t rows = d.rows, cols = d.cols;
     if (rows <= 0 || cols <= 0) return;
     const size_t colb = sizeof(double) * size_t(rows);
-    if (host_is_pinned(h) || colb * size_t(cols) < (size_t(8) << 20) || colb > kSlotBytes) {
+    if (host_is_pinned(h) || colb * size_t(cols) < kStageMin || colb > kSlotBytes) {
         RLRA_CUDA(cudaMemcpy2DAsync(h, sizeof(double) * ldh, d.p, sizeof(double) * d.ld, colb, cols,
                                     cudaMemcpyDeviceToHost, ctx.stream));
         RLRA_CUDA(cudaStreamSynchronize(ctx.stream));

@@ -779,7 +779,7 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
     return res;
 }
 
-bool span_rinv(Context& ctx, const DMat& Y, const DMat& Rinv) {
+bool span_rinv(Context& ctx, const DMat& Y, const DMat& Rinv, double floor) {
     const int m = int(Y.rows), n = int(Y.cols);
     if (m < n || n == 0) return false;
     ProfScope prof(ctx, "orth", m, n, 1, 0.0);
@@ -788,7 +788,7 @@ bool span_rinv(Context& ctx, const DMat& Y, const DMat& Rinv) {
     GemmOpts sy;
     sy.upper_tiles_only = true;
     gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G1, sy);
-    return chol_upper_inv(ctx, G1, Rinv, ctx.cholqr_pivot_floor);
+    return chol_upper_inv(ctx, G1, Rinv, floor);
 }
 
 bool orth_span_into(Context& ctx, const DMat& Y, const DMat& out) {

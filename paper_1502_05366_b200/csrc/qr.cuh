@@ -36,9 +36,10 @@ QrResult orth_span_inplace(Context& ctx, const DMat& Y);
 // for a single pass — the caller then orthonormalises Y in place.
 bool orth_span_into(Context& ctx, const DMat& Y, const DMat& out);
 
-// R^{-1} of one CholQR pass of Y (G = Y^T Y, Cholesky): false when the Gram
-// is too ill-conditioned (the caller then takes the orth_span_inplace path).
-bool span_rinv(Context& ctx, const DMat& Y, const DMat& Rinv);
+// R^{-1} of one CholQR pass of Y (G = Y^T Y, Cholesky): false when a pivot
+// falls below floor times its original diagonal (the caller then takes the
+// orth_span_inplace path).
+bool span_rinv(Context& ctx, const DMat& Y, const DMat& Rinv, double floor);
 
 // Always the Householder path (used for the fallback and for tests).
 QrResult householder_qr(Context& ctx, const DMat& Y, const DMat* R);

@@ -356,11 +356,11 @@ def test_qb_hierarchical_vs_reference(eng, nrb):
 def test_pageable_host_buffers_staged_bit_identical_to_pinned(eng):
     """A reference user's DenseMatrix is pageable memory: the C-ABI stages it
     through pinned slots with a pool of copy threads (csrc/hostio.cu) in both
-    directions.  Results equal the pinned-buffer call bit for bit (48 MB A:
-    over the staging threshold; U 16 MB comes back staged too)."""
+    directions.  Results equal the pinned-buffer call bit for bit (240 MB A
+    and the 80 MB U: both over the 64 MiB staging threshold)."""
     import torch
 
-    m, n, k, p, q = 4000, 1500, 500, 10, 2
+    m, n, k, p, q = 20000, 1500, 500, 10, 2
     a = make_test_matrix(m, n, np.exp(-np.arange(1500) / 80.0), seed=71)
     outs = []
     for pinned in (True, False):

@@ -1,3 +1,4 @@
 set -x
-timeout 900 python bench.py --gpus 2 --comm host --steps 2 --warmup 1 --no-cpu > gpurun_out/b2h.json 2> gpurun_out/b2h.err; echo "rc=$?"; cat gpurun_out/b2h.json; grep -v "^NCCL\|INFO" gpurun_out/b2h.err | tail -5
-timeout 900 python bench.py --gpus 4 --comm host --m 40000 --steps 2 --warmup 1 --no-cpu > gpurun_out/b4h.json 2> gpurun_out/b4h.err; echo "rc=$?"; cat gpurun_out/b4h.json; tail -5 gpurun_out/b4h.err
+python tools/parity_full.py C1 > gpurun_out/par_c1_r2c.jsonl 2>&1; cat gpurun_out/par_c1_r2c.jsonl
+python tools/e2e_pageable_c5.py > gpurun_out/e2e_pageable2.json 2>&1; cat gpurun_out/e2e_pageable2.json
+timeout 600 python -m pytest tests/test_gpu_algorithms.py -q -p no:cacheprovider -k "pageable or rsvd" > gpurun_out/t10.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/t10.log
