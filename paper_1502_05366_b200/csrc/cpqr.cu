@@ -54,6 +54,9 @@ struct CpqrArgs {
     int* out;  // [0] frank, [1] reached, [2] degenerate
     double* res;
     long long* phase_clk;  // optional: CTA 0's clock64 per step phase (RLRA_CPQR_PHASES)
+    // cpqr_res_kernel only
+    int* slot_s;       // 2 x G candidate storage columns
+    double* slot_col;  // 2 x G x m candidate column data
 };
 
 __global__ void __launch_bounds__(kCpqrThreads) cpqr_coop_kernel(CpqrArgs a) {
@@ -568,6 +571,440 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
     }
 }
 
+// ------------------------------------------- resident columns (m <= 768) ---
+// cpqr_step_kernel with every CTA's columns held ON CHIP for the whole
+// factorization instead of re-read and re-written through L2 each step: two
+// columns per warp in registers (row i at lane i % 32, slot i / 32) and the
+// rest in shared memory.  The pivot column reaches the other CTAs through a
+// per-CTA candidate slot: after its apply each CTA publishes its best
+// candidate's value, position and storage index AND the column itself
+// (slot_col), so after the step's one grid barrier every CTA forms H_f from
+// the winner's published copy.  Positions live with the columns (no n-sized
+// maps): the column at position f takes the pivot's old position, the pivot
+// takes f.  Same reflector, downdate and tie-break rules as the other CPQR
+// kernels (core/qr.hpp:140-236); only the summation order of the column dot
+// products differs (fixed rows per lane).
+constexpr int kResRegCols = 4;  // register-resident columns per warp
+constexpr int kResRows = 20;    // rows per lane (m <= 640)
+constexpr int kResThreads = 256;  // 8 warps: 4 x 20 + 20 doubles of registers per lane
+
+__global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
+    extern __shared__ double rsm[];
+    const int m = a.m, n = a.n;
+    const int G = gridDim.x, g = blockIdx.x, t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    const int cpb = (n + G - 1) / G;
+    const int j0 = g * cpb, j1 = min(n, j0 + cpb), nown = max(0, j1 - j0);
+    const int nreg = kResRegCols * nw;  // local columns [0, nreg) in registers
+    double* vsh = rsm;                   // m: H_f's vector
+    double* cnS = vsh + m;               // cpb
+    double* rnS = cnS + cpb;             // cpb
+    double* colS = rnS + cpb;            // (cpb - nreg) x m shared-memory columns
+    int* posS = reinterpret_cast<int*>(colS + size_t(max(0, cpb - nreg)) * m);  // cpb positions
+    __shared__ double sv[32], st[32], shb[32];
+    __shared__ int sp[32], ss[32];
+    __shared__ int s_piv, s_spv, s_win, s_best_c;
+    double xr[kResRegCols][kResRows];  // this warp's register columns
+    auto lc_of = [&](int b) { return warp * kResRegCols + b; };  // local index of register column b
+    const bool clk = a.phase_clk != nullptr && g == 0 && t == 0;
+    long long ph[5] = {0, 0, 0, 0, 0}, c0 = clock64();
+    auto mark = [&](int i) {
+        if (clk) {
+            const long long c1 = clock64();
+            ph[i] += c1 - c0;
+            c0 = c1;
+        }
+    };
+    // ---- load the owned columns, initial positions
+#pragma unroll
+    for (int b = 0; b < kResRegCols; ++b) {
+        const int c = lc_of(b);
+#pragma unroll
+        for (int u = 0; u < kResRows; ++u) {
+            const int i = lane + 32 * u;
+            xr[b][u] = (c < nown && i < m) ? a.W[i + int64_t(j0 + c) * a.ldw] : 0.0;
+        }
+    }
+    for (int c = nreg; c < nown; ++c)
+        for (int i = t; i < m; i += blockDim.x) colS[size_t(c - nreg) * m + i] = a.W[i + int64_t(j0 + c) * a.ldw];
+    for (int c = t; c < cpb; c += blockDim.x) posS[c] = j0 + c;
+    __syncthreads();
+
+    int par = 0;
+    // CTA best (value desc, position asc) over the warps' bests, the slot
+    // record, then the winning column's data into slot_col[par][g]
+    auto publish = [&](double bv, int bp, int bc, double tr) {
+        if (lane == 0) {
+            sv[warp] = bv;
+            sp[warp] = bp;
+            ss[warp] = bc;
+            st[warp] = tr;
+        }
+        __syncthreads();
+        if (t == 0) {
+            double v = -DBL_MAX, tt = 0.0;
+            int p = INT_MAX, c = -1;
+            for (int w = 0; w < nw; ++w) {
+                if (better(sv[w], sp[w], v, p)) {
+                    v = sv[w];
+                    p = sp[w];
+                    c = ss[w];
+                }
+                tt += st[w];
+            }
+            a.slot_v[par * G + g] = v;
+            a.slot_p[par * G + g] = p;
+            a.slot_s[par * G + g] = c >= 0 ? j0 + c : -1;
+            a.slot_t[par * G + g] = tt;
+            s_best_c = c;
+        }
+        __syncthreads();
+        const int c = s_best_c;
+        double* dst = a.slot_col + (size_t(par) * G + g) * m;
+        if (c >= 0 && c < nreg) {
+            if (warp == c / kResRegCols) {
+#pragma unroll
+                for (int b = 0; b < kResRegCols; ++b)
+                    if (c == lc_of(b)) {
+#pragma unroll
+                        for (int u = 0; u < kResRows; ++u)
+                            if (lane + 32 * u < m) __stcg(dst + lane + 32 * u, xr[b][u]);
+                    }
+            }
+        } else if (c >= nreg) {
+            for (int i = t; i < m; i += blockDim.x) __stcg(dst + i, colS[size_t(c - nreg) * m + i]);
+        }
+    };
+
+    // ---- squared norms (core/qr.hpp:157-161), fixed rows per lane
+    {
+        double bv = -DBL_MAX, tr = 0.0;
+        int bp = INT_MAX, bc = -1;
+        for (int c = nreg + warp; c < nown; c += nw) {  // shared-memory columns
+            double sum = 0.0;
+            for (int u = 0; u < kResRows; ++u) {
+                const int i = lane + 32 * u;
+                if (i < m) {
+                    const double x = colS[size_t(c - nreg) * m + i];
+                    sum += x * x;
+                }
+            }
+            sum = warp_sum(sum);
+            if (lane == 0) {
+                cnS[c] = sum;
+                rnS[c] = sum;
+            }
+            if (better(sum, j0 + c, bv, bp)) {
+                bv = sum;
+                bp = j0 + c;
+                bc = c;
+            }
+            tr += sum;
+        }
+#pragma unroll
+        for (int b = 0; b < kResRegCols; ++b) {
+            const int c = lc_of(b);
+            double sum = 0.0;
+#pragma unroll
+            for (int u = 0; u < kResRows; ++u) sum += xr[b][u] * xr[b][u];
+            sum = warp_sum(sum);
+            if (c < nown) {
+                if (lane == 0) {
+                    cnS[c] = sum;
+                    rnS[c] = sum;
+                }
+                if (better(sum, j0 + c, bv, bp)) {
+                    bv = sum;
+                    bp = j0 + c;
+                    bc = c;
+                }
+                tr += sum;
+            }
+        }
+        publish(bv, bp, bc, tr);
+    }
+    grid_sync(a.bar);
+
+    int frank = 0;
+    bool reached = false;
+    if (a.tol_mode) {
+        double tt = 0.0;
+        for (int c = 0; c < G; ++c) tt += a.slot_t[c];
+        const double r = sqrt(tt);
+        reached = r <= a.tol;
+        if (g == 0 && t == 0) *a.res = r;
+    }
+    int pend_c = -1, pend_f = 0;  // own pivot column whose rows pend_f.. become (alpha, 0, ...)
+    double pend_alpha = 0.0;
+    auto finish_pending = [&]() {
+        if (pend_c < 0) return;
+        if (pend_c < nreg) {
+#pragma unroll
+            for (int b = 0; b < kResRegCols; ++b)
+                if (pend_c == lc_of(b)) {
+#pragma unroll
+                    for (int u = 0; u < kResRows; ++u) {
+                        const int i = lane + 32 * u;
+                        if (i >= pend_f) xr[b][u] = (i == pend_f) ? pend_alpha : 0.0;
+                    }
+                }
+        } else {
+            for (int i = pend_f + t; i < m; i += blockDim.x)
+                colS[size_t(pend_c - nreg) * m + i] = (i == pend_f) ? pend_alpha : 0.0;
+        }
+        pend_c = -1;
+    };
+    while (!reached && frank < a.kmax) {
+        const int f = frank;
+        finish_pending();
+        // 1. pivot (value desc, position asc) over the CTA slots
+        if (warp == 0) {
+            double v = -DBL_MAX;
+            int p = INT_MAX, c = -1;
+            for (int q = lane; q < G; q += 32)
+                if (better(a.slot_v[par * G + q], a.slot_p[par * G + q], v, p)) {
+                    v = a.slot_v[par * G + q];
+                    p = a.slot_p[par * G + q];
+                    c = q;
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+                if (better(ov, op, v, p)) {
+                    v = ov;
+                    p = op;
+                    c = oc;
+                }
+            }
+            if (lane == 0) {
+                s_piv = p;
+                s_win = c;
+                s_spv = a.slot_s[par * G + c];
+            }
+        }
+        __syncthreads();
+        const int piv = s_piv, spv = s_spv, win = s_win;
+        mark(0);
+        // 2. householder_step on the published pivot column (core/qr.hpp:44-66), in every CTA
+        const double* pc = a.slot_col + (size_t(par) * G + win) * m;
+        double sum = 0.0;
+        for (int i = f + t; i < m; i += blockDim.x) {
+            const double x = __ldcg(pc + i);
+            vsh[i] = x;
+            sum += x * x;
+        }
+        sum = warp_sum(sum);
+        if (lane == 0) shb[warp] = sum;
+        __syncthreads();
+        double norm2 = 0.0;
+        for (int w = 0; w < nw; ++w) norm2 += shb[w];
+        const double x1 = vsh[f];
+        const double norm = sqrt(norm2);
+        const bool zero = norm < 1e-300;
+        const double alpha = x1 >= 0.0 ? -norm : norm;
+        const double beta = zero ? 0.0 : 2.0 / (2.0 * (norm2 - alpha * x1));
+        __syncthreads();
+        if (zero) {
+            for (int i = f + t; i < m; i += blockDim.x) vsh[i] = 0.0;
+        } else if (t == 0) {
+            vsh[f] = x1 - alpha;
+        }
+        // the swap (core/qr.hpp:182-187), on the owned positions
+        for (int c = t; c < nown; c += blockDim.x) {
+            const int pc_ = posS[c];
+            posS[c] = (j0 + c == spv) ? f : (pc_ == f ? piv : pc_);
+        }
+        __syncthreads();
+        if (g == 0) {
+            for (int i = t; i < m; i += blockDim.x) a.Vst[i + int64_t(f) * m] = i < f ? 0.0 : vsh[i];
+            if (t == 0) {
+                a.beta[f] = beta;
+                if (zero) a.out[2] = 1;
+            }
+        }
+        mark(1);
+        par ^= 1;  // this step's candidates go to the other buffer
+        // 3. apply H_f to the own trailing columns, downdate (core/qr.hpp:190-200)
+        // v(i) for this lane's rows, zero outside [f, m)
+        double vr[kResRows];
+#pragma unroll
+        for (int u = 0; u < kResRows; ++u) {
+            const int i = lane + 32 * u;
+            vr[u] = (i >= f && i < m) ? vsh[i] : 0.0;
+        }
+        double bv = -DBL_MAX, tr = 0.0;
+        int bp = INT_MAX, bc = -1;
+        const int uf = f >> 5, lf = f & 31;
+        // the downdate (core/qr.hpp:193-200) of local column c, whose row-f
+        // entry is d and rows > f give s2 on demand; the warp's best candidate
+        auto downdate = [&](int c, int pos, double d, auto&& tail_sq) {
+            double c2 = cnS[c] - d * d;
+            const double ref = rnS[c];
+            double rr = ref;
+            if (c2 < 1e-6 * ref || a.tol_mode) {  // uniform across the warp
+                const double s2 = warp_sum(tail_sq());
+                if (c2 < 1e-6 * ref) {
+                    c2 = s2;
+                    rr = s2;
+                }
+                tr += s2;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                cnS[c] = c2;
+                rnS[c] = rr;
+            }
+            __syncwarp();
+            if (better(c2, pos, bv, bp)) {
+                bv = c2;
+                bp = pos;
+                bc = c;
+            }
+        };
+        // register columns: the warp's kResRegCols columns together (independent
+        // dot-product chains and shuffle reductions interleave)
+        {
+            bool on[kResRegCols];
+            int pos[kResRegCols];
+#pragma unroll
+            for (int b = 0; b < kResRegCols; ++b) {
+                const int c = lc_of(b);
+                pos[b] = c < nown ? posS[c] : -1;
+                on[b] = c < nown && pos[b] > f;
+            }
+            if (beta != 0.0) {
+                double sd[kResRegCols];
+#pragma unroll
+                for (int b = 0; b < kResRegCols; ++b) sd[b] = 0.0;
+#pragma unroll
+                for (int u = 0; u < kResRows; ++u)
+#pragma unroll
+                    for (int b = 0; b < kResRegCols; ++b) sd[b] += vr[u] * xr[b][u];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int b = 0; b < kResRegCols; ++b) sd[b] += __shfl_xor_sync(0xffffffffu, sd[b], o);
+#pragma unroll
+                for (int b = 0; b < kResRegCols; ++b) {
+                    const double fct = on[b] ? beta * sd[b] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < kResRows; ++u) xr[b][u] -= fct * vr[u];
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < kResRegCols; ++b) {
+                if (!on[b]) continue;
+                double xf = 0.0;
+#pragma unroll
+                for (int u = 0; u < kResRows; ++u) xf = (u == uf) ? xr[b][u] : xf;
+                const double d = __shfl_sync(0xffffffffu, xf, lf);  // row f
+                downdate(lc_of(b), pos[b], d, [&] {
+                    double s2 = 0.0;
+#pragma unroll
+                    for (int u = 0; u < kResRows; ++u) {
+                        const int i = lane + 32 * u;
+                        if (i > f && i < m) s2 += xr[b][u] * xr[b][u];
+                    }
+                    return s2;
+                });
+            }
+        }
+        // shared-memory columns, two at a time, updated in place
+        for (int c0 = nreg + warp; c0 < nown; c0 += 2 * nw) {
+            const int cc[2] = {c0, c0 + nw};
+            bool on[2];
+            int pos[2];
+            double* col[2];
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                pos[b] = cc[b] < nown ? posS[cc[b]] : -1;
+                on[b] = cc[b] < nown && pos[b] > f;
+                col[b] = colS + size_t((on[b] ? cc[b] : nreg) - nreg) * m;
+            }
+            if (!on[0] && !on[1]) continue;
+            if (beta != 0.0) {
+                double sd[2] = {0.0, 0.0};
+#pragma unroll
+                for (int u = 0; u < kResRows; ++u) {
+                    const int i = lane + 32 * u;
+                    if (i >= f && i < m) {
+#pragma unroll
+                        for (int b = 0; b < 2; ++b) sd[b] += vr[u] * col[b][i];
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) sd[b] += __shfl_xor_sync(0xffffffffu, sd[b], o);
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    if (!on[b]) continue;
+                    const double fct = beta * sd[b];
+#pragma unroll
+                    for (int u = 0; u < kResRows; ++u) {
+                        const int i = lane + 32 * u;
+                        if (i >= f && i < m) col[b][i] -= fct * vr[u];
+                    }
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                if (!on[b]) continue;
+                const double* cb = col[b];
+                downdate(cc[b], pos[b], cb[f], [&] {
+                    double s2 = 0.0;
+                    for (int i = f + 1 + lane; i < m; i += 32) s2 += cb[i] * cb[i];
+                    return s2;
+                });
+            }
+        }
+        mark(2);
+        publish(bv, bp, bc, tr);
+        mark(3);
+        if (spv >= j0 && spv < j1) {
+            pend_c = spv - j0;
+            pend_f = f;
+            pend_alpha = zero ? 0.0 : alpha;
+        }
+        ++frank;
+        grid_sync(a.bar);
+        mark(4);
+        if (a.tol_mode && frank < a.rmax) {
+            double tt = 0.0;
+            for (int c = 0; c < G; ++c) tt += a.slot_t[par * G + c];
+            const double r = sqrt(tt);
+            if (g == 0 && t == 0) *a.res = r;
+            if (r <= a.tol) reached = true;
+        }
+    }
+    finish_pending();
+    __syncthreads();
+    if (clk)
+        for (int i = 0; i < 5; ++i) a.phase_clk[i] = ph[i];
+    // write the owned columns back (storage order) and their positions
+#pragma unroll
+    for (int b = 0; b < kResRegCols; ++b) {
+        const int c = lc_of(b);
+        if (c < nown) {
+#pragma unroll
+            for (int u = 0; u < kResRows; ++u) {
+                const int i = lane + 32 * u;
+                if (i < m) a.W[i + int64_t(j0 + c) * a.ldw] = xr[b][u];
+            }
+        }
+    }
+    for (int c = nreg; c < nown; ++c)
+        for (int i = t; i < m; i += blockDim.x) a.W[i + int64_t(j0 + c) * a.ldw] = colS[size_t(c - nreg) * m + i];
+    for (int c = t; c < nown; c += blockDim.x) a.perm[posS[c]] = j0 + c;
+    if (g == 0 && t == 0) {
+        a.out[0] = frank;
+        a.out[1] = reached ? 1 : 0;
+    }
+}
+
 // Wp(:, p) = W(:, perm[p]): storage order -> position order
 __global__ void gather_cols_kernel(const double* W, int64_t ldw, int m, int n, const int* perm, double* Wp,
                                    int64_t ldp) {
@@ -696,7 +1133,27 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
         RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCpqrThreads, 0));
     int G = std::max(1, std::min(ctx.num_sms * std::max(1, per_sm), ceil_div(n, 4 * (kCpqrThreads / 32))));
     G = std::min(G, ctx.num_sms);
-    Buf sv(ctx, sizeof(double) * 2 * G), sp(ctx, sizeof(int) * 2 * G), stt(ctx, sizeof(double) * 2 * G);
+    // resident-columns kernel when every CTA's columns fit on chip (two per
+    // warp in registers, the rest in shared memory) and m <= 32 * kCpqrRegs;
+    // RLRA_CPQR_RESIDENT=0 keeps the streaming kernel
+    static const bool res_env = !(std::getenv("RLRA_CPQR_RESIDENT") && std::getenv("RLRA_CPQR_RESIDENT")[0] == '0');
+    const int Gr = std::min(ctx.num_sms, std::max(1, n));
+    const int cpb_r = ceil_div(n, Gr), nreg_r = kResRegCols * (kResThreads / 32);
+    const size_t res_smem = sizeof(double) * (size_t(m) + 2 * size_t(cpb_r) + size_t(std::max(0, cpb_r - nreg_r)) * m) +
+                            sizeof(int) * size_t(cpb_r);
+    bool resident = res_env && !two_bar && m <= 32 * kResRows && res_smem <= 224 * 1024;
+    if (resident) {
+        RLRA_CUDA(cudaFuncSetAttribute(cpqr_res_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+        int per = 0;
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cpqr_res_kernel, kResThreads, res_smem));
+        resident = per >= 1;
+        if (resident) {
+            G = Gr;
+            one_bar = true;
+        }
+    }
+    Buf sv(ctx, sizeof(double) * 2 * G), sp(ctx, sizeof(int) * 2 * G), stt(ctx, sizeof(double) * 2 * G),
+        sst(ctx, sizeof(int) * 2 * G), scol(ctx, resident ? sizeof(double) * 2 * size_t(G) * m : 8);
     RLRA_CUDA(cudaMemsetAsync(out.p, 0, sizeof(int) * 4, ctx.stream));
     RLRA_CUDA(cudaMemsetAsync(res.p, 0, sizeof(double), ctx.stream));
     CpqrArgs a;
@@ -722,8 +1179,13 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     static const bool want_clk = std::getenv("RLRA_CPQR_PHASES") != nullptr;
     Buf clkb(ctx, sizeof(long long) * 8);
     a.phase_clk = (want_clk && one_bar) ? reinterpret_cast<long long*>(clkb.p) : nullptr;
+    a.slot_s = sst.i();
+    a.slot_col = scol.d();
     void* args[] = {&a};
-    if (one_bar) {
+    if (resident) {
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_res_kernel, dim3(G), dim3(kResThreads), args, res_smem,
+                                              ctx.stream));
+    } else if (one_bar) {
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_step_kernel, dim3(G), dim3(kCpqrStepThreads), args,
                                               step_smem, ctx.stream));
     } else {
