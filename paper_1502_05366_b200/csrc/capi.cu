@@ -942,13 +942,17 @@ rlra_status rlra_rsvd_rowsharded(rlra_ctx* ctx, rlra_comm* comm, int loc, const 
         OmegaSource om = omega_of(omega);
         Out U(C, loc, u, m_local, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
         OutVec<double> S(C, loc, sigma, k, "sigma");
-        if (loc == RLRA_HOST && m_local > 0 && n > 0) {
-            // host shard: the upload streams in row chunks under the local sketch GEMM
-            need(a, "a");
-            check_ld(lda, m_local, "a");
+        if (loc == RLRA_HOST && n > 0) {
+            // host shard: the upload streams in row chunks under the local sketch
+            // GEMM.  Every rank with a host shard (all ranks pass the same loc)
+            // takes this branch, an empty shard included: the first power step's
+            // shortcut needs every shard's A_g^T Y_g (zero for an empty one; a
+            // shard uploaded as one chunk sums it after its upload)
+            if (m_local > 0) {
+                need(a, "a");
+                check_ld(lda, m_local, "a");
+            }
             DMatBuf dA(C, m_local, n), Y(C, m_local, k + p), Zt(C, q > 0 ? n : 0, q > 0 ? k + p : 0);
-            // every rank takes the same branch: the Z shortcut needs all shards'
-            // partial sums (a rank whose shard is one chunk sums after its upload)
             if (q > 0 && !upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, &Zt.m))
                 gemm(C, Op::T, Op::N, 1.0, dA.m, Y.m, 0.0, Zt.m);
             if (q == 0) upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, nullptr);

@@ -250,6 +250,13 @@ bool upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
                        const DMat& Y, const DMat* Zt) {
     const int64_t m = dA.rows, n = dA.cols;
     if (m <= 0 || n <= 0) {
+        // an empty row shard still consumes its Omega draw (callback mode: the
+        // caller's RngState advances exactly as on the other ranks)
+        const int draw = om.next_draw++;
+        if (om.o->mode != RLRA_OMEGA_PHILOX && om.o->fill && n > 0) {
+            std::vector<double> h(size_t(n) * l);
+            om.o->fill(om.o->user, draw, int(n), l, h.data());
+        }
         if (Zt) zero_mat(ctx, *Zt);
         return Zt != nullptr;
     }

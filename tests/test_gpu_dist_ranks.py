@@ -92,6 +92,24 @@ def test_rsvd_rowsharded_ranks_match_engine_and_oracle(eng, orc, world):
     assert np.linalg.norm(U.T @ U - np.eye(k)) <= 1e-12
 
 
+def test_rsvd_rowsharded_empty_host_shard(orc):
+    """A rank holding no rows (host shard of 0 x n) still joins every
+    collective and consumes its Omega draw: the factorization equals the
+    oracle's, and every rank's RngState advanced like the reference's."""
+    m, n, k, p, q = 1500, 600, 40, 10, 2
+    a = make_test_matrix(m, n, np.exp(-np.arange(300) / 10.0), seed=46)
+    b = [0, 0, 700, 1500]
+    rngs = [R.Rng(12345) for _ in range(3)]
+    res = run_ranks(b, lambda r, e, c, r0, r1: e.rsvd_rowsharded(c, a[r0:r1], m, k, p, q, 1, rng=rngs[r]))
+    U = np.vstack([x[0] for x in res])
+    s, V = res[0][1], res[0][2]
+    uo, so, vo = orc.rsvd(a, k, p, q, 1, orc.rng(12345), 0)
+    assert sigma_ok(s, so)
+    assert np.linalg.norm(a - (U * s) @ V.T) <= 1.01 * np.linalg.norm(a - (uo * so) @ vo.T)
+    after = [r.next_u64() for r in rngs]
+    assert len(set(after)) == 1
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_id_cur_rand_rowsharded_ranks_pivots_match_oracle(orc, world):
     """The distributed CPQR of C^T (allgathered pivot statistics, positions
