@@ -93,6 +93,9 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
     asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ void lds_f64x2(uint32_t addr, double& a, double& b) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(a), "=d"(b) : "r"(addr));
+}
 
 // byte offset of element (k, x) in a swizzled stage tile
 __device__ __forceinline__ uint32_t tma_km_off(int k, int x) {  // 8 boxes [BK][16 x]
@@ -105,6 +108,24 @@ __device__ __forceinline__ uint32_t tma_xm_off(int k, int x) {  // [X][16 k] row
 __device__ __forceinline__ int tma_xm_row(int lr) { return 2 * (lr & 3) + (lr >> 2); }
 __device__ __forceinline__ int tma_km_row(int lr, int f) {
     return (lr & 1) + 8 * ((lr >> 1) & 1) + 4 * (lr >> 2) + 2 * f;
+}
+// Paired fragments (RLRA_GEMM_PAIRED, the default): every fragment load is a
+// 16-byte ld.shared.v2.f64 that feeds two DMMAs.
+//  * k-contiguous operands (B; A of A^T Y): the four k-steps of a 16-k stage
+//    use k = 2 lc + 8 q + h (q, h in {0, 1}) instead of lc + 4 s, so a lane's
+//    (k, k+1) sit in one 16-byte chunk; the rows of an 8-row fragment are
+//    xm_row(lr) = (lr >> 1) + 4 (lr & 1), which puts the two lr of each 8-lane
+//    phase in opposite chunk halves (conflict-free 16-byte loads);
+//  * x-contiguous A (A Z): fragments 2p and 2p+1 of a 16-row box take rows
+//    2 pi(lr) and 2 pi(lr) + 1, one 16-byte chunk, same pi.
+// The k-permutation is applied to both operands, so every k is summed once.
+#ifndef RLRA_GEMM_PAIRED
+#define RLRA_GEMM_PAIRED 1
+#endif
+__device__ __forceinline__ int tma_pi(int lr) { return (lr >> 1) + 4 * (lr & 1); }
+__device__ __forceinline__ int xm_row(int lr) { return RLRA_GEMM_PAIRED ? tma_pi(lr) : tma_xm_row(lr); }
+__device__ __forceinline__ int km_row(int lr, int f) {
+    return RLRA_GEMM_PAIRED ? 2 * tma_pi(lr) + f : tma_km_row(lr, f);
 }
 
 template <bool A_KM, int EPI, bool PHILOX, int CL>
@@ -269,18 +290,22 @@ __global__ void __launch_bounds__(384, 1)
     int arow[MF], bcol[NF];
 #pragma unroll
     for (int i = 0; i < MF; ++i)
-        arow[i] = A_KM ? wm * kTWM + (i >> 1) * 16 + tma_km_row(lr, i & 1) : wm * kTWM + i * 8 + tma_xm_row(lr);
+        arow[i] = A_KM ? wm * kTWM + (i >> 1) * 16 + km_row(lr, i & 1) : wm * kTWM + i * 8 + xm_row(lr);
 #pragma unroll
-    for (int j = 0; j < NF; ++j) bcol[j] = wn * kTWN + j * 8 + tma_xm_row(lr);
+    for (int j = 0; j < NF; ++j) bcol[j] = wn * kTWN + j * 8 + xm_row(lr);
     // fragment byte offsets at kk = 0; the later k-steps are an XOR of the
     // swizzle bits (4..6) with a constant (+ a row immediate for KM):
     //   XM: off(kk) = off(0) ^ (kk << 3)
     //   KM: off(kk) = (off(0) ^ ((kk & 4) << 4)) + kk * 128
+    //   paired: XM: off(q) = off(k0 = 2 lc) ^ (q << 6) (the (k, k+1) pair);
+    //           KM: off(q, h) = (off(k0 = 2 lc) ^ (h << 4)) + (8 q + h) * 128
+    constexpr int k0mul = RLRA_GEMM_PAIRED ? 2 : 1;
     uint32_t offa[MF], offb[NF];
 #pragma unroll
-    for (int i = 0; i < MF; ++i) offa[i] = A_KM ? tma_km_off(lc, arow[i]) : tma_xm_off(lc, arow[i]);
+    for (int i = 0; i < MF; ++i)
+        offa[i] = A_KM ? tma_km_off(k0mul * lc, arow[i]) : tma_xm_off(k0mul * lc, arow[i]);
 #pragma unroll
-    for (int j = 0; j < NF; ++j) offb[j] = tma_xm_off(lc, bcol[j]);
+    for (int j = 0; j < NF; ++j) offb[j] = tma_xm_off(k0mul * lc, bcol[j]);
 
     double acc[MF][NF][2];
 #pragma unroll
@@ -303,6 +328,30 @@ __global__ void __launch_bounds__(384, 1)
         for (int i = 0; i < MF; ++i) fa[i] = a_s + offa[i];
 #pragma unroll
         for (int j = 0; j < NF; ++j) fb[j] = b_s + offb[j];
+#if RLRA_GEMM_PAIRED
+#pragma unroll
+        for (int q = 0; q < kTBK / 8; ++q) {
+            double af[2][MF], bf[2][NF];
+            if (A_KM) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int i = 0; i < MF; i += 2)  // fa[i]: the even row, the chunk's first half
+                        lds_f64x2((fa[i] ^ uint32_t(h << 4)) + uint32_t((8 * q + h) * 128), af[h][i], af[h][i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < MF; ++i) lds_f64x2(fa[i] ^ uint32_t(q << 6), af[0][i], af[1][i]);
+            }
+#pragma unroll
+            for (int j = 0; j < NF; ++j) lds_f64x2(fb[j] ^ uint32_t(q << 6), bf[0][j], bf[1][j]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int i = 0; i < MF; ++i)
+#pragma unroll
+                    for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[h][i], bf[h][j]);
+        }
+#else
 #pragma unroll
         for (int kk = 0; kk < kTBK; kk += 4) {
             double af[MF], bf[NF];
@@ -317,6 +366,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int j = 0; j < NF; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
+#endif
         __syncwarp();
         if (lane == 0) {
             if (CL == 1) {
@@ -353,7 +403,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int j = 0; j < NF; ++j)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
+                        const int col = n0 + wn * kTWN + j * 8 + xm_row(2 * lc + h);
                         rin[ii][j][h] = (row < p.M && col < p.N) ? p.R[row + int64_t(col) * p.ldr] : 0.0;
                     }
             }
@@ -366,7 +416,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < NF; ++j) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int col = n0 + wn * kTWN + j * 8 + tma_xm_row(2 * lc + h);
+                    const int col = n0 + wn * kTWN + j * 8 + xm_row(2 * lc + h);
                     if (row < p.M && col < p.N) {
                         const double v = acc[i][j][h];
                         if (EPI == EPI_STORE && tpart >= 0) {

@@ -1,3 +1,5 @@
 set -x
-timeout 1200 python -m pytest tests/test_gpu_dist_ranks.py tests/test_gpu_dist.py -q -p no:cacheprovider > gpurun_out/t13.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/t13.log
-timeout 900 python bench.py --gpus 2 --comm host --m 40000 --steps 2 --warmup 1 --no-cpu > gpurun_out/b2h2.json 2> gpurun_out/b2h2.err; echo "rc=$?"; python -c "import json;d=json.load(open('gpurun_out/b2h2.json'));print(d['rel_error'], d['e2e']['ms_per_step'])"
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/t14_gpu_all.log 2>&1
+echo "pytest rc=$?"; grep -E "passed|failed|^FAILED|^ERROR" gpurun_out/t14_gpu_all.log | tail -10
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/t14_bench.json 2> gpurun_out/t14_bench.err; echo "bench rc=$?"; python -c "import json;d=json.load(open('gpurun_out/t14_bench.json'));print(d['ms_per_step'], d['value'], d['roofline']['frac'], d['e2e']['ms_per_step'], d['phases_ms'])"
+python tools/host_vs_device_c5.py
