@@ -117,16 +117,16 @@ __device__ __forceinline__ int tma_km_row(int lr, int f) {
 //    xm_row(lr) = (lr >> 1) + 4 (lr & 1), which puts the two lr of each 8-lane
 //    phase in opposite chunk halves (conflict-free 16-byte loads);
 //  * x-contiguous A (A Z): fragments 2p and 2p+1 of a 16-row box take rows
-//    2 pi(lr) and 2 pi(lr) + 1, one 16-byte chunk, same pi.
+//    2 lr and 2 lr + 1, one 16-byte chunk; the chunk index is lr ^ (k & 7)
+//    with k = 2 lc + 8 q + h, so the two lr of a phase (one even, one odd)
+//    never share a chunk.
 // The k-permutation is applied to both operands, so every k is summed once.
 #ifndef RLRA_GEMM_PAIRED
 #define RLRA_GEMM_PAIRED 1
 #endif
 __device__ __forceinline__ int tma_pi(int lr) { return (lr >> 1) + 4 * (lr & 1); }
 __device__ __forceinline__ int xm_row(int lr) { return RLRA_GEMM_PAIRED ? tma_pi(lr) : tma_xm_row(lr); }
-__device__ __forceinline__ int km_row(int lr, int f) {
-    return RLRA_GEMM_PAIRED ? 2 * tma_pi(lr) + f : tma_km_row(lr, f);
-}
+__device__ __forceinline__ int km_row(int lr, int f) { return RLRA_GEMM_PAIRED ? 2 * lr + f : tma_km_row(lr, f); }
 
 template <bool A_KM, int EPI, bool PHILOX, int CL>
 __global__ void __launch_bounds__(384, 1)
