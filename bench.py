@@ -449,9 +449,9 @@ def main():
                      "unit": "TFLOP/s", "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
                      # dram__bytes_read.sum + write.sum of the dominant launch (the TN
                      # A^T*Y product) in one ncu --set full capture
-                     # (profiles/r02_gemm_tma_ncu_summary.md): 36.20 GB read + 0.32 GB
+                     # (profiles/r02_gemm_tma_ncu_summary.md): 36.15 GB read + 0.32 GB
                      # write vs 32.0 GB algorithmic (A read once)
-                     "traffic": 36.196e9 + 0.3178e9,
+                     "traffic": 36.146e9 + 0.3207e9,
                      "traffic_unit": "bytes/launch (TN A^T*Y GEMM)",
                      "kernel": "dgemm_tma_kernel (A-streaming products: sketch, 2q power, projection)",
                      "peak_source": "measured DMMA peak, tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry)"},

@@ -1,4 +1,7 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_kernels.py -q -p no:cacheprovider -k "gemm or matmul or tma" > gpurun_out/p8.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/p8.log
-python tools/time_gemm.py
-timeout 1200 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active -k regex:dgemm_tma -c 2 --csv python tools/profile_gemm.py 2>&1 | grep -E "dgemm|gpu__|bank|dmma" | cut -c1-250 | tail -8
+mkdir -p /tmp/reps
+for s in 0 1 2; do
+timeout 1200 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:dgemm_tma --launch-skip $s -c 1 -o /tmp/reps/g$s -f python tools/profile_gemm.py > gpurun_out/r02c_gemm_ncu_$s.log 2>&1; echo "ncu skip=$s rc=$?"
+/usr/local/cuda/bin/ncu -i /tmp/reps/g$s.ncu-rep --page raw --csv > gpurun_out/r02c_gemm_raw_$s.csv 2>&1
+done
+timeout 1500 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r02c_step_launches.csv python tools/profile_step.py > gpurun_out/r02c_step.log 2>&1; echo "ncu1 rc=$?"
