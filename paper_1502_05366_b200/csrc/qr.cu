@@ -283,6 +283,7 @@ namespace {
 //  C  CTAs, 32 x 32 tiles with K = 64: Schur update G[J+, J+] -= R[J,J+]^T
 //     R[J,J+] (upper tiles) and acc[0:j1, J+] -= X[0:j1, J] R[J, J+].
 constexpr int kCholCoopMax = 1024;
+constexpr int kCholOuterNB = 512;  // diagonal blocks of the large-n Cholesky (cooperative kernel)
 constexpr int kCP = kCholNB + 1;  // shared-memory pitch
 
 struct CholCoopArgs {
@@ -296,6 +297,7 @@ struct CholCoopArgs {
     double floor;
     int* flag;
     unsigned long long* tprobe;  // optional phase timestamps (RLRA_CHOL_PROBE)
+    int keep_dorig;              // dorig already holds the pivot-test references (a diagonal block)
 };
 
 __device__ __forceinline__ void chol_probe(unsigned long long* tp, int idx) {
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
     for (int j = blockIdx.x; j < n; j += gridDim.x)
         for (int i = t; i < n; i += blockDim.x) {
             X[i + j * ldr] = (i == j) ? 1.0 : 0.0;
-            if (i == j) a.dorig[i] = G[i + j * ldg];
+            if (i == j && !a.keep_dorig) a.dorig[i] = G[i + j * ldg];
             if (i > j) G[i + j * ldg] = 0.0;
         }
     grid_sync(a.bar);
@@ -524,6 +526,25 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
     }
 }
 
+// the cooperative kernel on a diagonal block of a larger Cholesky: pivot
+// references from the caller's original diagonal, breakdown into the caller's
+// flag, no host synchronisation
+void chol_coop_block(Context& ctx, const DMat& G, const DMat& Rinv, double floor, double* dorig, int* flag) {
+    constexpr int smem = 2 * kCholNB * kCP * sizeof(double);
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RLRA_CUDA(cudaFuncSetAttribute(chol_inv_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_inv_coop_kernel, 256, smem));
+        grid_cap = std::max(1, per_sm) * ctx.num_sms;
+    }
+    CholCoopArgs a{ctx.gbar, G.p, G.ld, int(G.rows), Rinv.p, Rinv.ld, dorig, floor, flag, nullptr, 1};
+    void* args[] = {&a};
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)chol_inv_coop_kernel, dim3(std::min(grid_cap, ctx.num_sms)),
+                                          dim3(256), args, smem, ctx.stream));
+    ++ctx.launches;
+}
+
 bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
     const int n = int(G.rows);
     constexpr int smem = 2 * kCholNB * kCP * sizeof(double);
@@ -539,7 +560,7 @@ bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double f
     static unsigned long long* tprobe = nullptr;
     static bool want_probe = getenv("RLRA_CHOL_PROBE") != nullptr;
     if (want_probe && !tprobe) RLRA_CUDA(cudaMallocManaged(&tprobe, 64 * 8));
-    CholCoopArgs a{ctx.gbar, G.p, G.ld, n, Rinv.p, Rinv.ld, dorig.d(), floor, flag.i(), tprobe};
+    CholCoopArgs a{ctx.gbar, G.p, G.ld, n, Rinv.p, Rinv.ld, dorig.d(), floor, flag.i(), tprobe, 0};
     void* args[] = {&a};
     static const int grid_env = getenv("RLRA_CHOL_GRID") ? atoi(getenv("RLRA_CHOL_GRID")) : 0;
     const int grid = grid_env > 0 ? std::min(grid_env, grid_cap) : std::min(grid_cap, ctx.num_sms);
@@ -570,18 +591,29 @@ bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor)
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
     zero_mat(ctx, Rinv);
-    for (int j0 = 0; j0 < n; j0 += kCholNB) {
-        const int nb = std::min(kCholNB, n - j0), j1 = j0 + nb;
-        constexpr int smem = 2 * kCholNB * (kCholNB + 1) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            RLRA_CUDA(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = true;
+    // outer blocks of kCholOuterNB columns, each diagonal block factored (with
+    // its inverse) by the one-launch cooperative kernel against the ORIGINAL
+    // diagonal, the trailing update on the DMMA GEMM: n / 512 serial steps
+    // instead of n / 64 (RLRA_CHOL_NB64=1 keeps the 64-column chain)
+    static const bool nb64 = std::getenv("RLRA_CHOL_NB64") != nullptr;
+    const int NB = nb64 ? kCholNB : kCholOuterNB;
+    for (int j0 = 0; j0 < n; j0 += NB) {
+        const int nb = std::min(NB, n - j0), j1 = j0 + nb;
+        if (nb64) {
+            constexpr int smem = 2 * kCholNB * (kCholNB + 1) * sizeof(double);
+            static bool attr = false;
+            if (!attr) {
+                RLRA_CUDA(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                attr = true;
+            }
+            chol_diag_kernel<<<1, 256, smem, ctx.stream>>>(G.p, G.ld, j0, nb, Rinv.p, Rinv.ld, dorig.d(),
+                                                        floor, flag.i());
+            RLRA_LAUNCH_CHECK();
+            ++ctx.launches;
+        } else {
+            chol_coop_block(ctx, G.block(j0, j0, nb, nb), Rinv.block(j0, j0, nb, nb), floor, dorig.d() + j0,
+                            flag.i());
         }
-        chol_diag_kernel<<<1, 256, smem, ctx.stream>>>(G.p, G.ld, j0, nb, Rinv.p, Rinv.ld, dorig.d(),
-                                                    floor, flag.i());
-        RLRA_LAUNCH_CHECK();
-        ++ctx.launches;
         if (j1 < n) {
             const int rest = n - j1;
             DMatBuf P(ctx, nb, rest);
@@ -600,8 +632,8 @@ bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor)
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
     // off-diagonal blocks of R^{-1}: Rinv[0:j0, J] = -Rinv[0:j0,0:j0] R[0:j0,J] Rinv[J,J]
-    for (int j0 = kCholNB; j0 < n; j0 += kCholNB) {
-        const int nb = std::min(kCholNB, n - j0);
+    for (int j0 = NB; j0 < n; j0 += NB) {
+        const int nb = std::min(NB, n - j0);
         DMatBuf T(ctx, j0, nb);
         gemm(ctx, Op::N, Op::N, 1.0, Rinv.block(0, 0, j0, j0), G.block(0, j0, j0, nb), 0.0, T);
         gemm(ctx, Op::N, Op::N, -1.0, T, Rinv.block(j0, j0, nb, nb), 0.0, Rinv.block(0, j0, j0, nb));

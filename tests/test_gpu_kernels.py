@@ -419,3 +419,23 @@ def test_upper_tri_solve_k_beyond_the_old_shared_memory_bound(eng):
     assert st == 0, R.lib().rlra_last_error()
     err = torch.linalg.norm(T.t() - X) / torch.linalg.norm(X)
     assert float(err) <= 1e-12 and cl.value == 0
+
+
+@pytest.mark.parametrize("n", [1025, 1500, 2100])
+def test_chol_inv_large_blocked_vs_numpy(eng, n):
+    """n > 1024: diagonal blocks of 512 by the cooperative kernel, trailing
+    updates and the off-diagonal blocks of R^{-1} on the GEMM; R upper with
+    R^T R = G, R R^{-1} = I; a rank-deficient Gram is reported as breakdown."""
+    rs = np.random.default_rng(n)
+    y = rs.standard_normal((2 * n, n)) * np.exp(-np.arange(n) / (n / 6.0))
+    g = y.T @ y
+    r, ri, ok = eng.chol_inv(g, 1e-12)
+    assert ok
+    assert np.allclose(np.tril(r, -1), 0.0)
+    assert np.linalg.norm(r.T @ r - g) <= 1e-13 * np.linalg.norm(g)
+    assert np.linalg.norm(r @ ri - np.eye(n)) <= 1e-9
+    yd = y[:, : n // 2]
+    gd = np.zeros((n, n))
+    gd[: n // 2, : n // 2] = yd.T @ yd  # exactly singular beyond n/2
+    _, _, ok2 = eng.chol_inv(gd, 1e-12)
+    assert not ok2
