@@ -780,11 +780,13 @@ __device__ __forceinline__ int bar_or_partial(int nthreads, int pred) {
 // them interleave): t = |e| / (|d| + hypot(d, e)) with d = aqq - app,
 // e = 2 apq — the same t — and the skip test on squares.  Returns false when
 // a product is near over/underflow; the caller then takes jac_rotation_ref.
+// An exactly orthogonal pair (apq == 0: every pair with a zero or padded
+// column) is a plain skip on the fast path, as in the reference.
 __device__ __forceinline__ bool jac_rotation_fast(double app, double aqq, double apq, double& c, double& s,
                                                   int& act) {
     const double pr = app * aqq, d = aqq - app, e = 2.0 * apq;
     const double h2 = fma(d, d, e * e);
-    const bool ok = pr > 1e-290 && pr < 1e290 && h2 > 1e-290 && h2 < 1e290;
+    const bool ok = (pr > 1e-290 && pr < 1e290 && h2 > 1e-290 && h2 < 1e290) || apq == 0.0;
     act = apq * apq > 1e-30 * pr;
     const double h = h2 * rsqrt_nr2(h2);
     const double tm = fabs(e) * rcp_nr2(fabs(d) + h);
@@ -794,15 +796,26 @@ __device__ __forceinline__ bool jac_rotation_fast(double app, double aqq, double
     s = act ? t * cc : 0.0;
     return ok;
 }
-__device__ __noinline__ int jac_rotation_ref(double app, double aqq, double apq, double& c, double& s) {
-    c = 1.0;
-    s = 0.0;
-    if (!(app != 0.0 && aqq != 0.0 && fabs(apq) > 1e-15 * sqrt(app * aqq))) return 0;
+struct RotRef {
+    double c, s;
+    int act;
+};
+// (returned by value: the call leaves the caller's rotation in registers)
+__device__ __noinline__ RotRef jac_rotation_ref_v(double app, double aqq, double apq) {
+    RotRef r{1.0, 0.0, 0};
+    if (!(app != 0.0 && aqq != 0.0 && fabs(apq) > 1e-15 * sqrt(app * aqq))) return r;
     const double zeta = (aqq - app) / (2.0 * apq);
     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    c = 1.0 / sqrt(1.0 + t * t);
-    s = t * c;
-    return 1;
+    r.c = 1.0 / sqrt(1.0 + t * t);
+    r.s = t * r.c;
+    r.act = 1;
+    return r;
+}
+__device__ __forceinline__ int jac_rotation_ref(double app, double aqq, double apq, double& c, double& s) {
+    const RotRef r = jac_rotation_ref_v(app, aqq, apq);
+    c = r.c;
+    s = r.s;
+    return r.act;
 }
 
 // pair k of step st in a cross (I_k, J_{k+st}) or intra (tournament inside
@@ -895,6 +908,175 @@ __device__ __forceinline__ void bgram_apply(const double* Xs, int P, int Mp, con
 
 __device__ __forceinline__ void jb_publish(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Gram G0 = Xs^T Xs of a staged pair (C2 columns, pitch P, Mp rows) on DMMA:
+// warp w sums rows [w*Mp/8, (w+1)*Mp/8) for the upper 8x8 tiles (a tile's two
+// operand fragments are the same column-block loads), the 8 partials (Pb)
+// summed in a fixed order, G0 mirrored; J <- I.  The caller synchronises.
+template <int BW>
+__device__ __forceinline__ void bgram_gram(const double* Ws, int P, int Mp, double* Pb, double* G0, double* J) {
+    using B = BGram<BW>;
+    constexpr int C2 = B::C2, NB8 = B::NB8, NT = B::NT, GP = B::GP;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+    {
+        // two accumulator sets (even / odd k-steps) halve the DMMA chain
+        double acc[2][NT][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < NT; ++u) acc[h][u][0] = acc[h][u][1] = 0.0;
+        const int k1 = (warp + 1) * (Mp / 8);
+        for (int k = warp * (Mp / 8); k < k1; k += 8) {  // Mp / 8 is a multiple of 4
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && k + 4 >= k1) break;
+                double f[NB8];
+#pragma unroll
+                for (int bb = 0; bb < NB8; ++bb) f[bb] = Ws[(bb * 8 + lr) * P + k + 4 * h + lc];
+                int u = 0;
+#pragma unroll
+                for (int bi = 0; bi < NB8; ++bi)
+#pragma unroll
+                    for (int bj = bi; bj < NB8; ++bj, ++u) jac_dmma(acc[h][u][0], acc[h][u][1], f[bi], f[bj]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc] = acc[0][u][0] + acc[1][u][0];
+            Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc + 1] = acc[0][u][1] + acc[1][u][1];
+        }
+    }
+    __syncthreads();
+    for (int e = t; e < NT * 64; e += blockDim.x) {
+        const int u = e >> 6, w = e & 63;
+        int bi = 0, rem = u;
+        while (rem >= NB8 - bi) rem -= NB8 - bi++;
+        const int bj = bi + rem;
+        double sum = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * NT + u) * 64 + w];
+        const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
+        G0[row * GP + col] = sum;
+        G0[col * GP + row] = sum;
+    }
+    for (int e = t; e < C2 * C2; e += blockDim.x) J[(e / C2) * GP + e % C2] = (e / C2 == e % C2) ? 1.0 : 0.0;
+}
+
+// The visit's steps on G (double-buffered G0) accumulating J, by the BW*BW
+// threads t < BW*BW: thread (k, l) owns the 2x2 block of pairs (k, l),
+// computes both pairs' rotations itself from the diagonal entries (no serial
+// parameter phase), updates its G block into the other buffer and its J block
+// in place — one barrier (named barrier 1 unless BW*BW == 256) per step.
+// Returns whether any pair rotated (the same value on every caller thread).
+template <int BW>
+__device__ __forceinline__ int bgram_steps(double* G0, double* J, bool intra) {
+    using B = BGram<BW>;
+    constexpr int C2 = B::C2, GP = B::GP;
+    const int t = threadIdx.x;
+    int rot = 0;
+    const int k = t / BW, l = t % BW;
+    const int nsteps = intra ? BW - 1 : BW;
+    for (int st = 0; st < nsteps; ++st) {
+        const double* Gc = G0 + (st & 1) * C2 * GP;
+        double* Gn = G0 + ((st & 1) ^ 1) * C2 * GP;
+        int act = 0;
+        {
+            const int pqk = bgram_pair<BW>(intra, k, st), pql = bgram_pair<BW>(intra, l, st);
+            const int pk = pqk & 255, qk = pqk >> 8, pl = pql & 255, ql = pql >> 8;
+            // (a padded column's Gram entries are 0: never rotated)
+            const double kpp = Gc[pk * GP + pk], kqq = Gc[qk * GP + qk], kpq = Gc[pk * GP + qk];
+            const double lpp = Gc[pl * GP + pl], lqq = Gc[ql * GP + ql], lpq = Gc[pl * GP + ql];
+            double ck, sk, cl, sl;
+            int ak, al;
+            const bool okk = jac_rotation_fast(kpp, kqq, kpq, ck, sk, ak);
+            const bool okl = jac_rotation_fast(lpp, lqq, lpq, cl, sl, al);
+            if (!okk) ak = jac_rotation_ref(kpp, kqq, kpq, ck, sk);
+            if (!okl) al = jac_rotation_ref(lpp, lqq, lpq, cl, sl);
+            act = (k == l) ? ak : 0;
+            if (al) {  // J <- J R_l on rows {pk, qk}
+                const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
+                const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
+                J[pk * GP + pl] = cl * j0 - sl * j1;
+                J[pk * GP + ql] = sl * j0 + cl * j1;
+                J[qk * GP + pl] = cl * j2 - sl * j3;
+                J[qk * GP + ql] = sl * j2 + cl * j3;
+            }
+            if (k <= l) {  // G block (k, l) <- R_k^T B R_l, mirrored
+                double b00 = Gc[pk * GP + pl], b01 = Gc[pk * GP + ql];
+                double b10 = Gc[qk * GP + pl], b11 = Gc[qk * GP + ql];
+                if (al) {
+                    const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
+                    const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
+                    b00 = x0, b01 = x1, b10 = x2, b11 = x3;
+                }
+                if (ak) {
+                    const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
+                    const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
+                    b00 = y0, b01 = y1, b10 = y2, b11 = y3;
+                }
+                Gn[pk * GP + pl] = b00;
+                Gn[pk * GP + ql] = b01;
+                Gn[qk * GP + pl] = b10;
+                Gn[qk * GP + ql] = b11;
+                Gn[pl * GP + pk] = b00;
+                Gn[ql * GP + pk] = b01;
+                Gn[pl * GP + qk] = b10;
+                Gn[ql * GP + qk] = b11;
+            }
+        }
+        rot |= (BW * BW == 256) ? __syncthreads_or(act) : bar_or_partial(BW * BW, act);
+    }
+    return rot;
+}
+
+// V(rows, cols of the pair) <- V * Jb on DMMA, read and written through L2
+// (__ldcg: other CTAs wrote these columns in earlier rounds), by warps
+// [w0, w0 + nw) with 8-row slabs in flight
+template <int BW>
+__device__ __forceinline__ void bgram_apply_l2(const double* Jb, double* V, int64_t ldv, int n, int bI, int bJ,
+                                               int w0, int nw) {
+    using B = BGram<BW>;
+    constexpr int NB8 = B::NB8, JP = B::JP, KF = B::KF;
+    const int warp = int(threadIdx.x >> 5) - w0, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    auto gcol = [&](int c) { return c < BW ? bI * BW + c : bJ * BW + (c - BW); };
+    double bf[KF][NB8];
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf)
+#pragma unroll
+        for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
+    int icol[KF], ocol[NB8][2];
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) icol[kf] = gcol(4 * kf + lc);
+#pragma unroll
+    for (int ct = 0; ct < NB8; ++ct)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ocol[ct][h] = gcol(ct * 8 + 2 * lc + h);
+    constexpr int U = 32 / KF;  // V slabs (8 rows) in flight per warp
+    for (int sl0 = warp * U; sl0 < (n + 7) / 8; sl0 += nw * U) {
+        double af[U][KF];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+            for (int kf = 0; kf < KF; ++kf)
+                af[u][kf] = (row < n && icol[kf] < n) ? __ldcg(V + row + int64_t(icol[kf]) * ldv) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int row = (sl0 + u) * 8 + lr;
+#pragma unroll
+            for (int ct = 0; ct < NB8; ++ct) {
+                double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                if (row < n) {
+                    if (ocol[ct][0] < n) __stcg(V + row + int64_t(ocol[ct][0]) * ldv, o0);
+                    if (ocol[ct][1] < n) __stcg(V + row + int64_t(ocol[ct][1]) * ldv, o1);
+                }
+            }
+        }
+    }
 }
 
 // a.helpers == 0: CTA g runs pair slots g, g + grid, ... and applies J to
@@ -997,108 +1179,11 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
                 bgram_stage<BW>(Ws, P, Mp, a.W, a.ldw, (m + 1) & ~1, n, bI, bJ, wver, R, &stage_bar, stage_phase);
                 mark(0);
                 // ---- 1. Gram: warp w sums rows [w*Mp/8, (w+1)*Mp/8) ------------
-                {
-                    // two accumulator sets (even / odd k-steps) halve the DMMA chain
-                    double acc[2][NT][2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int u = 0; u < NT; ++u) acc[h][u][0] = acc[h][u][1] = 0.0;
-                    const int k1 = (warp + 1) * (Mp / 8);
-                    for (int k = warp * (Mp / 8); k < k1; k += 8) {  // Mp / 8 is a multiple of 4
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (h == 1 && k + 4 >= k1) break;
-                            double f[NB8];
-#pragma unroll
-                            for (int bb = 0; bb < NB8; ++bb) f[bb] = Ws[(bb * 8 + lr) * P + k + 4 * h + lc];
-                            int u = 0;
-#pragma unroll
-                            for (int bi = 0; bi < NB8; ++bi)
-#pragma unroll
-                                for (int bj = bi; bj < NB8; ++bj, ++u)
-                                    jac_dmma(acc[h][u][0], acc[h][u][1], f[bi], f[bj]);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < NT; ++u) {
-                        Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc] = acc[0][u][0] + acc[1][u][0];
-                        Pb[(warp * NT + u) * 64 + lr * 8 + 2 * lc + 1] = acc[0][u][1] + acc[1][u][1];
-                    }
-                }
-                __syncthreads();
-                for (int e = t; e < NT * 64; e += 256) {
-                    const int u = e >> 6, w = e & 63;
-                    int bi = 0, rem = u;
-                    while (rem >= NB8 - bi) rem -= NB8 - bi++;
-                    const int bj = bi + rem;
-                    double sum = 0.0;
-#pragma unroll
-                    for (int ww = 0; ww < 8; ++ww) sum += Pb[(ww * NT + u) * 64 + w];
-                    const int row = bi * 8 + (w >> 3), col = bj * 8 + (w & 7);
-                    G0[row * GP + col] = sum;
-                    G0[col * GP + row] = sum;
-                }
-                for (int e = t; e < C2 * C2; e += 256) J[(e / C2) * GP + e % C2] = (e / C2 == e % C2) ? 1.0 : 0.0;
+                bgram_gram<BW>(Ws, P, Mp, Pb, G0, J);
                 __syncthreads();
                 mark(1);
                 // ---- 2. the visit's steps on G: thread (k, l) owns pair block (k, l)
-                int rot = 0;
-                if (t < BW * BW) {  // the pair-block owners only: a named barrier of BW*BW threads per step
-                    const int k = t / BW, l = t % BW;
-                    const bool own = true;
-                    const int nsteps = intra ? BW - 1 : BW;
-                    for (int st = 0; st < nsteps; ++st) {
-                        const double* Gc = G0 + (st & 1) * C2 * GP;
-                        double* Gn = G0 + ((st & 1) ^ 1) * C2 * GP;
-                        int act = 0;
-                        if (own) {
-                            const int pqk = bgram_pair<BW>(intra, k, st), pql = bgram_pair<BW>(intra, l, st);
-                            const int pk = pqk & 255, qk = pqk >> 8, pl = pql & 255, ql = pql >> 8;
-                            // (a padded column's Gram entries are 0: never rotated)
-                            const double kpp = Gc[pk * GP + pk], kqq = Gc[qk * GP + qk], kpq = Gc[pk * GP + qk];
-                            const double lpp = Gc[pl * GP + pl], lqq = Gc[ql * GP + ql], lpq = Gc[pl * GP + ql];
-                            double ck, sk, cl, sl;
-                            int ak, al;
-                            const bool okk = jac_rotation_fast(kpp, kqq, kpq, ck, sk, ak);
-                            const bool okl = jac_rotation_fast(lpp, lqq, lpq, cl, sl, al);
-                            if (!okk) ak = jac_rotation_ref(kpp, kqq, kpq, ck, sk);
-                            if (!okl) al = jac_rotation_ref(lpp, lqq, lpq, cl, sl);
-                            act = (k == l) ? ak : 0;
-                            if (al) {  // J <- J R_l on rows {pk, qk}
-                                const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
-                                const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
-                                J[pk * GP + pl] = cl * j0 - sl * j1;
-                                J[pk * GP + ql] = sl * j0 + cl * j1;
-                                J[qk * GP + pl] = cl * j2 - sl * j3;
-                                J[qk * GP + ql] = sl * j2 + cl * j3;
-                            }
-                            if (k <= l) {  // G block (k, l) <- R_k^T B R_l, mirrored
-                                double b00 = Gc[pk * GP + pl], b01 = Gc[pk * GP + ql];
-                                double b10 = Gc[qk * GP + pl], b11 = Gc[qk * GP + ql];
-                                if (al) {
-                                    const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
-                                    const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
-                                    b00 = x0, b01 = x1, b10 = x2, b11 = x3;
-                                }
-                                if (ak) {
-                                    const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
-                                    const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
-                                    b00 = y0, b01 = y1, b10 = y2, b11 = y3;
-                                }
-                                Gn[pk * GP + pl] = b00;
-                                Gn[pk * GP + ql] = b01;
-                                Gn[qk * GP + pl] = b10;
-                                Gn[qk * GP + ql] = b11;
-                                Gn[pl * GP + pk] = b00;
-                                Gn[ql * GP + pk] = b01;
-                                Gn[pl * GP + qk] = b10;
-                                Gn[ql * GP + qk] = b11;
-                            }
-                        }
-                        rot |= (BW * BW == 256) ? __syncthreads_or(act) : bar_or_partial(BW * BW, act);
-                    }
-                }
+                int rot = t < BW * BW ? bgram_steps<BW>(G0, J, intra) : 0;
                 rot = __syncthreads_or(rot);
                 mark(2);
                 if (rot && t == 0) flags[sweep % 3] = 1;
@@ -1184,6 +1269,308 @@ __global__ void __launch_bounds__(256, 1) bgram_jacobi_kernel(GramJacArgs a) {
     if (blockIdx.x == 0 && t == 0) flags[4] = sweep;
     if (clk)
         for (int i = 0; i < 6; ++i) a.phase_clk[i] = ph[i];
+}
+
+// ------------------ cluster-resident Gram block Jacobi (l <= 256, one cluster) ---
+// The bgram schedule (blocks of BW = 8 columns, nb - 1 cross rounds + one
+// intra round per sweep, every column pair once per sweep, the same Gram /
+// steps arithmetic and stop rule) with the np = nb / 2 <= 16 pair CTAs
+// forming ONE thread-block cluster, so W never leaves shared memory.  Per
+// round a CTA
+//   1. waits for its pair's columns (an mbarrier completed by the senders'
+//      st.async bytes) and forms G = W_p^T W_p (DMMA),
+//   2. runs the steps on G (2 warps),
+//   3. sends W_p J (or W_p unchanged) straight into the shared memory of the
+//      CTAs owning each block next round (st.async, double-buffered), and logs
+//      J (jlog, one slot per (sweep parity, round, pair); rlog = rotated).
+// Cross-CTA ordering: the data's own mbarrier (RAW) and one split cluster
+// barrier per round, relaxed, for buffer reuse (WAR); a release/acquire
+// cluster barrier once per sweep carries the rotation flag (a word in CTA
+// 0's shared memory) and publishes the sweep's log.  V is off the critical
+// path: CTA g keeps V's rows [16 g, 16 g + 16) in shared memory (starting as
+// I), and while 2 warps run round r's steps the other 6 replay round r of
+// the PREVIOUS sweep's log on those rows (DMMA).  The last sweep rotates
+// nothing, so V is complete when the loop stops.
+struct CGramArgs {
+    double* W;
+    int64_t ldw;
+    int m, n;
+    int nb;                // column blocks (even, <= 32)
+    double* V;             // n x n
+    int64_t ldv;
+    double* jlog;          // [2][nb][np] C2 x C2 J, row-major (k, c)
+    unsigned char* rlog;   // [2][nb][np] rotated
+    int* flags;            // [3] status, [4] sweeps used
+    long long* phase_clk;  // optional: CTA 0's clock64 per phase (RLRA_JACOBI_PHASES)
+};
+
+constexpr int kCgVRows = 16, kCgVP = kCgVRows + 4;  // V rows per CTA; column pitch (== 4 mod 16)
+
+template <int BW>
+size_t cgram_smem(int m, int nb) {
+    using B = BGram<BW>;
+    return sizeof(double) * (size_t(2) * B::C2 * bgram_pitch(m) + 3 * B::C2 * B::GP + B::C2 * B::JP +
+                             8 * B::NT * 64 + size_t(nb) * BW * kCgVP);
+}
+
+__device__ __forceinline__ unsigned cg_map(const void* p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(jb_smem(p)), "r"(rank));
+    return r;
+}
+// 16 bytes into a peer's shared memory, completing on the peer's mbarrier
+__device__ __forceinline__ void cg_st_async(unsigned addr, double v0, double v1, unsigned bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+                 "d"(v0), "d"(v1), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void cg_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cg_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cg_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cg_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+template <int BW>
+__global__ void __launch_bounds__(256, 1) cgram_jacobi_kernel(CGramArgs a) {
+    using B = BGram<BW>;
+    constexpr int C2 = B::C2, NB8 = B::NB8, GP = B::GP, JP = B::JP, KF = B::KF;
+    static_assert(BW == 8, "one 8-column tile per block half");
+    extern __shared__ double csm[];
+    const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
+    const int Mp = bgram_rows(m), P = bgram_pitch(m);
+    double* Wb0 = csm;                      // 2 buffers of C2 columns, pitch P
+    double* G0 = Wb0 + size_t(2) * C2 * P;  // C2 x GP, two buffers
+    double* J = G0 + 2 * C2 * GP;           // C2 x GP
+    double* Jb = J + C2 * GP;               // C2 x JP (DMMA B operand)
+    double* Pb = Jb + C2 * JP;              // 8 warps x NT tiles x 64 partial Grams
+    double* Vs = Pb + 8 * B::NT * 64;       // V rows [16 g, 16 g + 16), column-major, pitch kCgVP
+    __shared__ unsigned char own[32 * 32];  // own[r * nb + b] = owner CTA << 1 | slot
+    __shared__ unsigned char prs[32 * 16 * 2];  // [r][pair] -> bI, bJ
+    __shared__ __align__(8) uint64_t inbar[2];
+    __shared__ unsigned sflag[2];  // CTA 0: rotated-in-sweep (sweep parity)
+    __shared__ int s_stop;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
+    const int g = int(blockIdx.x);
+    const unsigned in_bytes = unsigned(C2) * unsigned(Mp) * 8u;
+    auto pair_of = [&](int gg, int r, int& bI, int& bJ) {
+        if (r == nb - 1) {
+            bI = 2 * gg;
+            bJ = 2 * gg + 1;
+        } else {
+            const int b1 = rr_col(gg, r, nb), b2 = rr_col(nb - 1 - gg, r, nb);
+            bI = min(b1, b2);
+            bJ = max(b1, b2);
+        }
+    };
+    for (int e = t; e < np * nb; e += blockDim.x) {
+        const int r = e / np, gg = e % np;
+        int bI, bJ;
+        pair_of(gg, r, bI, bJ);
+        own[r * nb + bI] = (unsigned char)(gg << 1);
+        own[r * nb + bJ] = (unsigned char)(gg << 1 | 1);
+        prs[2 * (r * np + gg)] = (unsigned char)bI;
+        prs[2 * (r * np + gg) + 1] = (unsigned char)bJ;
+    }
+    const int vr0 = g * kCgVRows;
+    for (int e = t; e < nb * BW * kCgVP; e += blockDim.x) {
+        const int c = e / kCgVP, i = e % kCgVP;
+        Vs[e] = (i < kCgVRows && vr0 + i == c) ? 1.0 : 0.0;
+    }
+    if (t == 0) {
+        sflag[0] = sflag[1] = 0u;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(jb_smem(&inbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(jb_smem(&inbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // round 0's pair from global W (rows >= m and padded columns zero)
+    {
+        int bI, bJ;
+        pair_of(g, 0, bI, bJ);
+        for (int e = t; e < C2 * Mp; e += blockDim.x) {
+            const int c = e / Mp, i = e % Mp;
+            const int gc = c < BW ? bI * BW + c : bJ * BW + (c - BW);
+            Wb0[size_t(c) * P + i] = (gc < n && i < m) ? a.W[i + int64_t(gc) * a.ldw] : 0.0;
+        }
+    }
+    __syncthreads();
+    cg_sync();
+    cg_arrive_relaxed();  // pairs with round 0's wait
+    int sweep = 0, R = 0;
+    bool econv = false;
+    const bool clk = a.phase_clk != nullptr && g == 0 && t == 0;
+    long long ph[7] = {0, 0, 0, 0, 0, 0, 0}, c0 = clock64();
+    auto mark = [&](int i) {
+        if (clk) {
+            const long long c1 = clock64();
+            ph[i] += c1 - c0;
+            c0 = c1;
+        }
+    };
+    for (;;) {
+        if (sweep >= kOneSidedSweepCap) {
+            econv = true;
+            break;
+        }
+        for (int r = 0; r < nb; ++r, ++R) {
+            const bool intra = r == nb - 1;
+            int bI, bJ;
+            pair_of(g, r, bI, bJ);
+            double* Ws = Wb0 + size_t(R & 1) * C2 * P;
+            double* Wn = Wb0 + size_t((R & 1) ^ 1) * C2 * P;
+            // this round's columns (sent last round), then announce next round's
+            if (t == 0) {
+                if (R > 0) jb_mbar_wait(&inbar[R & 1], unsigned((R - 1) >> 1) & 1u);
+                asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                                 jb_smem(&inbar[(R & 1) ^ 1])),
+                             "r"(in_bytes)
+                             : "memory");
+            }
+            __syncthreads();
+            mark(0);
+            // ---- 1. Gram of the resident pair --------------------------------
+            bgram_gram<BW>(Ws, P, Mp, Pb, G0, J);
+            __syncthreads();
+            mark(1);
+            // ---- 2. steps (the BW * BW pair-block owners) || V replay ---------
+            int rot = 0;
+            if (t < BW * BW) {
+                rot = bgram_steps<BW>(G0, J, intra);
+            } else if (sweep > 0) {
+                // round r of the previous sweep's log on this CTA's V rows:
+                // task = (8-row tile rt, pair gg), pairs own disjoint columns
+                const size_t base = (size_t((sweep - 1) & 1) * nb + r) * np;
+                for (int task = warp - (BW * BW) / 32; task < 2 * np; task += 8 - (BW * BW) / 32) {
+                    const int rt = task & 1, gg = task >> 1;
+                    if (!__ldcg(a.rlog + base + gg)) continue;
+                    const int cI = prs[2 * (r * np + gg)] * BW, cJ = prs[2 * (r * np + gg) + 1] * BW;
+                    const double* Jg = a.jlog + (base + gg) * C2 * C2;
+                    double af[KF], bf[KF][NB8];
+#pragma unroll
+                    for (int kf = 0; kf < KF; ++kf) {
+                        const int k = 4 * kf + lc;
+                        af[kf] = Vs[(k < BW ? cI + k : cJ + k - BW) * kCgVP + rt * 8 + lr];
+#pragma unroll
+                        for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = __ldcg(Jg + k * C2 + ct * 8 + lr);
+                    }
+#pragma unroll
+                    for (int ct = 0; ct < NB8; ++ct) {
+                        double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                        for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[kf], bf[kf][ct]);
+                        const int c = (ct == 0 ? cI : cJ) + 2 * lc;
+                        Vs[c * kCgVP + rt * 8 + lr] = o0;
+                        Vs[(c + 1) * kCgVP + rt * 8 + lr] = o1;
+                    }
+                }
+            }
+            rot = __syncthreads_or(rot);
+            mark(2);
+            // ---- 3. W_p J (or W_p) into the next owners' buffers; log J ------
+            const int rn = r + 1 == nb ? 0 : r + 1;
+            const unsigned oI = own[rn * nb + bI], oJ = own[rn * nb + bJ];
+            const unsigned dst[2] = {cg_map(Wn + size_t(oI & 1u) * BW * P, oI >> 1),
+                                     cg_map(Wn + size_t(oJ & 1u) * BW * P, oJ >> 1)};
+            const unsigned dbar[2] = {cg_map(&inbar[(R & 1) ^ 1], oI >> 1), cg_map(&inbar[(R & 1) ^ 1], oJ >> 1)};
+            const size_t slot = (size_t(sweep & 1) * nb + r) * np + g;
+            if (t == 0) a.rlog[slot] = rot ? 1 : 0;
+            if (rot) {
+                for (int e = t; e < C2 * C2; e += blockDim.x) {
+                    const double v = J[(e / C2) * GP + e % C2];
+                    Jb[(e / C2) * JP + e % C2] = v;
+                    a.jlog[slot * C2 * C2 + e] = v;
+                }
+                __syncthreads();
+            }
+            mark(3);
+            cg_wait();  // every CTA finished reading the buffers written below (round R - 1)
+            mark(4);
+            if (rot) {
+                double bf[KF][NB8];
+#pragma unroll
+                for (int kf = 0; kf < KF; ++kf)
+#pragma unroll
+                    for (int ct = 0; ct < NB8; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * JP + ct * 8 + lr];
+                for (int sl0 = 2 * warp; sl0 < Mp / 8; sl0 += 16) {  // Mp / 8 is a multiple of 4
+                    double af[2][KF];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+#pragma unroll
+                        for (int kf = 0; kf < KF; ++kf) af[u][kf] = Ws[(4 * kf + lc) * P + (sl0 + u) * 8 + lr];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                        for (int ct = 0; ct < NB8; ++ct) {
+                            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                            for (int kf = 0; kf < KF; ++kf) jac_dmma(o0, o1, af[u][kf], bf[kf][ct]);
+                            // o0 = out[lr][2lc], o1 = out[lr][2lc + 1]: trade with
+                            // lane ^ 4 so each lane holds two rows of one column
+                            const bool ev = (lr & 1) == 0;
+                            const double y = __shfl_xor_sync(0xffffffffu, ev ? o1 : o0, 4);
+                            const int cc = 2 * lc + (ev ? 0 : 1), row = (sl0 + u) * 8 + (lr & ~1);
+                            cg_st_async(dst[ct] + unsigned((cc * P + row) * 8), ev ? o0 : y, ev ? y : o1, dbar[ct]);
+                        }
+                    }
+                }
+            } else {
+                for (int e = 2 * t; e < C2 * Mp; e += 2 * blockDim.x) {
+                    const int c = e / Mp, i = e % Mp, h = c / BW, cc = c % BW;
+                    cg_st_async(dst[h] + unsigned((cc * P + i) * 8), Ws[size_t(c) * P + i], Ws[size_t(c) * P + i + 1],
+                                dbar[h]);
+                }
+            }
+            if (rot && t == 0)
+                asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cg_map(&sflag[sweep & 1], 0)), "r"(1u)
+                             : "memory");
+            if (r == 0 && g == 0 && t == 0) sflag[(sweep + 1) & 1] = 0u;  // read by all at the end of sweep - 1
+            __syncthreads();
+            mark(5);
+            if (r == nb - 1)
+                cg_arrive_release();  // the sweep's flag stores, for the read below
+            else
+                cg_arrive_relaxed();
+            mark(6);
+        }
+        cg_wait();
+        if (t == 0) {
+            unsigned v;
+            asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(v) : "r"(cg_map(&sflag[sweep & 1], 0)) : "memory");
+            s_stop = v == 0u;
+        }
+        cg_arrive_relaxed();
+        __syncthreads();
+        ++sweep;
+        if (s_stop || n < 2) break;
+    }
+    cg_wait();
+    // the resident pair (round 0's) back to W once its last columns arrived
+    if (t == 0 && R > 0) jb_mbar_wait(&inbar[R & 1], unsigned((R - 1) >> 1) & 1u);
+    __syncthreads();
+    {
+        int bI, bJ;
+        pair_of(g, 0, bI, bJ);
+        const double* Ws = Wb0 + size_t(R & 1) * C2 * P;
+        for (int e = t; e < C2 * m; e += blockDim.x) {
+            const int c = e / m, i = e % m;
+            const int gc = c < BW ? bI * BW + c : bJ * BW + (c - BW);
+            if (gc < n) a.W[i + int64_t(gc) * a.ldw] = Ws[size_t(c) * P + i];
+        }
+    }
+    for (int e = t; e < kCgVRows * n; e += blockDim.x) {
+        const int c = e / kCgVRows, i = e % kCgVRows;
+        if (vr0 + i < n) a.V[(vr0 + i) + int64_t(c) * a.ldv] = Vs[c * kCgVP + i];
+    }
+    if (g == 0 && t == 0) {
+        a.flags[4] = sweep;
+        if (econv) a.flags[3] = RLRA_ECONV;
+    }
+    if (clk)
+        for (int i = 0; i < 7; ++i) a.phase_clk[i] = ph[i];
 }
 
 __device__ __forceinline__ void sg_cp16(void* smem, const void* gmem) {
@@ -1653,6 +2040,54 @@ __global__ void asym_kernel(const double* T, int64_t ldt, int n, double* part) {
 
 }  // namespace
 
+// cluster launch of cgram_jacobi_kernel<8>: np = nb / 2 CTAs, one cluster
+cudaLaunchConfig_t cgram_config(Context& ctx, int np, size_t smem, cudaLaunchAttribute* attr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(np));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx.stream;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(np);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+void cgram_attrs(size_t smem) {
+    static size_t set = 0;
+    if (set < smem) {
+        RLRA_CUDA(cudaFuncSetAttribute(cgram_jacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        RLRA_CUDA(cudaFuncSetAttribute(cgram_jacobi_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        set = smem;
+    }
+}
+
+// can one cluster of np CTAs with this shared memory be resident?
+bool cgram_fits(Context& ctx, int np, size_t smem) {
+    static const bool off = std::getenv("RLRA_CGRAM_OFF") != nullptr;
+    if (off || np < 2 || np > 16) return false;
+    cgram_attrs(smem);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = cgram_config(ctx, np, smem, attr);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)cgram_jacobi_kernel<8>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return nclusters >= 1;
+}
+
+void launch_cgram(Context& ctx, const CGramArgs& c, size_t smem) {
+    cgram_attrs(smem);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = cgram_config(ctx, c.nb / 2, smem, attr);
+    RLRA_CUDA(cudaLaunchKernelEx(&cfg, cgram_jacobi_kernel<8>, c));
+    RLRA_LAUNCH_CHECK();
+}
+
 void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& Vout) {
     const int m = int(A.rows), n = int(A.cols);
     if (n == 0) return;
@@ -1664,7 +2099,8 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         const char* e = std::getenv("RLRA_SVD_KERNEL");
         if (!e) return 0;
         const std::string v(e);
-        return v == "bgram" ? 1 : v == "block" ? 2 : v == "sgram" ? 3 : v == "onesided" ? 4 : v == "gram" ? 5 : 0;
+        return v == "bgram" ? 1 : v == "block" ? 2 : v == "sgram" ? 3 : v == "onesided" ? 4 : v == "gram" ? 5
+             : v == "cgram" ? 6 : 0;
     }();
     constexpr size_t kSmemCap = 220 * 1024;
     // blocks of 8 columns: twice the CTAs of 16-column blocks, and the
@@ -1673,7 +2109,12 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     static const int bw_env = std::getenv("RLRA_BGRAM_BW") ? std::atoi(std::getenv("RLRA_BGRAM_BW")) : 0;
     int bgw = (n > 16 && bgram_smem<8>(m) <= kSmemCap) ? 8 : 0;
     if (bw_env == 16 && n > 32 && bgram_smem<16>(m) <= kSmemCap) bgw = 16;
-    const bool use_bgram = (forced == 0 || forced == 1) && bgw > 0;
+    bool use_bgram = (forced == 0 || forced == 1) && bgw > 0;
+    // one cluster of pair CTAs when the blocks of 8 fit 16 of them (l <= 256):
+    // W stays in shared memory (RLRA_SVD_KERNEL=bgram keeps the L2 variant)
+    const int cnb = ceil_div(n, 8) + (ceil_div(n, 8) & 1);
+    const bool use_cgram = (forced == 0 || forced == 6) && n > 16 && cnb <= 32 && cgram_smem<8>(m, cnb) <= kSmemCap &&
+                           cgram_fits(ctx, cnb / 2, cgram_smem<8>(m, cnb));
     const int snb = ceil_div(n, kSGB) + (ceil_div(n, kSGB) & 1);
     const bool use_sgram = !use_bgram && forced != 2 && forced != 4 && forced != 5 && n > 2 * kSC2 &&
                            snb / 2 <= ctx.num_sms && m >= 2 * kSCR;
@@ -1704,6 +2145,25 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
     a.V = V.m.p;
     a.ldv = V.m.ld;
     a.flags = flags.i();
+    if (use_cgram) {
+        static const bool want_clk = std::getenv("RLRA_JACOBI_PHASES") != nullptr;
+        Buf clkb(ctx, want_clk ? sizeof(long long) * 8 : 8);
+        const size_t slots = size_t(2) * cnb * (cnb / 2);
+        Buf jlog(ctx, sizeof(double) * slots * 256), rlog(ctx, slots);
+        CGramArgs c{W.m.p, W.m.ld, m,     n, cnb, V.m.p, V.m.ld, jlog.d(), static_cast<unsigned char*>(rlog.p), flags.i(),
+                    want_clk ? reinterpret_cast<long long*>(clkb.p) : nullptr};
+        launch_cgram(ctx, c, cgram_smem<8>(m, cnb));
+        if (want_clk) {
+            long long h[7];
+            RLRA_CUDA(cudaMemcpyAsync(h, clkb.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+            RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+            std::fprintf(stderr,
+                         "cgram<8> m=%d n=%d clocks: wait_in %lld gram %lld steps %lld jlog %lld cl_wait %lld send %lld "
+                         "arrive %lld\n",
+                         m, n, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+        }
+        goto launched;
+    }
     if (use_bgram) {
         GramJacArgs g;
         g.bar = ctx.gbar;
