@@ -969,14 +969,16 @@ __device__ __forceinline__ void bgram_gram(const double* Ws, int P, int Mp, doub
 // parameter phase), updates its G block into the other buffer and its J block
 // in place — one barrier (named barrier 1 unless BW*BW == 256) per step.
 // Returns whether any pair rotated (the same value on every caller thread).
-template <int BW>
-__device__ __forceinline__ int bgram_steps(double* G0, double* J, bool intra) {
+template <int BW, bool INTRA>
+__device__ __forceinline__ int bgram_steps_t(double* G0, double* J) {
+    constexpr bool intra = INTRA;
     using B = BGram<BW>;
     constexpr int C2 = B::C2, GP = B::GP;
     const int t = threadIdx.x;
     int rot = 0;
     const int k = t / BW, l = t % BW;
-    const int nsteps = intra ? BW - 1 : BW;
+    constexpr int nsteps = INTRA ? BW - 1 : BW;
+#pragma unroll
     for (int st = 0; st < nsteps; ++st) {
         const double* Gc = G0 + (st & 1) * C2 * GP;
         double* Gn = G0 + ((st & 1) ^ 1) * C2 * GP;
@@ -994,6 +996,7 @@ __device__ __forceinline__ int bgram_steps(double* G0, double* J, bool intra) {
             if (!okk) ak = jac_rotation_ref(kpp, kqq, kpq, ck, sk);
             if (!okl) al = jac_rotation_ref(lpp, lqq, lpq, cl, sl);
             act = (k == l) ? ak : 0;
+            rot |= act;
             if (al) {  // J <- J R_l on rows {pk, qk}
                 const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
                 const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
@@ -1025,9 +1028,17 @@ __device__ __forceinline__ int bgram_steps(double* G0, double* J, bool intra) {
                 Gn[ql * GP + qk] = b11;
             }
         }
-        rot |= (BW * BW == 256) ? __syncthreads_or(act) : bar_or_partial(BW * BW, act);
+        // plain barrier per step; the rotation flags are OR-reduced once below
+        if (BW * BW == 256)
+            __syncthreads();
+        else
+            asm volatile("bar.sync 1, %0;\n" ::"n"(BW * BW) : "memory");
     }
-    return rot;
+    return (BW * BW == 256) ? __syncthreads_or(rot) : bar_or_partial(BW * BW, rot);
+}
+template <int BW>
+__device__ __forceinline__ int bgram_steps(double* G0, double* J, bool intra) {
+    return intra ? bgram_steps_t<BW, true>(G0, J) : bgram_steps_t<BW, false>(G0, J);
 }
 
 // V(rows, cols of the pair) <- V * Jb on DMMA, read and written through L2
