@@ -309,7 +309,19 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
         ++ctx.launches;
         return;
     }
-    const bool big = M >= 96 && N >= 96;
+    // 128 x 128 tiles unless they leave most SMs idle with little k to split:
+    // an l x l Gram (<= 4 big tiles) or a short-k product (k <= 1024) of
+    // fewer than 100 big tiles runs on 64 x 64 tiles, up to three CTAs per SM
+    // (C1: the k = 210 products 40 -> 20 us, its Grams 32 -> 24 us; the
+    // long-k sketch products stay faster on big tiles).
+    // RLRA_GEMM_BIG_MIN_TILES=t replaces the rule by "big iff >= t tiles".
+    static const int big_min_tiles = [] {
+        const char* e = std::getenv("RLRA_GEMM_BIG_MIN_TILES");
+        return e ? std::atoi(e) : -1;
+    }();
+    const int64_t big_tiles = int64_t(ceil_div(M, CfgBig::BM)) * ceil_div(N, CfgBig::BN);
+    const bool few = big_min_tiles >= 0 ? big_tiles < big_min_tiles : (big_tiles <= 4 || (big_tiles < 100 && K <= 1024));
+    const bool big = M >= 96 && N >= 96 && !few;
     const int BM = big ? CfgBig::BM : CfgSmall::BM;
     const int BN = big ? CfgBig::BN : CfgSmall::BN;
     const int BK = 16;

@@ -377,17 +377,20 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
             long long c_0 = clock64();
             // The serial chain per column is barrier -> pivot load -> 1/d ->
             // f -> the next pivot row's update -> store: the pivot test is
-            // branch-free, dref is read before the barrier, and 1/d comes from
-            // MUFU.RCP64H + three Newton steps (no slow-path guard).
+            // off the chain (1/d of max(d, 1e-300) unconditionally), 1/d comes
+            // from MUFU.RCP64H + three Newton steps, and the column loop is
+            // unrolled so which rows are still active, and who publishes the
+            // next pivot row, are compile-time facts (rows below the diagonal
+            // of the thread's column are updated too: never read, written as 0)
             bool all_ok = true;
-            for (int k = 0; k < nb; ++k) {
+#pragma unroll
+            for (int k = 0; k < kCholNB; ++k) {
                 const double dr = dref[k];
                 __syncthreads();
-                double d = s0[k][k];
+                const double d0 = s0[k][k];
                 const double skc = s0[k][cj];
-                const bool ok = (d > 0.0) && (d >= dr);
-                all_ok = all_ok && ok;
-                d = ok ? d : fmax(d, 1e-300);
+                all_ok = all_ok && (d0 > 0.0) && (d0 >= dr);
+                const double d = fmax(d0, 1e-300);
                 double rd;
                 asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(d));
                 double er = fma(-d, rd, 1.0);
@@ -399,13 +402,10 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
                 const double f = skc * rd;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const int i = rg + 4 * u;
-                    if (i > k && i <= cj) v[u] -= s0[k][i] * f;
+                    if (4 * u + 3 <= k) continue;  // rows rg + 4u <= k: done
+                    if (4 * u > k || rg + 4 * u > k) v[u] -= s0[k][rg + 4 * u] * f;
                 }
-                const int kn = k + 1;
-#pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (rg + 4 * u == kn) s0[kn][cj] = v[u];
+                if (k + 1 < kCholNB && rg == (k + 1) % 4) s0[k + 1][cj] = v[(k + 1) / 4];
                 if (t == 0) piv[k] = d;
             }
             if (t == 0 && !all_ok) bad = 1;

@@ -1,0 +1,31 @@
+"""Every profiled call of one C1 rsvd_v2 (2000 x 4000, k = 200, p = 10,
+q = 2) with its shape and device ms: where the C1 latency goes, GEMM by
+GEMM.  Prints one line per record and the per-name sums."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1502_05366_b200 as R
+from paper_1502_05366_b200.testmat import gen_test_matrix_device
+
+eng = R.Engine(0)
+m, n, k, p, q = 2000, 4000, 200, 10, 2
+A, _ = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(min(m, n)) / 20.0), seed=1)
+U = torch.empty(m * k, dtype=torch.float64, device="cuda")
+V = torch.empty(n * k, dtype=torch.float64, device="cuda")
+S = torch.empty(k, dtype=torch.float64, device="cuda")
+run = lambda: eng.device_rsvd(R.RSVD_V2, A.data_ptr(), m, n, m, k, p, q, 1, R.Omega.philox(12345), U.data_ptr(),
+                              S.data_ptr(), V.data_ptr())
+run()
+eng.synchronize()
+eng.profile(True)
+run()
+eng.synchronize()
+recs = eng.profile_records()
+eng.profile(False)
+for r in recs:
+    print(f"{r['name']:12s} M={r['M']:6d} N={r['N']:6d} K={r['K']:6d} {r['ms']*1e3:8.1f} us"
+          + (f" {r['flops'] / r['ms'] / 1e9:6.2f} TF/s" if r['flops'] > 0 else ""))
