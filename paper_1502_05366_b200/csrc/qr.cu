@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
             bool all_ok = true;
 #pragma unroll
             for (int k = 0; k < kCholNB; ++k) {
+                if (k >= nb) break;  // the rest is identity padding
                 const double dr = dref[k];
                 __syncthreads();
                 const double d0 = s0[k][k];
@@ -529,44 +530,44 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
 // the cooperative kernel on a diagonal block of a larger Cholesky: pivot
 // references from the caller's original diagonal, breakdown into the caller's
 // flag, no host synchronisation
-void chol_coop_block(Context& ctx, const DMat& G, const DMat& Rinv, double floor, double* dorig, int* flag) {
-    constexpr int smem = 2 * kCholNB * kCP * sizeof(double);
+constexpr int kCholSmem = 2 * kCholNB * kCP * sizeof(double);
+int chol_grid_cap(Context& ctx) {
     static int grid_cap = 0;
     if (!grid_cap) {
-        RLRA_CUDA(cudaFuncSetAttribute(chol_inv_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RLRA_CUDA(cudaFuncSetAttribute(chol_inv_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem));
         int per_sm = 0;
-        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_inv_coop_kernel, 256, smem));
+        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_inv_coop_kernel, 256, kCholSmem));
         grid_cap = std::max(1, per_sm) * ctx.num_sms;
     }
-    CholCoopArgs a{ctx.gbar, G.p, G.ld, int(G.rows), Rinv.p, Rinv.ld, dorig, floor, flag, nullptr, 1};
+    return grid_cap;
+}
+
+void launch_chol(Context& ctx, CholCoopArgs& a, int grid) {
     void* args[] = {&a};
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)chol_inv_coop_kernel, dim3(std::min(grid_cap, ctx.num_sms)),
-                                          dim3(256), args, smem, ctx.stream));
+    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)chol_inv_coop_kernel, dim3(grid), dim3(256), args, kCholSmem,
+                                          ctx.stream));
     ++ctx.launches;
 }
 
-bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
+void chol_coop_block(Context& ctx, const DMat& G, const DMat& Rinv, double floor, double* dorig, int* flag) {
+    const int grid_cap = chol_grid_cap(ctx);
+    CholCoopArgs a{ctx.gbar, G.p, G.ld, int(G.rows), Rinv.p, Rinv.ld, dorig, floor, flag, nullptr, 1};
+    launch_chol(ctx, a, std::min(grid_cap, ctx.num_sms));
+}
+
+bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double floor, int* dflag) {
     const int n = int(G.rows);
-    constexpr int smem = 2 * kCholNB * kCP * sizeof(double);
-    static int grid_cap = 0;
-    if (!grid_cap) {
-        RLRA_CUDA(cudaFuncSetAttribute(chol_inv_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int per_sm = 0;
-        RLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_inv_coop_kernel, 256, smem));
-        grid_cap = std::max(1, per_sm) * ctx.num_sms;
-    }
-    Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
-    RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    const int grid_cap = chol_grid_cap(ctx);
+    Buf dorig(ctx, sizeof(double) * n), flag(ctx, dflag ? 0 : sizeof(int));
+    if (!dflag) RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
     static unsigned long long* tprobe = nullptr;
     static bool want_probe = getenv("RLRA_CHOL_PROBE") != nullptr;
     if (want_probe && !tprobe) RLRA_CUDA(cudaMallocManaged(&tprobe, 64 * 8));
-    CholCoopArgs a{ctx.gbar, G.p, G.ld, n, Rinv.p, Rinv.ld, dorig.d(), floor, flag.i(), tprobe, 0};
-    void* args[] = {&a};
+    CholCoopArgs a{ctx.gbar, G.p, G.ld, n, Rinv.p, Rinv.ld, dorig.d(), floor, dflag ? dflag : flag.i(), tprobe, 0};
     static const int grid_env = getenv("RLRA_CHOL_GRID") ? atoi(getenv("RLRA_CHOL_GRID")) : 0;
     const int grid = grid_env > 0 ? std::min(grid_env, grid_cap) : std::min(grid_cap, ctx.num_sms);
-    RLRA_CUDA(cudaLaunchCooperativeKernel((void*)chol_inv_coop_kernel, dim3(grid), dim3(256), args, smem,
-                                          ctx.stream));
-    ++ctx.launches;
+    launch_chol(ctx, a, grid);
+    if (dflag) return true;  // the caller reads the flag later
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
     if (tprobe) fprintf(stderr, "phase A cycles: factor %llu\n", tprobe[50]);
@@ -580,13 +581,14 @@ bool chol_upper_inv_coop(Context& ctx, const DMat& G, const DMat& Rinv, double f
 
 }  // namespace
 
-bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor) {
+bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor, int* dflag) {
     ProfScope prof(ctx, "chol", int(G.rows), int(G.rows), 0, 0.0);
     GemmTag tag(ctx, "gemm_chol");
     const int n = int(G.rows);
-    if (n <= kCholCoopMax && !ctx.chol_blocked_gemm) return chol_upper_inv_coop(ctx, G, Rinv, floor);
-    Buf dorig(ctx, sizeof(double) * n), flag(ctx, sizeof(int));
-    RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    if (n <= kCholCoopMax && !ctx.chol_blocked_gemm) return chol_upper_inv_coop(ctx, G, Rinv, floor, dflag);
+    Buf dorig(ctx, sizeof(double) * n), flag(ctx, dflag ? 0 : sizeof(int));
+    if (!dflag) RLRA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    int* fl = dflag ? dflag : flag.i();
     diag_copy_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(G.p, G.ld, n, dorig.d());
     RLRA_LAUNCH_CHECK();
     ++ctx.launches;
@@ -607,12 +609,12 @@ bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor)
                 attr = true;
             }
             chol_diag_kernel<<<1, 256, smem, ctx.stream>>>(G.p, G.ld, j0, nb, Rinv.p, Rinv.ld, dorig.d(),
-                                                        floor, flag.i());
+                                                        floor, fl);
             RLRA_LAUNCH_CHECK();
             ++ctx.launches;
         } else {
             chol_coop_block(ctx, G.block(j0, j0, nb, nb), Rinv.block(j0, j0, nb, nb), floor, dorig.d() + j0,
-                            flag.i());
+                            fl);
         }
         if (j1 < n) {
             const int rest = n - j1;
@@ -638,6 +640,7 @@ bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor)
         gemm(ctx, Op::N, Op::N, 1.0, Rinv.block(0, 0, j0, j0), G.block(0, j0, j0, nb), 0.0, T);
         gemm(ctx, Op::N, Op::N, -1.0, T, Rinv.block(j0, j0, nb, nb), 0.0, Rinv.block(0, j0, j0, nb));
     }
+    if (dflag) return true;
     int h_flag = 0;
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -779,27 +782,30 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
         raise(RLRA_EDIM, fmt("compact_qr: matrix is %dx%d, need rows >= cols", m, n));
     QrResult res;
     if (n == 0) return res;
-    // pass 1: G1 = Y^T Y, R1, R1^{-1}
+    // pass 1: G1 = Y^T Y, R1, R1^{-1}; pass 2 on Q1 = Y R1^{-1}.  Y is only
+    // written after both Cholesky factorizations succeeded, so their
+    // breakdown flags are read once, after pass 2 (one host sync per orth)
     DMatBuf G1(ctx, n, n), R1i(ctx, n, n);
+    Buf bad(ctx, sizeof(int));
+    RLRA_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx.stream));
     GemmOpts sy;
     sy.upper_tiles_only = true;
     gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, G1, sy);
-    if (!chol_upper_inv(ctx, G1, R1i, ctx.cholqr_pivot_floor)) {
-        // Small problems take the reference's own algorithm (Householder,
-        // columnwise backward stable: resolves the tiny singular values the
-        // reference's tests probe, test_rsvd.cpp:188-202); large
-        // ill-conditioned ones take shifted CholQR3, Householder last.
-        if (int64_t(m) * n > (int64_t(1) << 20) && shifted_cholqr3(ctx, Y, R)) return res;
-        return householder_qr(ctx, Y, R);
-    }
+    chol_upper_inv(ctx, G1, R1i, ctx.cholqr_pivot_floor, bad.i());
     DMatBuf Q1(ctx, m, n);
     GemmOpts tri;
     tri.tri_b_upper = true;
     gemm(ctx, Op::N, Op::N, 1.0, Y, R1i, 0.0, Q1, tri);
-    // pass 2 on Q1
     DMatBuf G2(ctx, n, n), R2i(ctx, n, n);
     gemm(ctx, Op::T, Op::N, 1.0, Q1, Q1, 0.0, G2, sy);
-    if (!chol_upper_inv(ctx, G2, R2i, ctx.cholqr_pivot_floor)) {
+    chol_upper_inv(ctx, G2, R2i, ctx.cholqr_pivot_floor, bad.i());
+    RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (ctx.h_flags[0] != 0) {
+        // Small problems take the reference's own algorithm (Householder,
+        // columnwise backward stable: resolves the tiny singular values the
+        // reference's tests probe, test_rsvd.cpp:188-202); large
+        // ill-conditioned ones take shifted CholQR3, Householder last.
         if (int64_t(m) * n > (int64_t(1) << 20) && shifted_cholqr3(ctx, Y, R)) return res;
         return householder_qr(ctx, Y, R);
     }

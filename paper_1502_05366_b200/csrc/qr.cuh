@@ -52,7 +52,9 @@ void form_q(Context& ctx, const double* V, int64_t ldv, const double* beta, int 
 // Upper Cholesky of a symmetric positive-definite G (n x n, upper triangle
 // read) in place: G <- R (upper, lower zeroed), Rinv <- R^{-1}.  Returns false
 // when a pivot fell below floor * original diagonal (or was not positive).
-bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor);
+// dflag (device int, zeroed by the caller): OR the breakdown into it and
+// return true without a host synchronisation; the caller reads it later.
+bool chol_upper_inv(Context& ctx, const DMat& G, const DMat& Rinv, double floor, int* dflag = nullptr);
 
 // G(i, i) += s
 void add_diag(Context& ctx, const DMat& G, double s);
