@@ -271,6 +271,41 @@ def test_small_svd_variants_agree(eng, env):
     assert rel_fro((u * s) @ v.T, a) <= 1e-12
 
 
+@pytest.mark.parametrize("m,n,kind", [(256, 256, "graded"), (210, 210, "graded"), (300, 100, "deficient"),
+                                      (520, 17, "gauss"), (130, 129, "scaled"), (250, 250, "gauss")])
+def test_small_svd_cluster_kernel_bit_identical(eng, tmp_path, m, n, kind):
+    """l <= 256 runs the cluster-resident kernel (W in shared memory, st.async
+    exchange, V replayed from the rotation log); it performs the L2 variant's
+    arithmetic in the same order, so U, sigma and V are bit-identical to
+    RLRA_SVD_KERNEL=bgram's (a separate process: the choice is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    rs = np.random.default_rng(m * 13 + n)
+    a = rs.standard_normal((m, n))
+    if kind == "graded":
+        q1, _ = np.linalg.qr(rs.standard_normal((m, n)))
+        q2, _ = np.linalg.qr(rs.standard_normal((n, n)))
+        a = (q1 * np.exp(-np.arange(n) / 20.0)) @ q2.T
+    elif kind == "deficient":
+        a[:, 10:20] = 0.0
+        a[:, 30:40] = a[:, 50:60]
+    elif kind == "scaled":
+        a = a * 10.0 ** (-np.arange(n) * 30.0 / n)
+    np.save(tmp_path / "a.npy", a)
+    u, s, v = eng.small_svd(a)
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1502_05366_b200 as R; "
+            "a = np.load(%r); u, s, v = R.Engine(0).small_svd(a); np.savez(%r, u=u, s=s, v=v)"
+            % (ROOT, str(tmp_path / "a.npy"), str(tmp_path / "b.npz")))
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RLRA_SVD_KERNEL": "bgram"},
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    b = np.load(tmp_path / "b.npz")
+    assert np.array_equal(s, b["s"]) and np.array_equal(u, b["u"]) and np.array_equal(v, b["v"])
+    assert orthonormality_defect(u) <= 1e-11 and orthonormality_defect(v) <= 1e-11
+
+
 def test_small_svd_kats(eng):
     _, s, _ = eng.small_svd(np.diag([2.0, -3.0]))
     assert np.allclose(s, [3.0, 2.0], rtol=1e-15)  # test_jacobi.cpp:95-101

@@ -1,2 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_all.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/gpu_all.log
-python tools/run_configs.py C1 C2 C3 C4 C5 > gpurun_out/cfg_r2c.jsonl 2>gpurun_out/cfg_r2c.err; cat gpurun_out/cfg_r2c.jsonl | cut -c1-330
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -p no:cacheprovider -k "small_svd" > gpurun_out/p12.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/p12.log

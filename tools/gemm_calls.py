@@ -1,6 +1,6 @@
-"""Every profiled call of one C1 rsvd_v2 (2000 x 4000, k = 200, p = 10,
-q = 2) with its shape and device ms: where the C1 latency goes, GEMM by
-GEMM.  Prints one line per record and the per-name sums."""
+"""Every profiled call of one rsvd_v2 at C1 (2000 x 4000, k = 200, p = 10,
+q = 2; default) or C5 (argument "C5": 200000 x 20000, k = 500, p = 10,
+q = 2) with its shape and device ms: where the time goes, GEMM by GEMM."""
 import os
 import sys
 
@@ -12,8 +12,11 @@ import paper_1502_05366_b200 as R
 from paper_1502_05366_b200.testmat import gen_test_matrix_device
 
 eng = R.Engine(0)
-m, n, k, p, q = 2000, 4000, 200, 10, 2
-A, _ = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(min(m, n)) / 20.0), seed=1)
+if len(sys.argv) > 1 and sys.argv[1] == "C5":
+    m, n, k, p, q, dec = 200000, 20000, 500, 10, 2, 100.0
+else:
+    m, n, k, p, q, dec = 2000, 4000, 200, 10, 2, 20.0
+A, _ = gen_test_matrix_device(eng, m, n, np.exp(-np.arange(min(m, n)) / dec), seed=1)
 U = torch.empty(m * k, dtype=torch.float64, device="cuda")
 V = torch.empty(n * k, dtype=torch.float64, device="cuda")
 S = torch.empty(k, dtype=torch.float64, device="cuda")
