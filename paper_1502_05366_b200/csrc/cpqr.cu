@@ -596,11 +596,12 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
     const int cpb = (n + G - 1) / G;
     const int j0 = g * cpb, j1 = min(n, j0 + cpb), nown = max(0, j1 - j0);
     const int nreg = kResRegCols * nw;  // local columns [0, nreg) in registers
+    const int UR = (m + 31) >> 5, MP = 32 * UR;  // row chunks; shared-memory column pitch (rows >= m zero)
     double* vsh = rsm;                   // m: H_f's vector
     double* cnS = vsh + m;               // cpb
     double* rnS = cnS + cpb;             // cpb
-    double* colS = rnS + cpb;            // (cpb - nreg) x m shared-memory columns
-    int* posS = reinterpret_cast<int*>(colS + size_t(max(0, cpb - nreg)) * m);  // cpb positions
+    double* colS = rnS + cpb;            // (cpb - nreg) x MP shared-memory columns
+    int* posS = reinterpret_cast<int*>(colS + size_t(max(0, cpb - nreg)) * MP);  // cpb positions
     __shared__ double sv[32], st[32], shb[32];
     __shared__ int sp[32], ss[32];
     __shared__ int s_piv, s_spv, s_win, s_best_c;
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
         }
     }
     for (int c = nreg; c < nown; ++c)
-        for (int i = t; i < m; i += blockDim.x) colS[size_t(c - nreg) * m + i] = a.W[i + int64_t(j0 + c) * a.ldw];
+        for (int i = t; i < MP; i += blockDim.x) colS[size_t(c - nreg) * MP + i] = i < m ? a.W[i + int64_t(j0 + c) * a.ldw] : 0.0;
     for (int c = t; c < cpb; c += blockDim.x) posS[c] = j0 + c;
     __syncthreads();
 
@@ -672,7 +673,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
                     }
             }
         } else if (c >= nreg) {
-            for (int i = t; i < m; i += blockDim.x) __stcg(dst + i, colS[size_t(c - nreg) * m + i]);
+            for (int i = t; i < m; i += blockDim.x) __stcg(dst + i, colS[size_t(c - nreg) * MP + i]);
         }
     };
 
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
             for (int u = 0; u < kResRows; ++u) {
                 const int i = lane + 32 * u;
                 if (i < m) {
-                    const double x = colS[size_t(c - nreg) * m + i];
+                    const double x = colS[size_t(c - nreg) * MP + i];
                     sum += x * x;
                 }
             }
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
                 }
         } else {
             for (int i = pend_f + t; i < m; i += blockDim.x)
-                colS[size_t(pend_c - nreg) * m + i] = (i == pend_f) ? pend_alpha : 0.0;
+                colS[size_t(pend_c - nreg) * MP + i] = (i == pend_f) ? pend_alpha : 0.0;
         }
         pend_c = -1;
     };
@@ -921,19 +922,23 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
             for (int b = 0; b < 2; ++b) {
                 pos[b] = cc[b] < nown ? posS[cc[b]] : -1;
                 on[b] = cc[b] < nown && pos[b] > f;
-                col[b] = colS + size_t((on[b] ? cc[b] : nreg) - nreg) * m;
+                col[b] = colS + size_t((on[b] ? cc[b] : nreg) - nreg) * MP;
             }
             if (!on[0] && !on[1]) continue;
             if (beta != 0.0) {
+                // no row predicates: v is zero outside [f, m) and the padded
+                // rows are zero, so rows < f add +-0 to the dot products and
+                // keep their bits in the update — the same sums and values as
+                // restricting to [f, m); only the warp-uniform chunk bound UR
                 double sd[2] = {0.0, 0.0};
+                const double* p0 = col[0] + lane;
+                const double* p1 = col[1] + lane;
 #pragma unroll
-                for (int u = 0; u < kResRows; ++u) {
-                    const int i = lane + 32 * u;
-                    if (i >= f && i < m) {
-#pragma unroll
-                        for (int b = 0; b < 2; ++b) sd[b] += vr[u] * col[b][i];
+                for (int u = 0; u < kResRows; ++u)
+                    if (u < UR) {
+                        sd[0] += vr[u] * p0[32 * u];
+                        sd[1] += vr[u] * p1[32 * u];
                     }
-                }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -942,11 +947,10 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
                 for (int b = 0; b < 2; ++b) {
                     if (!on[b]) continue;
                     const double fct = beta * sd[b];
+                    double* pb = col[b] + lane;
 #pragma unroll
-                    for (int u = 0; u < kResRows; ++u) {
-                        const int i = lane + 32 * u;
-                        if (i >= f && i < m) col[b][i] -= fct * vr[u];
-                    }
+                    for (int u = 0; u < kResRows; ++u)
+                        if (u < UR) pb[32 * u] -= fct * vr[u];
                 }
                 __syncwarp();
             }
@@ -997,7 +1001,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cpqr_res_kernel(CpqrArgs a) {
         }
     }
     for (int c = nreg; c < nown; ++c)
-        for (int i = t; i < m; i += blockDim.x) a.W[i + int64_t(j0 + c) * a.ldw] = colS[size_t(c - nreg) * m + i];
+        for (int i = t; i < m; i += blockDim.x) a.W[i + int64_t(j0 + c) * a.ldw] = colS[size_t(c - nreg) * MP + i];
     for (int c = t; c < nown; c += blockDim.x) a.perm[posS[c]] = j0 + c;
     if (g == 0 && t == 0) {
         a.out[0] = frank;
@@ -1139,7 +1143,8 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     static const bool res_env = !(std::getenv("RLRA_CPQR_RESIDENT") && std::getenv("RLRA_CPQR_RESIDENT")[0] == '0');
     const int Gr = std::min(ctx.num_sms, std::max(1, n));
     const int cpb_r = ceil_div(n, Gr), nreg_r = kResRegCols * (kResThreads / 32);
-    const size_t res_smem = sizeof(double) * (size_t(m) + 2 * size_t(cpb_r) + size_t(std::max(0, cpb_r - nreg_r)) * m) +
+    const size_t res_smem = sizeof(double) * (size_t(m) + 2 * size_t(cpb_r) +
+                                              size_t(std::max(0, cpb_r - nreg_r)) * size_t(32 * ceil_div(m, 32))) +
                             sizeof(int) * size_t(cpb_r);
     bool resident = res_env && !two_bar && m <= 32 * kResRows && res_smem <= 224 * 1024;
     if (resident) {
