@@ -445,6 +445,12 @@ struct GramJacArgs {
     unsigned* mod;                 // [nb] stamp of the block's last modification
     unsigned* clean;               // [nb * nb + nb / 2] stamp of the pair's last rotation-free visit
     unsigned long long* counters;  // [0] visits, [1] skipped, [2] rotating
+    // sgram: V updates ordered apart from W (zeroed per call): vtick[b] = V
+    // updates of block b handed out (advanced by the W-chain owner),
+    // vdone[b] = V updates of block b completed
+    unsigned* vtick;
+    unsigned* vdone;
+    unsigned* tasks;  // sgram: [sweep cap] visit counters (zeroed per call)
 };
 
 // ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
@@ -1639,7 +1645,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
     const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
     const int ncw = int(a.ldw / kSCR), ncv = int(a.ldv / kSCR);  // chunks of W / V columns
     volatile int* flags = a.flags;
-    unsigned R = 0;
+    __shared__ int s_task;
     // ring counters (identical in every thread): qn chunks issued (one
     // cp.async group each), qu consumed; chunk q uses stage q % kSNST
     unsigned qn = 0, qu = 0;
@@ -1650,9 +1656,22 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
             break;
         }
         if (blockIdx.x == 0 && t == 0) flags[(sweep + 1) % 3] = 0;
-        for (int r = 0; r < nb; ++r) {
-            const bool intra = r == nb - 1;
-            for (int g = blockIdx.x; g < np; g += gridDim.x) {
+        // dynamic schedule: CTAs take the sweep's (round, pair) visits in
+        // order from a counter, so a CTA whose visit was cheap (nothing
+        // rotated, or skipped) runs ahead into the next round's ready pairs
+        // instead of idling until its fixed pair slot's inputs arrive.  Every
+        // visit with a smaller index is held by a running CTA, so the version
+        // waits below always resolve.
+        for (;;) {
+            {
+                if (t == 0) s_task = int(atomicAdd(a.tasks + sweep, 1u));
+                __syncthreads();
+                const int task = s_task;
+                __syncthreads();
+                if (task >= nb * np) break;
+                const int r = task / np, g = task % np;
+                const unsigned R = unsigned(sweep) * unsigned(nb) + unsigned(r);  // the visit's global round
+                const bool intra = r == nb - 1;
                 int bI = 2 * g, bJ = 2 * g + 1;
                 if (!intra) {
                     const int b1 = rr_col(g, r, nb), b2 = rr_col(nb - 1 - g, r, nb);
@@ -1679,8 +1698,9 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     continue;
                 }
                 // the visit's chunk sequence: [0, ncw) Gram of W, [ncw, 2 ncw)
-                // W for the apply, [2 ncw, 2 ncw + ncv) V for the apply
-                const int kend = 2 * ncw + ncv;
+                // W for the apply, [2 ncw, 2 ncw + ncv) V for the apply (issued
+                // only once the pair's V blocks are current, see step 3)
+                int kend = 2 * ncw;
                 int kin = 0;  // next sequence position to issue
                 auto issue = [&]() {  // sequence position kin into stage qn % kSNST (all threads)
                     const int k = kin;
@@ -1839,11 +1859,40 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     for (int kf = 0; kf < kSC2 / 4; ++kf)
 #pragma unroll
                         for (int ct = 0; ct < 3; ++ct) bf[kf][ct] = Jb[(4 * kf + lc) * kSJP + wc * 24 + ct * 8 + lr];
+                    __shared__ unsigned s_tick[2];
                     for (int mat = 0; mat < 2; ++mat) {
                         double* X = mat == 0 ? a.W : a.V;
                         const int64_t ld = mat == 0 ? a.ldw : a.ldv;
                         const int rows = mat == 0 ? m : n;
                         const int nch = mat == 0 ? ncw : ncv;
+                        if (mat == 1) {
+                            // W_p J is out: publish W now, so the blocks' next
+                            // owners start their Grams while this CTA does V_p J.
+                            // V keeps its own order: this pair's V update is the
+                            // s_tick-th of each block; wait for the earlier ones
+                            __syncthreads();
+                            if (t == 0) {
+                                s_tick[0] = __ldcg(a.vtick + bI);
+                                s_tick[1] = __ldcg(a.vtick + bJ);
+                                __stcg(a.vtick + bI, s_tick[0] + 1u);
+                                __stcg(a.vtick + bJ, s_tick[1] + 1u);
+                                __stcg(a.mod + bI, R + 1u);
+                                __stcg(a.mod + bJ, R + 1u);
+                                atomicAdd(a.counters + 2, 1ull);
+                                __threadfence();
+                                jb_publish(a.ver + bI, R + 1);
+                                jb_publish(a.ver + bJ, R + 1);
+                                jb_wait_at_least(a.vdone + bI, s_tick[0]);
+                                jb_wait_at_least(a.vdone + bJ, s_tick[1]);
+                                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                            }
+                            __syncthreads();
+                            kend = 2 * ncw + ncv;
+                            for (; qn - qu < unsigned(kSNST - 1) && kin < kend; ++qn, ++kin) {
+                                issue();
+                                sg_commit();
+                            }
+                        }
                         for (int ch = 0; ch < nch; ++ch) {
                             const int k0 = ch * kSCR;
                             consume([&](const double* Cb) {
@@ -1876,6 +1925,12 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             });
                         }
                     }
+                    __syncthreads();
+                    if (t == 0) {
+                        __threadfence();
+                        jb_publish(a.vdone + bI, s_tick[0] + 1u);
+                        jb_publish(a.vdone + bJ, s_tick[1] + 1u);
+                    }
                 } else {
                     // nothing rotated: drain the speculatively issued apply chunks
                     // (the rest of the sequence is never issued)
@@ -1883,20 +1938,13 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     qu = qn;
                 }
                 __syncthreads();
-                if (t == 0) {
-                    if (rot) {
-                        __stcg(a.mod + bI, R + 1u);
-                        __stcg(a.mod + bJ, R + 1u);
-                        atomicAdd(a.counters + 2, 1ull);
-                    } else {
-                        __stcg(a.clean + pid, R + 1u);
-                    }
+                if (t == 0 && !rot) {  // (a rotating visit published W before its V update)
+                    __stcg(a.clean + pid, R + 1u);
                     __threadfence();
                     jb_publish(a.ver + bI, R + 1);
                     jb_publish(a.ver + bJ, R + 1);
                 }
             }
-            ++R;
         }
         grid_sync(a.bar);
         const int rotated = flags[sweep % 3];
@@ -2259,15 +2307,22 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         Buf verb(ctx, sizeof(unsigned) * g.nb);
         RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
         g.ver = static_cast<unsigned*>(verb.p);
-        const size_t nst = size_t(g.nb) + size_t(g.nb) * g.nb + g.nb / 2;
+        const size_t nst = size_t(g.nb) + size_t(g.nb) * g.nb + g.nb / 2 + 2 * size_t(g.nb) + kOneSidedSweepCap;
         Buf stamps(ctx, sizeof(unsigned) * nst), cnt(ctx, sizeof(unsigned long long) * 4);
         RLRA_CUDA(cudaMemsetAsync(stamps.p, 0, sizeof(unsigned) * nst, ctx.stream));
         RLRA_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * 4, ctx.stream));
         g.mod = static_cast<unsigned*>(stamps.p);
         g.clean = g.mod + g.nb;
+        g.vtick = g.clean + size_t(g.nb) * g.nb + g.nb / 2;
+        g.vdone = g.vtick + g.nb;
+        g.tasks = g.vdone + g.nb;
         g.counters = static_cast<unsigned long long*>(cnt.p);
         void* args[] = {&g};
-        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)sgram_jacobi_kernel, dim3(g.nb / 2), dim3(256), args, kSGramSmem,
+        // visits are taken dynamically, so every SM can work (one CTA each):
+        // CTAs beyond the np pair slots pick up the next round's ready pairs
+        static const int sg_grid = std::getenv("RLRA_SGRAM_GRID") ? std::atoi(std::getenv("RLRA_SGRAM_GRID")) : 0;
+        const int sgrid = sg_grid > 0 ? std::min(sg_grid, ctx.num_sms) : ctx.num_sms;
+        RLRA_CUDA(cudaLaunchCooperativeKernel((void*)sgram_jacobi_kernel, dim3(sgrid), dim3(256), args, kSGramSmem,
                                               ctx.stream));
         if (std::getenv("RLRA_JACOBI_STATS")) {
             unsigned long long h[3];

@@ -1,2 +1,1 @@
-python tools/time_gemm.py
-python tools/run_configs.py C3 C5 2>&1 | cut -c1-200
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_all.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/gpu_all.log
