@@ -4,6 +4,7 @@
 // host<->device staging for RLRA_HOST buffers, status mapping, and the
 // thread-local last-error string.  The arithmetic lives in engine.cu and the
 // kernel files; nothing here computes on the CPU.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -525,6 +526,18 @@ rlra_status rlra_sample(rlra_ctx* ctx, int loc, int left, const double* a, int m
     });
 }
 
+// RLRA_HOSTIO_TIMES=1: wall-clock marks of the host-buffer paths (stderr);
+// with a context the mark first drains its stream
+static void host_time_mark(const char* what, Context* C = nullptr) {
+    static const bool on = std::getenv("RLRA_HOSTIO_TIMES") != nullptr;
+    if (!on) return;
+    if (C) cudaStreamSynchronize(C->stream);
+    static thread_local auto t0 = std::chrono::steady_clock::now();
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  [%s] +%.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+}
+
 rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int m, int n, int64_t lda,
                       int k, int p, int q, int s, const rlra_omega* omega, double* u, int64_t ldu,
                       double* sigma, double* v, int64_t ldv) {
@@ -533,6 +546,7 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
         check_sample_rank(k, p, m, n);
         if (variant != RLRA_RSVD_BASIC) check_sample(k + p, q, s, m, n);
         OmegaSource om = omega_of(omega);
+        host_time_mark("call entry (since the last mark)");
         Out U(C, loc, u, m, k, ldu, "u"), V(C, loc, v, n, k, ldv, "v");
         OutVec<double> S(C, loc, sigma, k, "sigma");
         if (loc == RLRA_HOST && m > 0 && n > 0) {
@@ -544,15 +558,18 @@ rlra_status rlra_rsvd(rlra_ctx* ctx, int loc, int variant, const double* a, int 
             const bool zt = variant != RLRA_RSVD_BASIC && q > 0 && m >= k + p;
             DMatBuf Zt(C, zt ? n : 0, zt ? k + p : 0);
             const bool have_zt = upload_and_sketch(C, a, lda, dA.m, k + p, om, Y.m, zt ? &Zt.m : nullptr);
+            host_time_mark("upload+sketch");
             rsvd(C, variant, dA.m, k, p, q, s, om, U.m, S.d, V.m, &Y.m, have_zt ? &Zt.m : nullptr);
         } else {
             In A(C, loc, a, m, n, lda, "a");
             rsvd(C, variant, A.m, k, p, q, s, om, U.m, S.d, V.m);
         }
+        host_time_mark("rsvd enqueued", &C);
         U.finish(C);
         V.finish(C);
         S.finish(C);
         sync(C);
+        host_time_mark("outputs");
     });
 }
 

@@ -4,6 +4,7 @@
 // cpqr.cu.  Host code here only sequences launches and reads back the few
 // scalars the reference's control flow branches on (the QB stop test, pivot
 // and breakdown flags).
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -277,6 +278,7 @@ bool upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
         RLRA_CUDA(cudaMemcpyAsync(Om.m.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
                                   ctx.stream));
     }
+    const auto t_up0 = std::chrono::steady_clock::now();
     // row chunks of whole 128-row GEMM tiles, ~32 of them for a large A (the
     // last chunk's sketch is the only part not hidden under the upload)
     const int64_t bytes = m * n * 8;
@@ -311,7 +313,13 @@ bool upload_and_sketch(Context& ctx, const double* hA, int64_t lda, const DMat& 
             gemm(ctx, Op::T, Op::N, 1.0, Ar, Yr, r0 == 0 ? 0.0 : 1.0, *Zt);
         }
     }
+    static const bool times = std::getenv("RLRA_HOSTIO_TIMES") != nullptr;
+    const auto t_enq = std::chrono::steady_clock::now();
     RLRA_CUDA(cudaStreamSynchronize(ctx.stream));  // h (callback Omega) outlives its copy; events done
+    if (times)
+        std::fprintf(stderr, "upload_and_sketch %lld x %lld: enqueued %.3f ms, done %.3f ms\n", (long long)m,
+                     (long long)n, std::chrono::duration<double, std::milli>(t_enq - t_up0).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_up0).count());
     for (auto e : ev) cudaEventDestroy(e);
     cudaEventDestroy(ready);
     return Zt && nchunk > 1;

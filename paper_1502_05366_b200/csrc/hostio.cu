@@ -1,5 +1,7 @@
 // hostio.cu — staged host <-> device copies (see hostio.cuh).
 #include <algorithm>
+#include <cstdio>
+#include <chrono>
 #include <atomic>
 #include <condition_variable>
 #include <cstdlib>
@@ -70,9 +72,18 @@ private:
 
 constexpr int kSlots = 4;
 constexpr size_t kSlotBytes = size_t(16) << 20;  // 16 MB pinned per slot (one-time pinning stays ~20 ms)
-// below this a pageable copy goes straight to the driver: the one-time cost of
-// the pool and the pinned slots would not pay for itself
-constexpr size_t kStageMin = size_t(64) << 20;
+// below this a pageable copy goes straight to the driver (the pool and the
+// pinned slots are created on a context's first staged copy, ~20 ms once;
+// above a few MB the staged path wins on every later call: C1's 64 MB A
+// uploads in 2.7 ms staged against 4.5 ms through the driver's pageable
+// path; RLRA_STAGE_MIN_MB overrides)
+size_t stage_min() {
+    static const size_t v = [] {
+        const char* e = std::getenv("RLRA_STAGE_MIN_MB");
+        return (e ? size_t(std::max(0, std::atoi(e))) : size_t(4)) << 20;
+    }();
+    return v;
+}
 
 struct Stager {
     Pool pool;
@@ -127,7 +138,7 @@ void h2d_copy(Context& ctx, cudaStream_t st, const double* h, int64_t ldh, const
     const int64_t rows = d.rows, cols = d.cols;
     if (rows <= 0 || cols <= 0) return;
     const size_t colb = sizeof(double) * size_t(rows);
-    if (host_is_pinned(h) || colb * size_t(cols) < kStageMin || colb > kSlotBytes) {
+    if (host_is_pinned(h) || colb * size_t(cols) < stage_min() || colb > kSlotBytes) {
         RLRA_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double) * d.ld, h, sizeof(double) * ldh, colb, cols,
                                     cudaMemcpyHostToDevice, st));
         return;
@@ -135,18 +146,49 @@ void h2d_copy(Context& ctx, cudaStream_t st, const double* h, int64_t ldh, const
     Stager& S = stager(ctx);
     const int per = int(std::min<size_t>(size_t(cols), kSlotBytes / colb));  // columns per slot
     static thread_local int next = 0;
+    static const bool times = std::getenv("RLRA_HOSTIO_TIMES") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&] {
+        if (!times) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back(e);
+    };
+    tmark();
     for (int64_t j0 = 0; j0 < cols; j0 += per) {
         const int j1 = int(std::min<int64_t>(cols, j0 + per));
         const int s = next;
         next = (next + 1) % kSlots;
+        const auto h0 = std::chrono::steady_clock::now();
         RLRA_CUDA(cudaEventSynchronize(S.done[s]));  // the slot's previous DMA has drained
+        const auto h1 = std::chrono::steady_clock::now();
         double* dst = S.slot[s];
         parallel_cols(S.pool, int(j0), j1, [&](int j) {
             std::memcpy(dst + size_t(j - j0) * size_t(rows), h + size_t(j) * size_t(ldh), colb);
         });
-        RLRA_CUDA(cudaMemcpy2DAsync(d.p + j0 * d.ld, sizeof(double) * d.ld, dst, colb, colb, j1 - j0,
-                                    cudaMemcpyHostToDevice, st));
+        if (times)
+            std::fprintf(stderr, "    piece slot %d: wait %.3f pack %.3f ms\n", s,
+                         std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
+        if (d.ld == rows)  // contiguous on both sides: one 1-D DMA (a 2-D copy of 16 KB rows runs at ~18 GB/s)
+            RLRA_CUDA(cudaMemcpyAsync(d.p + j0 * d.ld, dst, colb * size_t(j1 - j0), cudaMemcpyHostToDevice, st));
+        else
+            RLRA_CUDA(cudaMemcpy2DAsync(d.p + j0 * d.ld, sizeof(double) * d.ld, dst, colb, colb, j1 - j0,
+                                        cudaMemcpyHostToDevice, st));
         RLRA_CUDA(cudaEventRecord(S.done[s], st));
+        tmark();
+    }
+    if (times) {
+        cudaEventSynchronize(tev.back());
+        std::fprintf(stderr, "  h2d staged %zu MB:", size_t(colb) * size_t(cols) >> 20);
+        for (size_t i = 1; i < tev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+            std::fprintf(stderr, " %.3f", ms);
+        }
+        std::fprintf(stderr, " ms\n");
+        for (auto e : tev) cudaEventDestroy(e);
     }
 }
 
@@ -154,7 +196,7 @@ void d2h_copy(Context& ctx, const DMat& d, double* h, int64_t ldh) {
     const int64_t rows = d.rows, cols = d.cols;
     if (rows <= 0 || cols <= 0) return;
     const size_t colb = sizeof(double) * size_t(rows);
-    if (host_is_pinned(h) || colb * size_t(cols) < kStageMin || colb > kSlotBytes) {
+    if (host_is_pinned(h) || colb * size_t(cols) < stage_min() || colb > kSlotBytes) {
         RLRA_CUDA(cudaMemcpy2DAsync(h, sizeof(double) * ldh, d.p, sizeof(double) * d.ld, colb, cols,
                                     cudaMemcpyDeviceToHost, ctx.stream));
         RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -168,8 +210,12 @@ void d2h_copy(Context& ctx, const DMat& d, double* h, int64_t ldh) {
         const int64_t j0 = p * per, j1 = std::min<int64_t>(cols, j0 + per);
         const int s = int(p % kSlots);
         RLRA_CUDA(cudaStreamWaitEvent(ctx.stream, S.done[s], 0));  // the slot's previous DMA (any stream)
-        RLRA_CUDA(cudaMemcpy2DAsync(S.slot[s], colb, d.p + j0 * d.ld, sizeof(double) * d.ld, colb, j1 - j0,
-                                    cudaMemcpyDeviceToHost, ctx.stream));
+        if (d.ld == rows)
+            RLRA_CUDA(cudaMemcpyAsync(S.slot[s], d.p + j0 * d.ld, colb * size_t(j1 - j0), cudaMemcpyDeviceToHost,
+                                      ctx.stream));
+        else
+            RLRA_CUDA(cudaMemcpy2DAsync(S.slot[s], colb, d.p + j0 * d.ld, sizeof(double) * d.ld, colb, j1 - j0,
+                                        cudaMemcpyDeviceToHost, ctx.stream));
         RLRA_CUDA(cudaEventRecord(S.done[s], ctx.stream));
     };
     for (int64_t p = 0; p < std::min<int64_t>(npieces, kSlots); ++p) enqueue(p);

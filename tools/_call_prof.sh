@@ -1,2 +1,2 @@
-python tools/run_configs.py C1 C2 C3 C4 C5 > gpurun_out/cfg_final.jsonl 2>gpurun_out/cfg_final.err; cut -c1-150 gpurun_out/cfg_final.jsonl
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc=$?"; tail -1 gpurun_out/bench_final.json | cut -c1-600
+python tools/host_api_c1.py > gpurun_out/h1.txt 2>&1; head -1 gpurun_out/h1.txt; tail -1 gpurun_out/h1.txt
+python tools/host_api_pinned_c1.py
