@@ -995,6 +995,13 @@ __device__ __forceinline__ int bgram_steps_t(double* G0, double* J) {
             // (a padded column's Gram entries are 0: never rotated)
             const double kpp = Gc[pk * GP + pk], kqq = Gc[qk * GP + qk], kpq = Gc[pk * GP + qk];
             const double lpp = Gc[pl * GP + pl], lqq = Gc[ql * GP + ql], lpq = Gc[pl * GP + ql];
+            // this thread's J and G blocks: loaded under the rotation chain
+            // (independent of it), updated without branches (a skipped
+            // rotation keeps the values: selects, not arithmetic)
+            const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
+            const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
+            double b00 = Gc[pk * GP + pl], b01 = Gc[pk * GP + ql];
+            double b10 = Gc[qk * GP + pl], b11 = Gc[qk * GP + ql];
             double ck, sk, cl, sl;
             int ak, al;
             const bool okk = jac_rotation_fast(kpp, kqq, kpq, ck, sk, ak);
@@ -1004,26 +1011,20 @@ __device__ __forceinline__ int bgram_steps_t(double* G0, double* J) {
             act = (k == l) ? ak : 0;
             rot |= act;
             if (al) {  // J <- J R_l on rows {pk, qk}
-                const double j0 = J[pk * GP + pl], j1 = J[pk * GP + ql];
-                const double j2 = J[qk * GP + pl], j3 = J[qk * GP + ql];
                 J[pk * GP + pl] = cl * j0 - sl * j1;
                 J[pk * GP + ql] = sl * j0 + cl * j1;
                 J[qk * GP + pl] = cl * j2 - sl * j3;
                 J[qk * GP + ql] = sl * j2 + cl * j3;
             }
+            {
+                const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
+                const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
+                b00 = al ? x0 : b00, b01 = al ? x1 : b01, b10 = al ? x2 : b10, b11 = al ? x3 : b11;
+                const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
+                const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
+                b00 = ak ? y0 : b00, b01 = ak ? y1 : b01, b10 = ak ? y2 : b10, b11 = ak ? y3 : b11;
+            }
             if (k <= l) {  // G block (k, l) <- R_k^T B R_l, mirrored
-                double b00 = Gc[pk * GP + pl], b01 = Gc[pk * GP + ql];
-                double b10 = Gc[qk * GP + pl], b11 = Gc[qk * GP + ql];
-                if (al) {
-                    const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
-                    const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
-                    b00 = x0, b01 = x1, b10 = x2, b11 = x3;
-                }
-                if (ak) {
-                    const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
-                    const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
-                    b00 = y0, b01 = y1, b10 = y2, b11 = y3;
-                }
                 Gn[pk * GP + pl] = b00;
                 Gn[pk * GP + ql] = b01;
                 Gn[qk * GP + pl] = b10;

@@ -17,6 +17,17 @@ __global__ void chain(double* out, double x0, long long* cyc, int iters) {
         if (OP == 5) x = rsqrt(x + 1.0);
         if (OP == 6) x = __shfl_sync(0xffffffffu, x, (threadIdx.x + 1) & 31) + 1e-300;
         if (OP == 7) x = __drcp_rn(x + 1.0);
+        if (OP == 8) {  // MUFU.RSQ64H (the Jacobi rotation's seed) alone
+            double y;
+            asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x + 1.0));
+            x = y;
+        }
+        if (OP == 9) {  // MUFU.RCP64H alone
+            double y;
+            asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x + 1.0));
+            x = y;
+        }
+        if (OP == 10) x = __shfl_sync(0xffffffffu, x, 3) + 1e-300;  // broadcast shuffle
     }
     long long t1 = clock64();
     out[threadIdx.x] = x;
@@ -28,9 +39,10 @@ int main() {
     long long* cyc;
     cudaMalloc(&out, 1024 * 8);
     cudaMallocManaged(&cyc, 8);
-    const char* names[] = {"dfma", "dadd", "sqrt", "1/x", "x/y", "rsqrt", "shfl+dadd", "__drcp_rn"};
+    const char* names[] = {"dfma", "dadd", "sqrt", "1/x", "x/y", "rsqrt", "shfl+dadd", "__drcp_rn",
+                           "rsqrt.approx.f64 (+dadd)", "rcp.approx.f64 (+dadd)", "shfl.idx+dadd"};
     const int iters = 4096;
-    for (int op = 0; op < 8; ++op) {
+    for (int op = 0; op < 11; ++op) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (op) {
                 case 0: chain<0><<<1, 32>>>(out, 0.5, cyc, iters); break;
@@ -41,6 +53,9 @@ int main() {
                 case 5: chain<5><<<1, 32>>>(out, 0.5, cyc, iters); break;
                 case 6: chain<6><<<1, 32>>>(out, 0.5, cyc, iters); break;
                 case 7: chain<7><<<1, 32>>>(out, 0.5, cyc, iters); break;
+                case 8: chain<8><<<1, 32>>>(out, 0.5, cyc, iters); break;
+                case 9: chain<9><<<1, 32>>>(out, 0.5, cyc, iters); break;
+                case 10: chain<10><<<1, 32>>>(out, 0.5, cyc, iters); break;
             }
             cudaDeviceSynchronize();
         }
