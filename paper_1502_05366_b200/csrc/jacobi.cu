@@ -1811,27 +1811,25 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                         const int pk = pqk & 255, qk = (pqk >> 8) & 255, pl = pql & 255, ql = (pql >> 8) & 255;
                         const bool ak = (pqk >> 16) != 0, al = (pql >> 16) != 0;
                         const double ck = rc[k], sk = rs[k], cl = rc[l], sl = rs[l];
+                        const double j0 = J[pk * kSGP + pl], j1 = J[pk * kSGP + ql];
+                        const double j2 = J[qk * kSGP + pl], j3 = J[qk * kSGP + ql];
+                        double b00 = Gc[pk * kSGP + pl], b01 = Gc[pk * kSGP + ql];
+                        double b10 = Gc[qk * kSGP + pl], b11 = Gc[qk * kSGP + ql];
                         if (al) {
-                            const double j0 = J[pk * kSGP + pl], j1 = J[pk * kSGP + ql];
-                            const double j2 = J[qk * kSGP + pl], j3 = J[qk * kSGP + ql];
                             J[pk * kSGP + pl] = cl * j0 - sl * j1;
                             J[pk * kSGP + ql] = sl * j0 + cl * j1;
                             J[qk * kSGP + pl] = cl * j2 - sl * j3;
                             J[qk * kSGP + ql] = sl * j2 + cl * j3;
                         }
+                        {  // branch-free (selects keep the values of a skipped rotation)
+                            const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
+                            const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
+                            b00 = al ? x0 : b00, b01 = al ? x1 : b01, b10 = al ? x2 : b10, b11 = al ? x3 : b11;
+                            const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
+                            const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
+                            b00 = ak ? y0 : b00, b01 = ak ? y1 : b01, b10 = ak ? y2 : b10, b11 = ak ? y3 : b11;
+                        }
                         if (k <= l) {
-                            double b00 = Gc[pk * kSGP + pl], b01 = Gc[pk * kSGP + ql];
-                            double b10 = Gc[qk * kSGP + pl], b11 = Gc[qk * kSGP + ql];
-                            if (al) {
-                                const double x0 = cl * b00 - sl * b01, x1 = sl * b00 + cl * b01;
-                                const double x2 = cl * b10 - sl * b11, x3 = sl * b10 + cl * b11;
-                                b00 = x0, b01 = x1, b10 = x2, b11 = x3;
-                            }
-                            if (ak) {
-                                const double y0 = ck * b00 - sk * b10, y2 = sk * b00 + ck * b10;
-                                const double y1 = ck * b01 - sk * b11, y3 = sk * b01 + ck * b11;
-                                b00 = y0, b01 = y1, b10 = y2, b11 = y3;
-                            }
                             Gn[pk * kSGP + pl] = b00;
                             Gn[pk * kSGP + ql] = b01;
                             Gn[qk * kSGP + pl] = b10;
