@@ -14,6 +14,10 @@ ROLES = [
     ("dgemm_tma_kernel<1, 0, 0, 1>", "TMA GEMM, A*Omega sketch, A*Z power, Y*R^-1, lift (NN)"),
     ("dgemm_tma_kernel<1, 0, 1, 2>", "TMA GEMM sketch with in-register Philox Omega (RLRA_SKETCH_FUSED=1)"),
     ("bgram_jacobi_kernel", "Gram block Jacobi SVD of R-hat (owners + V helpers)"),
+    ("cgram_jacobi_kernel", "cluster-resident Gram block Jacobi SVD of R-hat (l <= 256)"),
+    ("sgram_jacobi_kernel", "streaming Gram block Jacobi SVD (dynamic visits)"),
+    ("dgemm_ws_kernel", "cp.async GEMM (64x64 tiles for short-k / small Grams)"),
+    ("dgemm_kernel", "cp.async GEMM (64x64 tiles for short-k / small Grams)"),
     ("block_jacobi_kernel", "one-sided block Jacobi SVD of R-hat"),
     ("chol_inv_coop_kernel", "one-launch Cholesky + R^-1 of the l x l Grams"),
     ("philox_fill_kernel", "Philox Omega materialised for the sketch"),
