@@ -40,11 +40,16 @@ rlra_status guard(rlra_ctx* ctx, const char* name, F&& f) {
     try {
         if (!ctx) raise(RLRA_EINVAL, "null rlra_ctx");
         RLRA_CUDA(cudaSetDevice(ctx->c.device));
+        ctx->c.svd_pending = 0;
         f(ctx->c);
+        small_svd_deferred_checks(ctx->c);
         return RLRA_OK;
     } catch (const Error& e) {
         g_err = e.msg;
-        if (ctx) cudaStreamSynchronize(ctx->c.stream);
+        if (ctx) {
+            cudaStreamSynchronize(ctx->c.stream);
+            ctx->c.svd_pending = 0;
+        }
         return static_cast<rlra_status>(e.status);
     } catch (const std::exception& e) {
         g_err = e.what();

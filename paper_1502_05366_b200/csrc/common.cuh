@@ -94,6 +94,11 @@ struct Context {
     const char* gemm_tag = "gemm";
     // pinned staging slots + host copy threads for pageable buffers (hostio.cu, lazy)
     void* stager = nullptr;
+    // small_svd convergence checks deferred to the end of the API call (no
+    // host sync inside the factorization): status words land in
+    // h_flags[32 + i] asynchronously; the C-ABI guard reads them after its sync
+    int svd_pending = 0;
+    int svd_pending_mn[8][2] = {};
 };
 
 // Scoped label for GEMM launches (profiling/accounting only).

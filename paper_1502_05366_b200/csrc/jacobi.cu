@@ -2377,10 +2377,24 @@ launched:
         needs.i());
     RLRA_LAUNCH_CHECK();
     ctx.launches += 3;
+    if (prof.idx < 0 && ctx.svd_pending < 8) {
+        // no host sync: the convergence status is checked when the API call
+        // ends (the C-ABI guard), and the completion kernel runs always (it
+        // leaves the columns alone when no singular value fell below the floor)
+        const int slot = ctx.svd_pending++;
+        ctx.svd_pending_mn[slot][0] = m;
+        ctx.svd_pending_mn[slot][1] = n;
+        RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags + 32 + slot, flags.i() + 3, sizeof(int), cudaMemcpyDeviceToHost,
+                                  ctx.stream));
+        Buf done(ctx, sizeof(int) * n), r(ctx, sizeof(double) * m);
+        completion_kernel<<<1, 256, 0, ctx.stream>>>(U.p, U.ld, m, n, needs.i(), done.i(), r.d());
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        return;
+    }
     RLRA_CUDA(cudaMemcpyAsync(ctx.h_flags, flags.p, sizeof(int) * 8, cudaMemcpyDeviceToHost,
                               ctx.stream));
     // any column needing completion?
-    Buf anyneed(ctx, sizeof(double));
     {
         // count needs on host: copy the n flags (small)
         std::vector<int> h(n);
@@ -2400,6 +2414,18 @@ launched:
             ++ctx.launches;
         }
     }
+}
+
+// the small_svd checks deferred in ctx (see Context::svd_pending)
+void small_svd_deferred_checks(Context& ctx) {
+    if (ctx.svd_pending == 0) return;
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    const int np = ctx.svd_pending;
+    ctx.svd_pending = 0;
+    for (int i = 0; i < np; ++i)
+        if (ctx.h_flags[32 + i] == RLRA_ECONV)
+            raise(RLRA_ECONV, fmt("small_svd: no convergence after %d sweeps on %dx%d input", kOneSidedSweepCap,
+                                  ctx.svd_pending_mn[i][0], ctx.svd_pending_mn[i][1]));
 }
 
 void small_svd(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V) {

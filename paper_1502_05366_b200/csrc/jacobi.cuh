@@ -18,6 +18,10 @@ namespace rlra_b200 {
 // modified.  Throws ConvergenceError after 60 sweeps.
 void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V);
 
+// Raises the convergence errors small_svd_tall deferred to the end of the
+// API call (ctx.svd_pending); called by the C-ABI after every entry point.
+void small_svd_deferred_checks(Context& ctx);
+
 // Any shape: r = min(m,n); U (m x r), V (n x r) (jacobi.hpp:148-152).
 void small_svd(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V);
 

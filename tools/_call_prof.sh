@@ -1,4 +1,6 @@
-cd $GRAFT_REPO_ROOT
-timeout 600 python tools/profile_step.py > gpurun_out/step_plain.log 2>&1 && \
-timeout 1500 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/step_launches.csv python tools/profile_step.py > gpurun_out/step_ncu.log 2>&1
-echo "rc=$?"; cat gpurun_out/step_plain.log | tail -1; tail -1 gpurun_out/step_ncu.log; wc -l gpurun_out/step_launches.csv
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_all.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/gpu_all.log
+python tools/run_configs.py C1 C5 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    d = json.loads(l); print(d['config'], d['time_s'], d['phases_ms'].get('small_svd'))"
+python tools/host_api_c1.py 2>&1 | head -1
