@@ -335,6 +335,10 @@ __global__ void completion_kernel(double* U, int64_t ldu, int m, int n, const in
     __shared__ double sv[32];
     __shared__ int si[32];
     __shared__ int nd;
+    // the common case — no column needs completion — leaves at once
+    int any = 0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) any |= needs[j];
+    if (!__syncthreads_or(any)) return;
     if (threadIdx.x == 0) {
         nd = 0;
         for (int j = 0; j < n; ++j)
