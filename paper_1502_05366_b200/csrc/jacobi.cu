@@ -2142,12 +2142,17 @@ bool cgram_fits(Context& ctx, int np, size_t smem) {
     return nclusters >= 1;
 }
 
-void launch_cgram(Context& ctx, const CGramArgs& c, size_t smem) {
+// false when the cluster cannot be placed at launch time (e.g. another
+// context holds the SMs of every GPC): the caller takes the L2 variant
+bool launch_cgram(Context& ctx, const CGramArgs& c, size_t smem) {
     cgram_attrs(smem);
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = cgram_config(ctx, c.nb / 2, smem, attr);
-    RLRA_CUDA(cudaLaunchKernelEx(&cfg, cgram_jacobi_kernel<8>, c));
-    RLRA_LAUNCH_CHECK();
+    if (cudaLaunchKernelEx(&cfg, cgram_jacobi_kernel<8>, c) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
 }
 
 void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& Vout) {
@@ -2214,8 +2219,8 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         Buf jlog(ctx, sizeof(double) * slots * 256), rlog(ctx, slots);
         CGramArgs c{W.m.p, W.m.ld, m,     n, cnb, V.m.p, V.m.ld, jlog.d(), static_cast<unsigned char*>(rlog.p), flags.i(),
                     want_clk ? reinterpret_cast<long long*>(clkb.p) : nullptr};
-        launch_cgram(ctx, c, cgram_smem<8>(m, cnb));
-        if (want_clk) {
+        const bool ok = launch_cgram(ctx, c, cgram_smem<8>(m, cnb));
+        if (ok && want_clk) {
             long long h[7];
             RLRA_CUDA(cudaMemcpyAsync(h, clkb.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
             RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -2224,7 +2229,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
                          "arrive %lld\n",
                          m, n, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
         }
-        goto launched;
+        if (ok) goto launched;
     }
     if (use_bgram) {
         GramJacArgs g;
