@@ -1,4 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_all.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/gpu_all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc=$?"; tail -1 gpurun_out/bench_final.json | cut -c1-300
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref.json | cut -c1-300
+timeout 1200 python bench.py --gpus 2 --comm host --steps 2 --warmup 1 > gpurun_out/b2h.json 2> gpurun_out/b2h.err; echo "n2 rc=$?"; tail -1 gpurun_out/b2h.json | cut -c1-250
