@@ -1,7 +1,5 @@
 // hostio.cu — staged host <-> device copies (see hostio.cuh).
 #include <algorithm>
-#include <cstdio>
-#include <chrono>
 #include <atomic>
 #include <condition_variable>
 #include <cstdlib>
@@ -146,49 +144,21 @@ void h2d_copy(Context& ctx, cudaStream_t st, const double* h, int64_t ldh, const
     Stager& S = stager(ctx);
     const int per = int(std::min<size_t>(size_t(cols), kSlotBytes / colb));  // columns per slot
     static thread_local int next = 0;
-    static const bool times = std::getenv("RLRA_HOSTIO_TIMES") != nullptr;
-    std::vector<cudaEvent_t> tev;
-    auto tmark = [&] {
-        if (!times) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, st);
-        tev.push_back(e);
-    };
-    tmark();
     for (int64_t j0 = 0; j0 < cols; j0 += per) {
         const int j1 = int(std::min<int64_t>(cols, j0 + per));
         const int s = next;
         next = (next + 1) % kSlots;
-        const auto h0 = std::chrono::steady_clock::now();
         RLRA_CUDA(cudaEventSynchronize(S.done[s]));  // the slot's previous DMA has drained
-        const auto h1 = std::chrono::steady_clock::now();
         double* dst = S.slot[s];
         parallel_cols(S.pool, int(j0), j1, [&](int j) {
             std::memcpy(dst + size_t(j - j0) * size_t(rows), h + size_t(j) * size_t(ldh), colb);
         });
-        if (times)
-            std::fprintf(stderr, "    piece slot %d: wait %.3f pack %.3f ms\n", s,
-                         std::chrono::duration<double, std::milli>(h1 - h0).count(),
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
-        if (d.ld == rows)  // contiguous on both sides: one 1-D DMA (a 2-D copy of 16 KB rows runs at ~18 GB/s)
+        if (d.ld == rows)  // contiguous on both sides: one 1-D DMA
             RLRA_CUDA(cudaMemcpyAsync(d.p + j0 * d.ld, dst, colb * size_t(j1 - j0), cudaMemcpyHostToDevice, st));
         else
             RLRA_CUDA(cudaMemcpy2DAsync(d.p + j0 * d.ld, sizeof(double) * d.ld, dst, colb, colb, j1 - j0,
                                         cudaMemcpyHostToDevice, st));
         RLRA_CUDA(cudaEventRecord(S.done[s], st));
-        tmark();
-    }
-    if (times) {
-        cudaEventSynchronize(tev.back());
-        std::fprintf(stderr, "  h2d staged %zu MB:", size_t(colb) * size_t(cols) >> 20);
-        for (size_t i = 1; i < tev.size(); ++i) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
-            std::fprintf(stderr, " %.3f", ms);
-        }
-        std::fprintf(stderr, " ms\n");
-        for (auto e : tev) cudaEventDestroy(e);
     }
 }
 
