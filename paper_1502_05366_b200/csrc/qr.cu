@@ -429,6 +429,9 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
         //   panel   R_JJ^T R[J, c] = G[J, c]        (a column c per warp)
         //   rows    X[r, J] R_JJ   = acc[r, J]      (a row r < j0 per warp)
         //   X_JJ    R_JJ X[J, j]   = e_j            (a column j per warp)
+        // (only CTAs with a task stage R_JJ: 148 CTAs loading the same 32 KB
+        // block would queue on the same L2 lines)
+        if (int(blockIdx.x) * 8 < rest + j0 + nb) {
         for (int e = t; e < kCholNB * kCholNB; e += blockDim.x) {
             const int i = e % kCholNB, j = e / kCholNB;
             s1[i][j] = (i < nb && j < nb) ? (i <= j ? __ldcg(G + (j0 + i) + int64_t(j0 + j) * ldg) : 0.0)
@@ -472,6 +475,7 @@ __global__ void __launch_bounds__(256) chol_inv_coop_kernel(CholCoopArgs a) {
                 if (lane < nb) X[(j0 + lane) + int64_t(j0 + j) * ldr] = b0;
                 if (lane + 32 < nb) X[(j0 + lane + 32) + int64_t(j0 + j) * ldr] = b1;
             }
+        }
         }
         grid_sync(a.bar);
         chol_probe(a.tprobe, 2 + 3 * (j0 / kCholNB));

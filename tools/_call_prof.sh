@@ -1,1 +1,1 @@
-timeout 1200 python bench.py --gpus 2 --comm host --steps 2 --warmup 1 > gpurun_out/b2h.json 2> gpurun_out/b2h.err; echo "n2 rc=$?"; tail -1 gpurun_out/b2h.json | cut -c1-250
+timeout 4200 python tools/parity_full.py C4 > gpurun_out/parity_c4b.jsonl 2> gpurun_out/parity_c4b.err; echo "rc=$?"; cut -c1-400 gpurun_out/parity_c4b.jsonl
