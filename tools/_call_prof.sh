@@ -1,3 +1,7 @@
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_all.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/gpu_all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_final3.json 2> gpurun_out/bench_final3.err; echo "bench rc=$?"; tail -1 gpurun_out/bench_final3.json | cut -c1-250
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -p no:cacheprovider -k "gemm or matmul" > gpurun_out/p11.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/p11.log
+python tools/time_gemm.py
+python tools/gemm_calls.py C3 2>&1 | grep -E "gemm_sketch|gemm_power" | head -3
+python tools/run_configs.py C1 C3 C5 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    d = json.loads(l); print(d['config'], d['time_s'])"
