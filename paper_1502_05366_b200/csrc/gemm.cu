@@ -359,15 +359,31 @@ void gemm(Context& ctx, Op opa, Op opb, int M, int N, int K, double alpha, const
     // deterministic reduction ((s+1) M N doubles through HBM) + one launch.
     int splits = 1;
     if (o.epi != EPI_RESID && !o.tri_b_upper) {
-        if (o.force_splits > 0) {
-            splits = o.force_splits;
+        static const int env_splits = std::getenv("RLRA_GEMM_SPLITS") ? std::atoi(std::getenv("RLRA_GEMM_SPLITS")) : 0;
+        if (o.force_splits > 0 || env_splits > 0) {
+            splits = o.force_splits > 0 ? o.force_splits : env_splits;
         } else {
             const double cta_rate = 2.5e11 / per_sm;  // FP64 flop/s of one CTA (37 TF / 148 SMs)
             const double hbm = 5.0e12;                // B/s, reduction traffic
+            // without split-K the TMA path splits the last partial wave's tiles
+            // into s_t k-chunks (tail split, below): that wave then costs
+            // 1/s_t of a tile plus a small reduction, not a whole tile
+            const bool vec_ok = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                                (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+            const bool tail_ok = big && vec_ok && opb == Op::N && !o.philox_b && o.epi == EPI_STORE &&
+                                 !o.upper_tiles_only && tma_choice() && tail_choice();
             auto model = [&](int64_t s) {
                 const int64_t kc = int64_t(ceil_div(ceil_div(K, int(s)), BK)) * BK;
+                const double t_tile = 2.0 * BM * BN * double(kc) / cta_rate;
+                if (s == 1 && tail_ok) {
+                    const int64_t full = tiles / cap, ntail = tiles - full * cap;
+                    const int64_t s_t = ntail > 0 ? std::min<int64_t>(8, cap / ntail) : 1;
+                    if (full > 0 && ntail > 0 && s_t >= 2 && K >= 8 * kTBK * s_t)
+                        return double(full) * t_tile + t_tile / double(s_t) +
+                               2.0 * double(ntail * s_t) * BM * BN * 8.0 / hbm + 4e-6;
+                }
                 const int64_t waves = (tiles * s + cap - 1) / cap;
-                double t = double(waves) * 2.0 * BM * BN * double(kc) / cta_rate;
+                double t = double(waves) * t_tile;
                 if (s > 1) t += double(s + 1) * 8.0 * double(M) * N / hbm + 4e-6;
                 return t;
             };
