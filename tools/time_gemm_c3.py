@@ -1,6 +1,7 @@
 """CUDA-event times of C3's A-streaming products (TN: 10000 x 610, k = 20000;
-NN: 20000 x 610, k = 10000) on the engine stream; RLRA_GEMM_SPLITS forces a
-split-K count for A/B runs.  Prints JSON."""
+NN: 20000 x 610, k = 10000) on the engine stream — or C1's (2000 x 4000,
+l = 210) with SHAPE=C1; RLRA_GEMM_SPLITS forces a split-K count for A/B
+runs.  Prints JSON."""
 import json
 import os
 import sys
@@ -10,7 +11,7 @@ import torch
 
 import paper_1502_05366_b200 as R
 
-m, n, l = 20000, 10000, 610
+m, n, l = (2000, 4000, 210) if os.environ.get("SHAPE") == "C1" else (20000, 10000, 610)
 eng = R.Engine(0)
 st = torch.cuda.ExternalStream(eng.stream)
 A = torch.empty(m * n, dtype=torch.float64, device="cuda")
@@ -28,9 +29,9 @@ for name, fn in (("TN", lambda: eng.device_matmul(True, False, A.data_ptr(), m, 
     eng.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for _ in range(5):
+    for _ in range(20):
         fn()
     e1.record(st)
     e1.synchronize()
-    out[name + "_ms"] = round(e0.elapsed_time(e1) / 5, 3)
+    out[name + "_ms"] = round(e0.elapsed_time(e1) / 20, 3)
 print(json.dumps(out), flush=True)
