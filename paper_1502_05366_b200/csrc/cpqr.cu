@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
             }
         };
         if (m - f <= 32 * kCpqrRegs) {
+            // row chunks below f still live (warp-uniform): the rest are zero
+            // on both sides and are skipped instead of loaded and multiplied
+            const int UR = (m - f + 31) >> 5;
             for (int j = j0 + warp; j < j1; j += 2 * nw) {
                 const int jj[2] = {j, j + nw};
                 bool on[2];
@@ -471,13 +474,14 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
 #pragma unroll
                     for (int u = 0; u < kCpqrRegs; ++u) {
                         const int i = f + lane + 32 * u;
-                        x[b][u] = (on[b] && i < m) ? wj[i] : 0.0;
+                        x[b][u] = (u < UR && on[b] && i < m) ? wj[i] : 0.0;
                     }
                 }
                 if (beta != 0.0) {
                     double sd[2] = {0.0, 0.0};
 #pragma unroll
                     for (int u = 0; u < kCpqrRegs; ++u) {
+                        if (u >= UR) break;
                         const int i = f + lane + 32 * u;
                         const double vi = i < m ? vsh[i] : 0.0;
 #pragma unroll
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
 #pragma unroll
                         for (int u = 0; u < kCpqrRegs; ++u) {
                             const int i = f + lane + 32 * u;
-                            if (i < m) x[b][u] -= fct * vsh[i];
+                            if (u < UR && i < m) x[b][u] -= fct * vsh[i];
                         }
                     }
 #pragma unroll
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(kCpqrStepThreads) cpqr_step_kernel(CpqrArgs a)
 #pragma unroll
                         for (int u = 0; u < kCpqrRegs; ++u) {
                             const int i = f + lane + 32 * u;
-                            if (i < m) wj[i] = x[b][u];
+                            if (u < UR && i < m) wj[i] = x[b][u];
                         }
                     }
                 }
