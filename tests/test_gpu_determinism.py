@@ -9,8 +9,11 @@ case runs the same input many times, with the GPU kept busy differently
 between repetitions (a background GEMM on another context perturbs the
 scheduling), and requires bit-identical results:
   * bgram_jacobi_kernel (V helpers, point-to-point block versions), the
-    streaming sgram_jacobi_kernel (bulk-copy ring, clean-pair skips),
-  * cpqr_step_kernel (one grid barrier per pivot step), the cooperative
+    cluster-resident cgram_jacobi_kernel (st.async exchange, split cluster
+    barriers, V replay), the streaming sgram_jacobi_kernel (cp.async ring,
+    clean-pair skips, dynamically taken visits),
+  * cpqr_step_kernel and cpqr_res_kernel (one grid barrier per pivot step;
+    register and shared-memory resident columns), the cooperative
     Cholesky (chol_inv_coop_kernel) inside CholQR2,
   * the TMA DMMA GEMM (mbarrier ring) incl. split-K,
   * whole rsvd_v2 / id_rand / qb_blocked calls."""
@@ -51,6 +54,28 @@ def test_bgram_jacobi_bit_identical_across_runs(eng):
     for k in range(REPS):
         _noise(eng2, k)
         outs.append(eng.small_svd(a))
+    assert _same(outs)
+
+
+def test_cluster_jacobi_bit_identical_across_runs(eng):
+    eng2 = R.Engine(0)
+    a = make_test_matrix(230, 210, np.exp(-np.arange(210) / 20.0), seed=66)
+    outs = []
+    for k in range(REPS):
+        _noise(eng2, k)
+        outs.append(eng.small_svd(a))
+    assert _same(outs)
+
+
+def test_resident_cpqr_shared_memory_columns_bit_identical_across_runs(eng):
+    """610 x 10000: 68 columns per CTA, 32 in registers, 36 in shared memory."""
+    eng2 = R.Engine(0)
+    a = make_test_matrix(610, 10000, 10.0 ** (-8.0 * np.arange(610) / 610), seed=67)
+    outs = []
+    for k in range(6):
+        _noise(eng2, k)
+        f = eng.pivoted_qr_partial(a, 600)
+        outs.append((f["perm"], f["s1"]))
     assert _same(outs)
 
 
