@@ -1282,6 +1282,40 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     return r;
 }
 
+void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T) {
+    // Blocked back substitution on DMMA: for the diagonal blocks from the
+    // bottom up, T_I <- S_II^{-1} T_I (one warp per right-hand side, the
+    // block's column in shared memory), then the rank-kTriNB update
+    // T[0:i0, :] -= S[0:i0, I] T_I on the tensor-core GEMM.  Shared memory
+    // holds one kTriNB slice per warp, so k is unbounded; the
+    // contraction's k^2 (n - k) flops run on DMMA.
+    const int k = int(S11.rows), nc = int(T.cols);
+    if (k == 0 || nc == 0) return;
+    constexpr int kTriNB = 64, kWpb = 8, kTriRec = 512;
+    if (k > kTriRec) {
+        // recursive halving (split on a kTriNB boundary): T2 <- S22^{-1} T2,
+        // T1 -= S12 T2 with K = k2 >= 256 (the rank-64 updates of the flat loop
+        // ran at ~8 TFLOP/s), T1 <- S11^{-1} T1
+        const int k1 = ((k / 2 + kTriNB - 1) / kTriNB) * kTriNB, k2 = k - k1;
+        upper_tri_solve_inplace(ctx, S11.block(k1, k1, k2, k2), T.block(k1, 0, k2, nc));
+        gemm(ctx, Op::N, Op::N, -1.0, S11.block(0, k1, k1, k2), T.block(k1, 0, k2, nc), 1.0, T.block(0, 0, k1, nc));
+        upper_tri_solve_inplace(ctx, S11.block(0, 0, k1, k1), T.block(0, 0, k1, nc));
+        return;
+    }
+    const size_t smem = sizeof(double) * size_t(kTriNB) * kWpb;
+    const int blocks = std::max(1, std::min(ctx.num_sms * 4, ceil_div(nc, kWpb)));
+    for (int i0 = ((k - 1) / kTriNB) * kTriNB; i0 >= 0; i0 -= kTriNB) {  // block rows aligned at 0
+        const int nb = std::min(k, i0 + kTriNB) - i0;
+        trisolve_kernel<<<blocks, kWpb * 32, smem, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
+                                                                 T.p + i0, T.ld, nc, T.p + i0, T.ld);
+        RLRA_LAUNCH_CHECK();
+        ++ctx.launches;
+        if (i0 > 0)
+            gemm(ctx, Op::N, Op::N, -1.0, S11.block(0, i0, i0, nb), T.block(i0, 0, nb, nc), 1.0,
+                 T.block(0, 0, i0, nc));
+    }
+}
+
 bool upper_tri_solve(Context& ctx, const DMat& S11, const DMat& S12, const DMat& T) {
     const int k = int(S11.rows), nc = int(S12.cols);
     if (S11.cols != k)
@@ -1304,26 +1338,8 @@ bool upper_tri_solve(Context& ctx, const DMat& S11, const DMat& S12, const DMat&
         dmin = std::min(dmin, hd[i]);
     }
     if (nc > 0) {
-        // Blocked back substitution on DMMA: for the diagonal blocks from the
-        // bottom up, T_I <- S_II^{-1} T_I (one warp per right-hand side, the
-        // block's column in shared memory), then the rank-kTriNB update
-        // T[0:i0, :] -= S[0:i0, I] T_I on the tensor-core GEMM.  Shared memory
-        // holds one kTriNB slice per warp, so k is unbounded; the
-        // contraction's k^2 (n - k) flops run on DMMA.
-        constexpr int kTriNB = 64, kWpb = 8;
         copy_mat(ctx, S12, T);
-        const size_t smem = sizeof(double) * size_t(kTriNB) * kWpb;
-        const int blocks = std::max(1, std::min(ctx.num_sms * 4, ceil_div(nc, kWpb)));
-        for (int i0 = ((k - 1) / kTriNB) * kTriNB; i0 >= 0; i0 -= kTriNB) {  // block rows aligned at 0
-            const int nb = std::min(k, i0 + kTriNB) - i0;
-            trisolve_kernel<<<blocks, kWpb * 32, smem, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
-                                                                     T.p + i0, T.ld, nc, T.p + i0, T.ld);
-            RLRA_LAUNCH_CHECK();
-            ++ctx.launches;
-            if (i0 > 0)
-                gemm(ctx, Op::N, Op::N, -1.0, S11.block(0, i0, i0, nb), T.block(i0, 0, nb, nc), 1.0,
-                     T.block(0, 0, i0, nc));
-        }
+        upper_tri_solve_inplace(ctx, S11, T);
     }
     if (dmax / dmin > 1e12) {
         if (nc > 0) {

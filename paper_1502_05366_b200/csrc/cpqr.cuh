@@ -28,4 +28,8 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
 // Throws NumericalError on a zero diagonal.  Returns `clamped`.
 bool upper_tri_solve(Context& ctx, const DMat& S11, const DMat& S12, const DMat& T);
 
+// T (k x nc) <- S11^{-1} T for upper-triangular S11, blocked on DMMA (no
+// clamp, no diagonal check: a zero pivot leaves inf/NaN in T).
+void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T);
+
 }  // namespace rlra_b200

@@ -127,7 +127,7 @@ void finish_qr_bt(Context& ctx, const DMat& Q, const DMat& Bt, int k, const DMat
     DMatBuf R(ctx, l, l), Uh(ctx, l, l), Vh(ctx, l, l);
     Buf s(ctx, sizeof(double) * l);
     orth_inplace(ctx, Bt, &R.m);                       // compact_qr(bt)
-    small_svd_tall(ctx, R, Uh, s.d(), Vh);             // small_svd(f.r)
+    small_svd_tall(ctx, R, Uh, s.d(), Vh, true);       // small_svd(f.r)
     GemmTag tag(ctx, "gemm_lift");
     gemm(ctx, Op::N, Op::N, 1.0, Q, Vh.m.block(0, 0, l, k), 0.0, U);   // (Q*Vhat)(:,1:k)
     gemm(ctx, Op::N, Op::N, 1.0, Bt, Uh.m.block(0, 0, l, k), 0.0, V);  // (Qhat*Uhat)(:,1:k)

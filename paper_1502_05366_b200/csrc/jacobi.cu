@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <string>
 
+#include "cpqr.cuh"
+#include "gemm.cuh"
 #include "jacobi.cuh"
 #include "reduce.cuh"
 
@@ -455,6 +457,7 @@ struct GramJacArgs {
     unsigned* vtick;
     unsigned* vdone;
     unsigned* tasks;  // sgram: [sweep cap] visit counters (zeroed per call)
+    int skip_v;       // sgram: rotate W only (V recovered afterwards as R^{-1} W, see small_svd_tall)
 };
 
 // ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
@@ -1877,19 +1880,24 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             if (t == 0) {
                                 s_tick[0] = __ldcg(a.vtick + bI);
                                 s_tick[1] = __ldcg(a.vtick + bJ);
-                                __stcg(a.vtick + bI, s_tick[0] + 1u);
-                                __stcg(a.vtick + bJ, s_tick[1] + 1u);
+                                if (!a.skip_v) {
+                                    __stcg(a.vtick + bI, s_tick[0] + 1u);
+                                    __stcg(a.vtick + bJ, s_tick[1] + 1u);
+                                }
                                 __stcg(a.mod + bI, R + 1u);
                                 __stcg(a.mod + bJ, R + 1u);
                                 atomicAdd(a.counters + 2, 1ull);
                                 __threadfence();
                                 jb_publish(a.ver + bI, R + 1);
                                 jb_publish(a.ver + bJ, R + 1);
-                                jb_wait_at_least(a.vdone + bI, s_tick[0]);
-                                jb_wait_at_least(a.vdone + bJ, s_tick[1]);
-                                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                                if (!a.skip_v) {
+                                    jb_wait_at_least(a.vdone + bI, s_tick[0]);
+                                    jb_wait_at_least(a.vdone + bJ, s_tick[1]);
+                                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                                }
                             }
                             __syncthreads();
+                            if (a.skip_v) break;  // W only: the ring is empty (every W chunk consumed)
                             kend = 2 * ncw + ncv;
                             for (; qn - qu < unsigned(kSNST - 1) && kin < kend; ++qn, ++kin) {
                                 issue();
@@ -1929,7 +1937,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                         }
                     }
                     __syncthreads();
-                    if (t == 0) {
+                    if (t == 0 && !a.skip_v) {
                         __threadfence();
                         jb_publish(a.vdone + bI, s_tick[0] + 1u);
                         jb_publish(a.vdone + bJ, s_tick[1] + 1u);
@@ -2155,7 +2163,75 @@ bool launch_cgram(Context& ctx, const CGramArgs& c, size_t smem) {
     return true;
 }
 
-void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& Vout) {
+// E = V^T V - I over the upper triangle (E from an upper-tiles-only Gram):
+// the diagonal shifted in place, per-CTA max |E_ij| (NaN counts as infinite)
+__global__ void orth_defect_kernel(double* E, int64_t lde, int n, double* part) {
+    __shared__ double red[256];
+    double mx = 0.0;
+    for (int j = blockIdx.x; j < n; j += gridDim.x)
+        for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+            double e = E[i + int64_t(j) * lde];
+            if (i == j) {
+                e -= 1.0;
+                E[i + int64_t(j) * lde] = e;
+            }
+            const double a = fabs(e);
+            mx = (a == a) ? fmax(mx, a) : INFINITY;
+        }
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// V from the rotated W of an upper-triangular square R: the one-sided
+// rotations keep W = R V, so V = R^{-1} W (blocked back substitution on
+// DMMA).  This is accurate when R's column-scaled condition is modest (the
+// QR-preconditioned Jacobi SVD of Drmac-Veselic; R-hat of a QB or rsvd is
+// graded by construction), so it is verified, not assumed: accepted when
+// max|V^T V - I| <= kVsolveTol; a defect above kVsolveExact (the level the
+// accumulated rotations reach at l ~ 10^4: 1.6e-13 at C2) gets one
+// Newton-Schulz step V <- V - V E / 2, taking it to O(E^2) + rounding.  Returns false
+// (V garbage) when rejected; the caller re-runs the sweeps accumulating V.
+constexpr double kVsolveTol = 1e-11, kVsolveExact = 1e-12;
+bool vsolve_from_r(Context& ctx, const DMat& Rm, const DMat& W, const DMat& V, double* defect) {
+    const int n = int(Rm.rows);
+    ProfScope prof(ctx, "svd_vsolve", n, n, 0, 0.0);
+    copy_mat(ctx, W, V);
+    upper_tri_solve_inplace(ctx, Rm, V);
+    DMatBuf E(ctx, n, n);
+    GemmOpts sy;
+    sy.upper_tiles_only = true;
+    gemm(ctx, Op::T, Op::N, 1.0, V, V, 0.0, E, sy);
+    const int blocks = std::min(n, ctx.num_sms);
+    Buf part(ctx, sizeof(double) * blocks);
+    orth_defect_kernel<<<blocks, 256, 0, ctx.stream>>>(E.m.p, E.m.ld, n, part.d());
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+    std::vector<double> h(blocks);
+    RLRA_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * blocks, cudaMemcpyDeviceToHost, ctx.stream));
+    RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    double mx = 0.0;
+    for (double v : h) mx = (v == v) ? std::max(mx, v) : INFINITY;
+    *defect = mx;
+    // RLRA_SVD_VSOLVE_TOL overrides the acceptance bound (a negative value
+    // rejects every solve: the fallback's test hook)
+    static const double tol = std::getenv("RLRA_SVD_VSOLVE_TOL") ? std::atof(std::getenv("RLRA_SVD_VSOLVE_TOL"))
+                                                                 : kVsolveTol;
+    if (!(mx <= tol)) return false;
+    static const bool force_ns = std::getenv("RLRA_SVD_VSOLVE_NS") != nullptr;  // test hook
+    if (mx <= kVsolveExact && !force_ns) return true;  // already as orthonormal as accumulated rotations
+    symmetrize_upper(ctx, E);
+    DMatBuf V0(ctx, n, n);
+    copy_mat(ctx, V, V0);
+    gemm(ctx, Op::N, Op::N, -0.5, V0, E, 1.0, V);
+    return true;
+}
+
+void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& Vout, bool upper_tri) {
     const int m = int(A.rows), n = int(A.cols);
     if (n == 0) return;
     ProfScope prof(ctx, "small_svd", m, n, 0, 0.0);
@@ -2302,6 +2378,18 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
                                            int(kSGramSmem)));
             attr = true;
         }
+        // A = R-hat (upper triangular, square): the sweeps rotate W only and
+        // V comes from R^{-1} W afterwards (vsolve_from_r) — a rotating
+        // visit's V_p J is 39 % of its flops; RLRA_SVD_VSOLVE=0 keeps V
+        // accumulated.  A rejected solve re-runs the sweeps with V.
+        static const bool vsolve_on = !std::getenv("RLRA_SVD_VSOLVE") || std::atoi(std::getenv("RLRA_SVD_VSOLVE")) != 0;
+        bool skip_v = upper_tri && vsolve_on && m == n;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+        if (attempt) {
+            copy_mat(ctx, A, W);
+            eye_mat(ctx, V);
+            RLRA_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 8, ctx.stream));
+        }
         GramJacArgs g{};
         g.bar = ctx.gbar;
         g.W = W.m.p;
@@ -2312,6 +2400,7 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.ldv = V.m.ld;
         g.nb = ceil_div(n, kSGB) + (ceil_div(n, kSGB) & 1);
         g.flags = flags.i();
+        g.skip_v = skip_v ? 1 : 0;
         Buf verb(ctx, sizeof(unsigned) * g.nb);
         RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
         g.ver = static_cast<unsigned*>(verb.p);
@@ -2336,7 +2425,16 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
             unsigned long long h[3];
             RLRA_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
             RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-            std::fprintf(stderr, "sgram: %llu visits, %llu skipped (clean), %llu rotating\n", h[0], h[1], h[2]);
+            std::fprintf(stderr, "sgram: %llu visits, %llu skipped (clean), %llu rotating%s\n", h[0], h[1], h[2],
+                         skip_v ? " (W only)" : "");
+        }
+        if (!skip_v) break;
+        double defect = 0.0;
+        const bool ok = vsolve_from_r(ctx, A, W.m, V.m, &defect);
+        if (std::getenv("RLRA_JACOBI_STATS"))
+            std::fprintf(stderr, "sgram: V = R^-1 W, max|V^T V - I| = %.3e (%s)\n", defect, ok ? "accepted" : "rejected");
+        if (ok) break;
+        skip_v = false;
         }
     } else if (forced != 4 && n > 2 * kGB) {
         // columns too long for shared memory: Gram block Jacobi (32-column blocks)

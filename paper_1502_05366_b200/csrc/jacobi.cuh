@@ -16,7 +16,10 @@ namespace rlra_b200 {
 
 // A (m x n, m >= n) -> U (m x n), sigma (n, device), V (n x n).  A is not
 // modified.  Throws ConvergenceError after 60 sweeps.
-void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V);
+// upper_tri: A is square upper triangular (the R-hat of finish_qr_bt); the
+// streaming kernel may then recover V as A^{-1} W (verified, jacobi.cu).
+void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, const DMat& V,
+                    bool upper_tri = false);
 
 // Raises the convergence errors small_svd_tall deferred to the end of the
 // API call (ctx.svd_pending); called by the C-ABI after every entry point.
