@@ -2,6 +2,8 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <unistd.h>
+#include <cstring>
 #include <string>
 
 #include "cpqr.cuh"
@@ -458,7 +460,15 @@ struct GramJacArgs {
     unsigned* vdone;
     unsigned* tasks;  // sgram: [sweep cap] visit counters (zeroed per call)
     int skip_v;       // sgram: rotate W only (V recovered afterwards as R^{-1} W, see small_svd_tall)
+    // sgram, W only: each visit split into two row halves taken as separate
+    // tasks (2 CTAs per pair), partial Grams exchanged through xg
+    int halves;
+    double* xg;       // [2 generations][np slots][2 halves][kSXG] partial Grams (upper triangle)
+    unsigned* xstamp; // [2 np][2]: partial of round R written (R + 1)
+    unsigned* xack;   // [2 np][2]: partner's partial of round R read (R + 1)
+    volatile unsigned* dbg;  // RLRA_SGRAM_DEBUG: mapped host record of a wait that timed out (then trap)
 };
+
 
 // ---- bulk-copy / mbarrier / release-acquire helpers (bgram staging) ----
 __device__ __forceinline__ unsigned jb_smem(const void* p) {
@@ -488,6 +498,31 @@ __device__ __forceinline__ void jb_wait_at_least(const unsigned* p, unsigned v) 
     }
 }
 
+// a version/stamp wait that, in debug mode, records itself and traps after ~1 s
+__device__ __forceinline__ void sg_wait_dbg(const unsigned* p, unsigned v, volatile unsigned* dbg, unsigned code,
+                                            unsigned R, unsigned hh) {
+    if (!dbg) {
+        jb_wait_at_least(p, v);
+        return;
+    }
+    unsigned cur;
+    for (long long it = 0;; ++it) {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(p) : "memory");
+        if (cur >= v) return;
+        __nanosleep(128);
+        if (it > (1ll << 24)) {
+            dbg[0] = 1u;
+            dbg[1] = code;
+            dbg[2] = R;
+            dbg[3] = hh;
+            dbg[4] = blockIdx.x;
+            dbg[5] = cur;
+            dbg[6] = v;
+            __threadfence_system();
+            asm volatile("trap;");
+        }
+    }
+}
 __global__ void __launch_bounds__(256) gram_jacobi_kernel(GramJacArgs a) {
     extern __shared__ double gsm[];
     double(*G)[kGPitch] = reinterpret_cast<double(*)[kGPitch]>(gsm);
@@ -1635,6 +1670,10 @@ constexpr int kSCP = kSCR + 4;   // chunk pitch (== 4 mod 16), 16-byte aligned r
 constexpr int kSGP = kSC2 + 1;   // G / J pitch
 constexpr int kSJP = kSC2 + 4;   // J pitch for B fragments (== 4 mod 16)
 constexpr int kSPT = 7;          // tiles per partial-Gram reduction round (3 rounds of 7)
+constexpr int kSXG = kSC2 * (kSC2 + 1) / 2;  // packed upper triangle of a 48 x 48 partial Gram
+// packed row-major upper triangle: row i starts at sx_off(i) = i*48 - i(i-1)/2
+__device__ __forceinline__ int sx_off(int i) { return i * kSC2 - (i * (i - 1)) / 2; }
+
 constexpr size_t kSGramSmem = sizeof(double) * (size_t(kSNST) * kSC2 * kSCP + size_t(8) * kSPT * 64 +
                                                 3 * kSC2 * kSGP + kSC2 * kSJP + 2 * kSGB);
 
@@ -1652,6 +1691,14 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, lr = lane >> 2, lc = lane & 3;
     const int m = a.m, n = a.n, nb = a.nb, np = nb / 2;
     const int ncw = int(a.ldw / kSCR), ncv = int(a.ldv / kSCR);  // chunks of W / V columns
+    const int H = a.halves ? 2 : 1;  // tasks per visit (row halves)
+    auto prog = [&](unsigned code, unsigned task, unsigned R) {  // RLRA_SGRAM_DEBUG progress record
+        if (a.dbg && threadIdx.x == 0) {
+            a.dbg[16 + 4 * blockIdx.x] = code;
+            a.dbg[17 + 4 * blockIdx.x] = task;
+            a.dbg[18 + 4 * blockIdx.x] = R;
+        }
+    };
     volatile int* flags = a.flags;
     __shared__ int s_task;
     // ring counters (identical in every thread): qn chunks issued (one
@@ -1676,8 +1723,17 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 __syncthreads();
                 const int task = s_task;
                 __syncthreads();
-                if (task >= nb * np) break;
-                const int r = task / np, g = task % np;
+                prog(1, task, 0);
+                if (task >= nb * np * H) break;
+                const int hh = task % H;  // the row half this task covers (halves mode)
+                const int r = (task / H) / np, g = (task / H) % np;
+                // halves: chunks [cbeg, cbeg + nch) of the W rows; the two tasks
+                // of a visit are adjacent in the order, so a half waiting on its
+                // partner's partial Gram always has the partner held or next
+                const int nch2 = (ncw + 1) / 2;
+                const int cbeg = H == 2 ? hh * nch2 : 0;
+                const int nch = H == 2 ? min(ncw, cbeg + nch2) - cbeg : ncw;
+                unsigned* verv = a.ver + hh * nb;  // this half's block versions
                 const unsigned R = unsigned(sweep) * unsigned(nb) + unsigned(r);  // the visit's global round
                 const bool intra = r == nb - 1;
                 int bI = 2 * g, bJ = 2 * g + 1;
@@ -1688,34 +1744,47 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 }
                 auto gcol = [&](int c) { return c < kSGB ? bI * kSGB + c : bJ * kSGB + (c - kSGB); };
                 const int pid = intra ? nb * nb + g : bI * nb + bJ;
+                const int xslot = int(R & 1u) * np + g;  // partial-Gram slot (two generations)
                 if (t == 0) {
-                    jb_wait_at_least(a.ver + bI, R);
-                    jb_wait_at_least(a.ver + bJ, R);
+                    sg_wait_dbg(verv + bI, R, a.dbg, 1, R, hh);
+                    sg_wait_dbg(verv + bJ, R, a.dbg, 2, R, hh);
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the previous writers' stores
+                    // (halves: both tasks decide alike — clean and mod only change
+                    // after both halves' partial Grams were exchanged)
                     const unsigned c = __ldcg(a.clean + pid);
                     s_skip = c != 0u && c >= __ldcg(a.mod + bI) && c >= __ldcg(a.mod + bJ);
-                    atomicAdd(a.counters + 0, 1ull);
-                    if (s_skip) atomicAdd(a.counters + 1, 1ull);
+                    if (hh == 0) {
+                        atomicAdd(a.counters + 0, 1ull);
+                        if (s_skip) atomicAdd(a.counters + 1, 1ull);
+                    }
                 }
+                prog(2, 0, R);
                 __syncthreads();
                 if (s_skip) {
                     if (t == 0) {
-                        jb_publish(a.ver + bI, R + 1);
-                        jb_publish(a.ver + bJ, R + 1);
+                        if (H == 2) {
+                            // the slot's next user may write — but only once this
+                            // half's previous use of the slot (round R - 2) was read:
+                            // a skipped visit must not overtake it (acks stay monotone)
+                            if (R >= 2u) sg_wait_dbg(a.xack + 2 * xslot + hh, R - 1, a.dbg, 5, R, hh);
+                            jb_publish(a.xack + 2 * xslot + hh, R + 1);
+                        }
+                        jb_publish(verv + bI, R + 1);
+                        jb_publish(verv + bJ, R + 1);
                     }
                     continue;
                 }
                 // the visit's chunk sequence: [0, ncw) Gram of W, [ncw, 2 ncw)
                 // W for the apply, [2 ncw, 2 ncw + ncv) V for the apply (issued
                 // only once the pair's V blocks are current, see step 3)
-                int kend = 2 * ncw;
+                int kend = 2 * nch;
                 int kin = 0;  // next sequence position to issue
                 auto issue = [&]() {  // sequence position kin into stage qn % kSNST (all threads)
                     const int k = kin;
-                    const bool isv = k >= 2 * ncw;
+                    const bool isv = k >= 2 * nch;
                     const double* X = isv ? a.V : a.W;
                     const int64_t ld = isv ? a.ldv : a.ldw;
-                    const int row0 = (isv ? k - 2 * ncw : (k < ncw ? k : k - ncw)) * kSCR;
+                    const int row0 = (isv ? k - 2 * nch : cbeg + (k < nch ? k : k - nch)) * kSCR;
                     double* dst = Ring + (qn % kSNST) * (kSC2 * kSCP);
 #pragma unroll
                     for (int it = 0; it < kSC2 * kSCR / 2 / 256; ++it) {  // 16-byte pieces: 32 per column
@@ -1751,7 +1820,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     double acc[kSNT][2];
 #pragma unroll
                     for (int u = 0; u < kSNT; ++u) acc[u][0] = acc[u][1] = 0.0;
-                    for (int ch = 0; ch < ncw; ++ch) {
+                    for (int ch = 0; ch < nch; ++ch) {
                         consume([&](const double* Cb) {
 #pragma unroll
                             for (int h = 0; h < kSCR / 32; ++h) {
@@ -1790,6 +1859,46 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             G0[col * kSGP + row] = sum;
                         }
                         __syncthreads();
+                    }
+                    if (H == 2) {
+                        // exchange the halves' partial Grams (upper triangle,
+                        // row-major packed): wait until the slot's previous user
+                        // (round R - 2) read our last partial, write ours, then
+                        // read the partner's; G = P + P' is the same sum in both
+                        // halves (IEEE addition commutes), so both run the same steps
+                        double* mine = a.xg + (size_t(xslot) * 2 + hh) * kSXG;
+                        const double* theirs = a.xg + (size_t(xslot) * 2 + (1 - hh)) * kSXG;
+                        prog(3, 0, R);
+                        if (t == 0 && R >= 2u) {
+                            sg_wait_dbg(a.xack + 2 * xslot + (1 - hh), R - 1, a.dbg, 3, R, hh);
+                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        }
+                        __syncthreads();
+                        for (int e = t; e < kSC2 * kSC2; e += 256) {
+                            const int i = e / kSC2, j = e % kSC2;
+                            if (j >= i) __stcg(mine + sx_off(i) + (j - i), G0[i * kSGP + j]);
+                        }
+                        __syncthreads();
+                        prog(4, 0, R);
+                        if (t == 0) {
+                            __threadfence();
+                            jb_publish(a.xstamp + 2 * xslot + hh, R + 1);
+                            sg_wait_dbg(a.xstamp + 2 * xslot + (1 - hh), R + 1, a.dbg, 4, R, hh);
+                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        }
+                        __syncthreads();
+                        for (int e = t; e < kSC2 * kSC2; e += 256) {
+                            const int i = e / kSC2, j = e % kSC2;
+                            if (j < i) continue;
+                            const double v = G0[i * kSGP + j] + __ldcg(theirs + sx_off(i) + (j - i));
+                            G0[i * kSGP + j] = v;
+                            G0[j * kSGP + i] = v;
+                        }
+                        __syncthreads();
+                        if (t == 0) {
+                            __threadfence();
+                            jb_publish(a.xack + 2 * xslot + hh, R + 1);
+                        }
                     }
                 }
                 for (int e = t; e < kSC2 * kSC2; e += 256) J[(e / kSC2) * kSGP + e % kSC2] = (e / kSC2 == e % kSC2) ? 1.0 : 0.0;
@@ -1849,6 +1958,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                     }
                     __syncthreads();
                 }
+                prog(6, rot, R);
                 if (rot) {
                     if (t == 0) flags[sweep % 3] = 1;
                     for (int e = t; e < kSC2 * kSC2; e += 256) Jb[(e / kSC2) * kSJP + e % kSC2] = J[(e / kSC2) * kSGP + e % kSC2];
@@ -1870,7 +1980,7 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                         double* X = mat == 0 ? a.W : a.V;
                         const int64_t ld = mat == 0 ? a.ldw : a.ldv;
                         const int rows = mat == 0 ? m : n;
-                        const int nch = mat == 0 ? ncw : ncv;
+                        const int nchm = mat == 0 ? nch : ncv;
                         if (mat == 1) {
                             // W_p J is out: publish W now, so the blocks' next
                             // owners start their Grams while this CTA does V_p J.
@@ -1886,10 +1996,13 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                                 }
                                 __stcg(a.mod + bI, R + 1u);
                                 __stcg(a.mod + bJ, R + 1u);
-                                atomicAdd(a.counters + 2, 1ull);
+                                if (hh == 0) {
+                                    atomicAdd(a.counters + 2, 1ull);
+                                    if (a.phase_clk) atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk) + 2 * sweep + 1, 1ull);
+                                }
                                 __threadfence();
-                                jb_publish(a.ver + bI, R + 1);
-                                jb_publish(a.ver + bJ, R + 1);
+                                jb_publish(verv + bI, R + 1);
+                                jb_publish(verv + bJ, R + 1);
                                 if (!a.skip_v) {
                                     jb_wait_at_least(a.vdone + bI, s_tick[0]);
                                     jb_wait_at_least(a.vdone + bJ, s_tick[1]);
@@ -1898,14 +2011,14 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             }
                             __syncthreads();
                             if (a.skip_v) break;  // W only: the ring is empty (every W chunk consumed)
-                            kend = 2 * ncw + ncv;
+                            kend = 2 * nch + ncv;
                             for (; qn - qu < unsigned(kSNST - 1) && kin < kend; ++qn, ++kin) {
                                 issue();
                                 sg_commit();
                             }
                         }
-                        for (int ch = 0; ch < nch; ++ch) {
-                            const int k0 = ch * kSCR;
+                        for (int ch = 0; ch < nchm; ++ch) {
+                            const int k0 = ((mat == 0 ? cbeg : 0) + ch) * kSCR;
                             consume([&](const double* Cb) {
                                 double o[2][3][2];
 #pragma unroll
@@ -1952,12 +2065,19 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 if (t == 0 && !rot) {  // (a rotating visit published W before its V update)
                     __stcg(a.clean + pid, R + 1u);
                     __threadfence();
-                    jb_publish(a.ver + bI, R + 1);
-                    jb_publish(a.ver + bJ, R + 1);
+                    jb_publish(verv + bI, R + 1);
+                    jb_publish(verv + bJ, R + 1);
                 }
             }
         }
+        prog(8, sweep, 0);
         grid_sync(a.bar);
+        prog(9, sweep, 0);
+        if (a.phase_clk && blockIdx.x == 0 && t == 0) {  // RLRA_JACOBI_PHASES: sweep end times
+            unsigned long long tn;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+            a.phase_clk[2 * sweep] = (long long)tn;
+        }
         const int rotated = flags[sweep % 3];
         ++sweep;
         if (!rotated || n < 2) break;
@@ -2401,8 +2521,27 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.nb = ceil_div(n, kSGB) + (ceil_div(n, kSGB) & 1);
         g.flags = flags.i();
         g.skip_v = skip_v ? 1 : 0;
-        Buf verb(ctx, sizeof(unsigned) * g.nb);
-        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * g.nb, ctx.stream));
+        // W only: split every visit into two row-half tasks (RLRA_SGRAM_HALVES=0: one CTA per visit)
+        static const bool halves_on = !std::getenv("RLRA_SGRAM_HALVES") || std::atoi(std::getenv("RLRA_SGRAM_HALVES")) != 0;
+        g.halves = (skip_v && halves_on && ldw / kSCR >= 4) ? 1 : 0;
+        const int snp = g.nb / 2;
+        Buf xgb(ctx, g.halves ? sizeof(double) * size_t(4) * snp * kSXG : 8),
+            xsb(ctx, g.halves ? sizeof(unsigned) * size_t(8) * snp : 8);
+        if (g.halves) {
+            RLRA_CUDA(cudaMemsetAsync(xsb.p, 0, sizeof(unsigned) * size_t(8) * snp, ctx.stream));
+            g.xg = xgb.d();
+            g.xstamp = static_cast<unsigned*>(xsb.p);
+            g.xack = g.xstamp + 4 * snp;
+        }
+        static const bool sg_phases = std::getenv("RLRA_JACOBI_PHASES") != nullptr;
+        Buf swb(ctx, sg_phases ? sizeof(long long) * (2 * kOneSidedSweepCap + 2) : 8);
+        long long t_start = 0;
+        if (sg_phases) {
+            RLRA_CUDA(cudaMemsetAsync(swb.p, 0, sizeof(long long) * (2 * kOneSidedSweepCap + 2), ctx.stream));
+            g.phase_clk = reinterpret_cast<long long*>(swb.p);
+        }
+        Buf verb(ctx, sizeof(unsigned) * 2 * g.nb);  // halves: one version per (half, block)
+        RLRA_CUDA(cudaMemsetAsync(verb.p, 0, sizeof(unsigned) * 2 * g.nb, ctx.stream));
         g.ver = static_cast<unsigned*>(verb.p);
         const size_t nst = size_t(g.nb) + size_t(g.nb) * g.nb + g.nb / 2 + 2 * size_t(g.nb) + kOneSidedSweepCap;
         Buf stamps(ctx, sizeof(unsigned) * nst), cnt(ctx, sizeof(unsigned long long) * 4);
@@ -2414,6 +2553,14 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         g.vdone = g.vtick + g.nb;
         g.tasks = g.vdone + g.nb;
         g.counters = static_cast<unsigned long long*>(cnt.p);
+        static unsigned* dbg_host = nullptr;
+        if (std::getenv("RLRA_SGRAM_DEBUG")) {
+            if (!dbg_host) RLRA_CUDA(cudaHostAlloc(&dbg_host, 4096, cudaHostAllocMapped));
+            std::memset(dbg_host, 0, 4096);
+            unsigned* dp = nullptr;
+            RLRA_CUDA(cudaHostGetDevicePointer(&dp, dbg_host, 0));
+            g.dbg = dp;
+        }
         void* args[] = {&g};
         // visits are taken dynamically, so every SM can work (one CTA each):
         // CTAs beyond the np pair slots pick up the next round's ready pairs
@@ -2421,12 +2568,54 @@ void small_svd_tall(Context& ctx, const DMat& A, const DMat& U, double* sigma, c
         const int sgrid = sg_grid > 0 ? std::min(sg_grid, ctx.num_sms) : ctx.num_sms;
         RLRA_CUDA(cudaLaunchCooperativeKernel((void*)sgram_jacobi_kernel, dim3(sgrid), dim3(256), args, kSGramSmem,
                                               ctx.stream));
+        if (g.dbg) {
+            cudaError_t e = cudaErrorNotReady;
+            for (int it = 0; it < 2000 && e == cudaErrorNotReady; ++it) {
+                e = cudaStreamQuery(ctx.stream);
+                if (e == cudaErrorNotReady) usleep(5000);
+            }
+            if (e == cudaErrorNotReady) {
+                std::fprintf(stderr, "sgram debug: still running after 10 s; per-CTA (code task R):\n");
+                for (int b = 0; b < sgrid; ++b)
+                    std::fprintf(stderr, "%d:(%u %u %u) ", b, dbg_host[16 + 4 * b], dbg_host[17 + 4 * b], dbg_host[18 + 4 * b]);
+                std::fprintf(stderr, "\n");
+                if (g.halves) {
+                    cudaStream_t s2;
+                    cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+                    std::vector<unsigned> hx(8 * snp), hv(2 * g.nb);
+                    cudaMemcpyAsync(hx.data(), xsb.p, sizeof(unsigned) * hx.size(), cudaMemcpyDeviceToHost, s2);
+                    cudaMemcpyAsync(hv.data(), verb.p, sizeof(unsigned) * hv.size(), cudaMemcpyDeviceToHost, s2);
+                    cudaStreamSynchronize(s2);
+                    std::fprintf(stderr, "xstamp/xack per slot (s: st0 st1 ack0 ack1):");
+                    for (int q = 0; q < 2 * snp; ++q)
+                        std::fprintf(stderr, " %d:(%u %u %u %u)", q, hx[2 * q], hx[2 * q + 1], hx[4 * snp + 2 * q], hx[4 * snp + 2 * q + 1]);
+                    std::fprintf(stderr, "\nver half0/half1:");
+                    for (int b = 0; b < g.nb; ++b) std::fprintf(stderr, " %d:(%u %u)", b, hv[b], hv[g.nb + b]);
+                    std::fprintf(stderr, "\n");
+                }
+                std::fflush(stderr);
+                std::abort();
+            }
+            std::fprintf(stderr, "sgram debug: %s; record %u code %u R %u half %u block %u cur %u want %u\n",
+                         cudaGetErrorString(e), dbg_host[0], dbg_host[1], dbg_host[2], dbg_host[3], dbg_host[4],
+                         dbg_host[5], dbg_host[6]);
+        }
         if (std::getenv("RLRA_JACOBI_STATS")) {
             unsigned long long h[3];
             RLRA_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
             RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-            std::fprintf(stderr, "sgram: %llu visits, %llu skipped (clean), %llu rotating%s\n", h[0], h[1], h[2],
-                         skip_v ? " (W only)" : "");
+            std::fprintf(stderr, "sgram: %llu visits, %llu skipped (clean), %llu rotating%s%s\n", h[0], h[1], h[2],
+                         skip_v ? " (W only)" : "", g.halves ? " (row halves)" : "");
+        }
+        if (sg_phases) {
+            std::vector<long long> h(2 * kOneSidedSweepCap);
+            RLRA_CUDA(cudaMemcpyAsync(h.data(), swb.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
+            RLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+            (void)t_start;
+            std::fprintf(stderr, "sgram sweeps (end us, rotating visits):");
+            for (int sw = 0; sw < kOneSidedSweepCap && h[2 * sw]; ++sw)
+                std::fprintf(stderr, " [%d] %.0f %lld", sw, (h[2 * sw] - h[0]) * 1e-3, h[2 * sw + 1]);
+            std::fprintf(stderr, "\n");
         }
         if (!skip_v) break;
         double defect = 0.0;
