@@ -1093,6 +1093,39 @@ __global__ void trisolve_kernel(const double* S, int64_t lds, int k, const doubl
     }
 }
 
+// T (nb x nc, in place) <- S^{-1} T for an upper-triangular nb x nb block, nb
+// <= 64: S staged once per CTA in shared memory, one warp per right-hand side
+// with its column in registers (lane owns rows lane, lane + 32), the pivots
+// as reciprocals (the verified V = R^{-1} W solve; the ID's tri-solve keeps
+// trisolve_kernel's division, the reference's arithmetic)
+__global__ void __launch_bounds__(256) trisolve_reg_kernel(const double* S, int64_t lds, int nb, double* T,
+                                                           int64_t ldt, int nc) {
+    __shared__ double Ss[64][65];
+    __shared__ double rp[64];
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+        const int i = e % 64, j = e / 64;
+        Ss[i][j] = (i < nb && j < nb && i <= j) ? S[i + int64_t(j) * lds] : 0.0;
+    }
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) rp[i] = i < nb ? 1.0 / S[i + int64_t(i) * lds] : 0.0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + warp; c < nc; c += gridDim.x * wpb) {
+        double* col = T + int64_t(c) * ldt;
+        double b0 = lane < nb ? col[lane] : 0.0, b1 = lane + 32 < nb ? col[lane + 32] : 0.0;
+        for (int i = nb - 1; i >= 0; --i) {
+            const double xi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31) * rp[i];
+            if (lane == (i & 31)) {
+                if (i < 32) b0 = xi;
+                else b1 = xi;
+            }
+            if (lane < i) b0 -= Ss[lane][i] * xi;
+            if (lane + 32 < i) b1 -= Ss[lane + 32][i] * xi;
+        }
+        if (lane < nb) col[lane] = b0;
+        if (lane + 32 < nb) col[lane + 32] = b1;
+    }
+}
+
 __global__ void clamp_kernel(double* T, int64_t ldt, int k, int nc) {
     const int64_t tot = int64_t(k) * nc;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot;
@@ -1282,7 +1315,7 @@ CpqrResult pivoted_qr(Context& ctx, const DMat& A, int k, double tol, const DMat
     return r;
 }
 
-void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T) {
+void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T, bool fast) {
     // Blocked back substitution on DMMA: for the diagonal blocks from the
     // bottom up, T_I <- S_II^{-1} T_I (one warp per right-hand side, the
     // block's column in shared memory), then the rank-kTriNB update
@@ -1297,17 +1330,21 @@ void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T) {
         // T1 -= S12 T2 with K = k2 >= 256 (the rank-64 updates of the flat loop
         // ran at ~8 TFLOP/s), T1 <- S11^{-1} T1
         const int k1 = ((k / 2 + kTriNB - 1) / kTriNB) * kTriNB, k2 = k - k1;
-        upper_tri_solve_inplace(ctx, S11.block(k1, k1, k2, k2), T.block(k1, 0, k2, nc));
+        upper_tri_solve_inplace(ctx, S11.block(k1, k1, k2, k2), T.block(k1, 0, k2, nc), fast);
         gemm(ctx, Op::N, Op::N, -1.0, S11.block(0, k1, k1, k2), T.block(k1, 0, k2, nc), 1.0, T.block(0, 0, k1, nc));
-        upper_tri_solve_inplace(ctx, S11.block(0, 0, k1, k1), T.block(0, 0, k1, nc));
+        upper_tri_solve_inplace(ctx, S11.block(0, 0, k1, k1), T.block(0, 0, k1, nc), fast);
         return;
     }
     const size_t smem = sizeof(double) * size_t(kTriNB) * kWpb;
     const int blocks = std::max(1, std::min(ctx.num_sms * 4, ceil_div(nc, kWpb)));
     for (int i0 = ((k - 1) / kTriNB) * kTriNB; i0 >= 0; i0 -= kTriNB) {  // block rows aligned at 0
         const int nb = std::min(k, i0 + kTriNB) - i0;
-        trisolve_kernel<<<blocks, kWpb * 32, smem, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
-                                                                 T.p + i0, T.ld, nc, T.p + i0, T.ld);
+        if (fast)
+            trisolve_reg_kernel<<<blocks, kWpb * 32, 0, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
+                                                                     T.p + i0, T.ld, nc);
+        else
+            trisolve_kernel<<<blocks, kWpb * 32, smem, ctx.stream>>>(S11.p + i0 + int64_t(i0) * S11.ld, S11.ld, nb,
+                                                                     T.p + i0, T.ld, nc, T.p + i0, T.ld);
         RLRA_LAUNCH_CHECK();
         ++ctx.launches;
         if (i0 > 0)

@@ -30,6 +30,7 @@ bool upper_tri_solve(Context& ctx, const DMat& S11, const DMat& S12, const DMat&
 
 // T (k x nc) <- S11^{-1} T for upper-triangular S11, blocked on DMMA (no
 // clamp, no diagonal check: a zero pivot leaves inf/NaN in T).
-void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T);
+// fast: diagonal blocks by trisolve_reg_kernel (registers + reciprocal pivots).
+void upper_tri_solve_inplace(Context& ctx, const DMat& S11, const DMat& T, bool fast = false);
 
 }  // namespace rlra_b200

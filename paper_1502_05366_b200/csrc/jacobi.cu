@@ -2321,7 +2321,7 @@ bool vsolve_from_r(Context& ctx, const DMat& Rm, const DMat& W, const DMat& V, d
     const int n = int(Rm.rows);
     ProfScope prof(ctx, "svd_vsolve", n, n, 0, 0.0);
     copy_mat(ctx, W, V);
-    upper_tri_solve_inplace(ctx, Rm, V);
+    upper_tri_solve_inplace(ctx, Rm, V, true);
     DMatBuf E(ctx, n, n);
     GemmOpts sy;
     sy.upper_tiles_only = true;
