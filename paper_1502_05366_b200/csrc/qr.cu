@@ -742,6 +742,21 @@ void add_diag(Context& ctx, const DMat& G, double s) {
 // then CholQR2 on Y1; R = R3 R2 R1.  Used when plain CholQR2's Gram is too
 // ill-conditioned (e.g. B^T of the C2 QB, kappa ~ 1e7-1e8).  Returns false
 // when even this breaks down (exact rank deficiency), leaving Y untouched.
+// C = A B for upper-triangular n x n A and B: only the upper tiles are
+// formed (the k-range of each cut to the triangle of B), the strictly lower
+// triangle is written as zeros — the same values as the full product
+static void upper_product(Context& ctx, const DMat& A, const DMat& B, const DMat& C) {
+    const int n = int(C.rows);
+    GemmOpts o;
+    o.tri_b_upper = true;
+    o.upper_tiles_only = true;
+    gemm(ctx, Op::N, Op::N, 1.0, A, B, 0.0, C, o);
+    const int blocks = int(std::min<int64_t>(1024, std::max<int64_t>(1, (int64_t(n) * n + 255) / 256)));
+    zero_lower_kernel<<<blocks, 256, 0, ctx.stream>>>(C.p, C.ld, n);
+    RLRA_LAUNCH_CHECK();
+    ++ctx.launches;
+}
+
 static bool shifted_cholqr3(Context& ctx, const DMat& Y, const DMat* R) {
     const int m = int(Y.rows), n = int(Y.cols);
     Buf nrm(ctx, sizeof(double));
@@ -772,8 +787,8 @@ static bool shifted_cholqr3(Context& ctx, const DMat& Y, const DMat* R) {
     gemm(ctx, Op::N, Op::N, 1.0, Q2, R3i, 0.0, Y, tri);
     if (R) {
         DMatBuf T(ctx, n, n);
-        gemm(ctx, Op::N, Op::N, 1.0, G3, G2, 0.0, T, tri);   // R3 R2
-        gemm(ctx, Op::N, Op::N, 1.0, T, G, 0.0, *R, tri);    // (R3 R2) R1
+        upper_product(ctx, G3, G2, T);   // R3 R2
+        upper_product(ctx, T, G, *R);    // (R3 R2) R1
     }
     return true;
 }
@@ -814,10 +829,7 @@ QrResult orth_inplace(Context& ctx, const DMat& Y, const DMat* R) {
         return householder_qr(ctx, Y, R);
     }
     gemm(ctx, Op::N, Op::N, 1.0, Q1, R2i, 0.0, Y, tri);
-    if (R) {
-        // R = R2 * R1 (both upper): B = R1 upper triangular
-        gemm(ctx, Op::N, Op::N, 1.0, G2, G1, 0.0, *R, tri);
-    }
+    if (R) upper_product(ctx, G2, G1, *R);  // R = R2 R1
     return res;
 }
 
