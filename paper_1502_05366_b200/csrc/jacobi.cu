@@ -957,6 +957,12 @@ __device__ __forceinline__ void bgram_apply(const double* Xs, int P, int Mp, con
 __device__ __forceinline__ void jb_publish(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// a relaxed store for a publish that follows a gpu-scope fence of the same
+// thread (the fence already orders every earlier write and every write it
+// observed before it)
+__device__ __forceinline__ void jb_store_relaxed(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Gram G0 = Xs^T Xs of a staged pair (C2 columns, pitch P, Mp rows) on DMMA:
 // warp w sums rows [w*Mp/8, (w+1)*Mp/8) for the upper 8x8 tiles (a tile's two
@@ -1721,8 +1727,9 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
             {
                 if (t == 0) s_task = int(atomicAdd(a.tasks + sweep, 1u));
                 __syncthreads();
+                // (every path passes the s_skip barrier below before thread 0
+                // can write s_task again, so no second barrier is needed here)
                 const int task = s_task;
-                __syncthreads();
                 prog(1, task, 0);
                 if (task >= nb * np * H) break;
                 const int hh = task % H;  // the row half this task covers (halves mode)
@@ -1769,8 +1776,10 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                             if (R >= 2u) sg_wait_dbg(a.xack + 2 * xslot + hh, R - 1, a.dbg, 5, R, hh);
                             jb_publish(a.xack + 2 * xslot + hh, R + 1);
                         }
-                        jb_publish(verv + bI, R + 1);
-                        jb_publish(verv + bJ, R + 1);
+                        // nothing written: the fence after the version waits orders
+                        // the predecessors' W writes before these stores
+                        jb_store_relaxed(verv + bI, R + 1);
+                        jb_store_relaxed(verv + bJ, R + 1);
                     }
                     continue;
                 }
@@ -2001,8 +2010,8 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                                     if (a.phase_clk) atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk) + 2 * sweep + 1, 1ull);
                                 }
                                 __threadfence();
-                                jb_publish(verv + bI, R + 1);
-                                jb_publish(verv + bJ, R + 1);
+                                jb_store_relaxed(verv + bI, R + 1);
+                                jb_store_relaxed(verv + bJ, R + 1);
                                 if (!a.skip_v) {
                                     jb_wait_at_least(a.vdone + bI, s_tick[0]);
                                     jb_wait_at_least(a.vdone + bJ, s_tick[1]);
@@ -2065,8 +2074,8 @@ __global__ void __launch_bounds__(256, 1) sgram_jacobi_kernel(GramJacArgs a) {
                 if (t == 0 && !rot) {  // (a rotating visit published W before its V update)
                     __stcg(a.clean + pid, R + 1u);
                     __threadfence();
-                    jb_publish(verv + bI, R + 1);
-                    jb_publish(verv + bJ, R + 1);
+                    jb_store_relaxed(verv + bI, R + 1);
+                    jb_store_relaxed(verv + bJ, R + 1);
                 }
             }
         }
