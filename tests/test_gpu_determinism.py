@@ -11,7 +11,8 @@ scheduling), and requires bit-identical results:
   * bgram_jacobi_kernel (V helpers, point-to-point block versions), the
     cluster-resident cgram_jacobi_kernel (st.async exchange, split cluster
     barriers, V replay), the streaming sgram_jacobi_kernel (cp.async ring,
-    clean-pair skips, dynamically taken visits),
+    clean-pair skips, dynamically taken visits; and its W-only row-half
+    visits with partial Grams exchanged between CTAs),
   * cpqr_step_kernel and cpqr_res_kernel (one grid barrier per pivot step;
     register and shared-memory resident columns), the cooperative
     Cholesky (chol_inv_coop_kernel) inside CholQR2,
@@ -131,4 +132,27 @@ def test_sgram_jacobi_bit_identical_across_runs():
     out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RLRA_SVD_KERNEL": "sgram"},
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
+    assert out.stdout.strip().splitlines()[-1] == "SAME"
+
+
+def test_sgram_row_half_visits_bit_identical_across_runs():
+    """The W-only streaming Jacobi on an rsvd's R-hat with every visit split
+    into two row-half tasks (partial Grams exchanged through two-generation
+    slots, per-half block versions, monotone acknowledgements): repeated
+    rsvd_v2 calls under a perturbed schedule give bit-identical U, sigma, V,
+    and the log shows the row-half path ran (forced sgram at l = 610: 10 row
+    chunks, so both halves stream five)."""
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r); "
+            "import paper_1502_05366_b200 as R; from helpers import make_test_matrix; "
+            "a = make_test_matrix(1500, 1200, np.exp(-np.arange(1200) / 150.0), seed=68); "
+            "e = R.Engine(0); e2 = R.Engine(0); rs = np.random.default_rng(2); outs = []\n"
+            "for k in range(6):\n"
+            "    e2.matmul(rs.standard_normal((500 + 50 * k, 300)), rs.standard_normal((300, 250)))\n"
+            "    outs.append(e.rsvd_v2(a, 600, 10, 2, 1, rng=R.Rng(12345)))\n"
+            "ok = all(all(np.array_equal(x, y) for x, y in zip(outs[0], o)) for o in outs[1:])\n"
+            "print('SAME' if ok else 'DIFF')" % (ROOT, os.path.join(ROOT, "tests")))
+    env = {**os.environ, "RLRA_SVD_KERNEL": "sgram", "RLRA_JACOBI_STATS": "1"}
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "(row halves)" in out.stderr and "accepted" in out.stderr, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == "SAME"
